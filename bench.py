@@ -1,0 +1,362 @@
+"""Benchmark: sparse-coded patches/s of the STMP encoding path on B200.
+
+Contract:
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--method omp|mp]
+                  [--selector tree|exact] [--impl ours|reference]
+One process per GPU (torchrun for N>1).  A step is one encode of the config's
+whole patch batch (config 1 by default: 1,048,576 patches, 16384x64 dictionary,
+tree 32x32x16, OMP K=8), inputs already resident in HBM.  Weak scaling: every
+rank encodes its own N patches (independent patch shards, no data-path
+collective); timing is the max over ranks of device-event time.
+
+`--impl reference` times the reference's own CPU algorithm (the oracle port in
+oracle/, the reference package cannot travel to the GPU box) on all host cores
+over a bounded sample of the same workload.
+"""
+
+import os
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1412_0680_b200 import roofline as RL  # noqa: E402
+from paper_1412_0680_b200 import tree as T  # noqa: E402
+from paper_1412_0680_b200 import workloads as W  # noqa: E402
+
+METRIC = "sparse-coded patches/sec (tree-MP/OMP) on 1 B200; % of HBM/tensor roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--method", default="omp", choices=["omp", "mp"])
+    ap.add_argument("--selector", default="tree", choices=["tree", "exact"])
+    ap.add_argument("--patches", type=int, default=0, help="override N per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def tree_path(cid):
+    for p in (os.path.join(ROOT, "tests", "golden", "trees", f"c{cid}.npz"),
+              os.path.join(ROOT, "artifacts", "trees", f"c{cid}.npz")):
+        if os.path.exists(p):
+            return p
+    raise FileNotFoundError(f"no shipped tree structure for config {cid}")
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks sampler
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.rows = []
+        self.proc = None
+        self.index = index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle port)
+
+_POOL_STATE = {}
+
+
+def _cpu_worker(args):
+    lo, hi = args
+    from oracle import stmp_oracle as O
+    st = _POOL_STATE
+    sel = (O.tree_selector(st["otree"], st["a64"], st["alpha"]) if st["otree"] is not None
+           else O.exact_selector(st["a64"]))
+    for x in st["X"][lo:hi]:
+        O.encode_one(sel, st["a64"], x, st["K"], st["method"])
+    return hi - lo
+
+
+def cpu_rate(wl, flat, X, K, method, selector, seconds, cores=None):
+    """Time the reference CPU algorithm (oracle port, f64 NumPy, per-patch loop as
+    in pkg/src/stmp/pipelines.py:199-206) on a fork pool of all host cores."""
+    from oracle import stmp_oracle as O
+    cores = cores or len(os.sched_getaffinity(0))
+    a64 = wl.atoms.astype(np.float64)
+    otree = O.OracleTree.from_flat(flat) if selector == "tree" else None
+    _POOL_STATE.update(a64=a64, otree=otree, alpha=wl.cfg.alpha, K=K, method=method, X=X)
+    # calibrate on one core
+    t0 = time.perf_counter()
+    probe = 16 if selector == "tree" else 2
+    _cpu_worker((0, probe))
+    per = (time.perf_counter() - t0) / probe
+    sample = int(min(len(X), max(cores * 4, seconds * cores / per)))
+    bounds = [(s, min(s + max(1, sample // (cores * 4)), sample)) for s in
+              range(0, sample, max(1, sample // (cores * 4)))]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_worker, bounds[:1])  # warm the workers
+        t0 = time.perf_counter()
+        done = sum(pool.map(_cpu_worker, bounds))
+        wall = time.perf_counter() - t0
+    return done / wall, cores, done, wall
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------ main
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    cfg = W.CONFIGS[args.config]
+    exhaustive = args.selector == "exact"
+    N = args.patches or (cfg.N if not exhaustive else min(cfg.N, 65536))
+    workload = f"{cfg.name}/{'tree' if not exhaustive else 'exhaustive'}-{args.method.upper()}"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        wl = W.make_dictionary(cfg)
+        flat = T.load_structure(tree_path(cfg.cid), wl.atoms) if not exhaustive else None
+        sample_rows = min(N, 65536 if cfg.n <= 256 else 4096)
+        X = W.make_patches(wl, sample_rows)
+        # size each step to ~3 s of the whole CPU so the run ends within minutes
+        rate0, cores, _, _ = cpu_rate(wl, flat, X, cfg.K, args.method, args.selector, 3.0)
+        per_step = int(max(cores, min(len(X), rate0 * 3.0)))
+        times = []
+        for step in range(args.warmup + args.steps):
+            r, cores, done, wall = cpu_rate(wl, flat, X[:per_step], cfg.K, args.method,
+                                            args.selector, 1e9)
+            if step >= args.warmup:
+                times.append((done, wall))
+        done = sum(d for d, _ in times)
+        wall = sum(w for _, w in times)
+        value = done / wall
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": "patches/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * wall / max(1, len(times)), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload, "patches_per_step": per_step, "K": cfg.K,
+                       "dictionary": [cfg.m, cfg.n], "branching": list(cfg.branching)},
+            "cpu_baseline": {"value": value, "unit": "patches/s", "cores": cores, "kind": "port",
+                             "sample": f"{per_step} patches per step (prefix of the config batch), "
+                                       f"oracle port of the reference (f64 NumPy per-patch loop), "
+                                       f"{cores}-process fork pool on {cpu_model()}"},
+            "e2e": {"value": value, "unit": "patches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import paper_1412_0680_b200 as P
+    from paper_1412_0680_b200 import build
+    build.build()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    wl = W.make_dictionary(cfg)
+    flat = T.load_structure(tree_path(cfg.cid), wl.atoms)
+    chunk_start = rank * (-(-N // cfg.chunk) * cfg.chunk)  # distinct patch shard per rank
+    X_host = W.make_patches(wl, N, start=chunk_start)
+    sel = P.ExactSelector(wl.atoms) if exhaustive else P.TreeSelector(flat, wl.atoms, cfg.alpha)
+    Xd = torch.as_tensor(X_host).cuda()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return P.encode(sel, Xd, cfg.K, method=args.method)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    e0.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    # keep sampling a little longer if the timed region was short
+    total_ms = e0.elapsed_time(e1)
+    per_launch_ms = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([total_ms], device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    clocks = sampler.stop()
+
+    # end-to-end through the host-buffer C ABI (pinned host memory)
+    e2e = None
+    if not args.no_e2e:
+        Xp = torch.from_numpy(X_host).pin_memory()
+        outs = dict(idx=torch.empty((N, cfg.K), dtype=torch.int32).pin_memory().numpy(),
+                    coef=torch.empty((N, cfg.K), dtype=torch.float32).pin_memory().numpy(),
+                    count=torch.empty(N, dtype=torch.int32).pin_memory().numpy(),
+                    resnorm=torch.empty(N, dtype=torch.float32).pin_memory().numpy(),
+                    ip=torch.empty((N, 2), dtype=torch.int32).pin_memory().numpy())
+        Xn = Xp.numpy()
+        for _ in range(2):
+            P.encode_host(sel, Xn, cfg.K, args.method, out=outs)
+        e2e_steps = max(3, min(args.steps, 10))
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            P.encode_host(sel, Xn, cfg.K, args.method, out=outs)
+        el = torch.tensor([time.perf_counter() - t0], device="cuda")
+        if dist:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        h2d = N * cfg.n * 4
+        d2h = N * (cfg.K * 8 + 4 + 4 + 8)
+        e2e = {"value": world * N * e2e_steps / float(el.item()), "unit": "patches/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "stmp_encode_host (C ABI, pinned host buffers, chunked H2D/encode/D2H)"}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    value = world * N * args.steps / (total_ms / 1e3)
+    launch_ms = statistics.mean(per_launch_ms)
+    peaks = {}
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        peaks = json.load(open(pk))
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    rm = RL.model(cfg, N=N, method=args.method, exhaustive=exhaustive, hbm_gbs=hbm)
+    if rm["bound"] == "hbm":
+        achieved = rm["bytes_per_patch"] * N / (launch_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None}
+    else:
+        bf16 = float(peaks.get("bf16_tflops", 1590.0))
+        achieved = rm["flops_per_patch"] * N / (launch_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
+                "frac": achieved / bf16, "traffic": None}
+    roof.update({
+        "peak_source": "MEASURED_PEAKS.json" if peaks else "B200_PROFILING.md fallback",
+        "model": "SURVEY §8d per-patch algorithmic bytes/FLOPs x patches per launch / mean launch time",
+        "bytes_per_patch": rm["bytes_per_patch"], "flops_per_patch": rm["flops_per_patch"],
+        "launch_ms": launch_ms,
+        "fp32_simt_frac": rm["flops_per_patch"] * N / (launch_ms / 1e3) / 1e12 / RL.FP32_SIMT_TFLOPS,
+        "kernel": "encode_fused_kernel",
+    })
+    traffic_file = os.path.join(ROOT, "profiles", f"traffic_c{cfg.cid}.json")
+    if os.path.exists(traffic_file):
+        tr = json.load(open(traffic_file))
+        if tr.get("patches") == N and tr.get("method") == args.method and tr.get("selector") == args.selector:
+            roof["traffic"] = tr.get("bytes_per_launch")
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        rate, cores, done, wall = cpu_rate(wl, flat, X_host[:65536 if cfg.n <= 256 else 4096],
+                                           cfg.K, args.method, args.selector, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "patches/s", "cores": cores, "kind": "port",
+               "sample": f"{done} patches (prefix of the batch) in {wall:.1f}s, oracle port of the "
+                         f"reference (f64 NumPy per-patch loop), {cores}-process pool on {cpu_model()}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "patches/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded, BASELINE.json config shapes/distributions)",
+        "config": {"workload": workload, "patches_per_gpu": N, "dictionary": [cfg.m, cfg.n],
+                   "branching": list(cfg.branching), "K": cfg.K, "method": args.method,
+                   "parallelism": f"patch shards x{world}",
+                   "l2": f"inputs {N * cfg.n * 4 / 1e6:.0f} MB vs 126 MB L2 (no explicit flush)"},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "clocks": clocks,
+        "roofline_model_patches_per_s": rm["patches_per_s_roof"],
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

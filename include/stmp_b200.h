@@ -1,0 +1,122 @@
+/*
+ * stmp_b200.h -- C ABI of the B200-native Shallow Tree Matching Pursuit
+ * encoding path (arXiv 1412.0680).
+ *
+ * The reference (package `stmp`, pure Python + NumPy) has no FFI: its plugin
+ * seam is the duck-typed selector protocol consumed by `matching_pursuit`
+ * (pkg/src/stmp/pursuit.py:194-221): an object with `.dictionary` and
+ * `.select(r, counter) -> (index, signed_score)`.  Each entry point below
+ * names the reference interface it replaces; INTEGRATION.md shows the
+ * ctypes binding a maintainer adds on the reference side.
+ *
+ * Conventions:
+ *   - plain pointers and sizes only; `stream` is a cudaStream_t (NULL = legacy default);
+ *   - every encode/select buffer is a DEVICE pointer owned by the caller; the
+ *     library owns only the immutable dictionary / tree handles;
+ *   - all device work is asynchronous on `stream`;
+ *   - status codes map to the reference's exceptions:
+ *       STMP_OK 0, STMP_EINVAL 1 -> ValueError, STMP_ESTALE 2 -> StaleTreeError,
+ *       STMP_ECUDA 3 -> RuntimeError; message via stmp_last_error() (thread-local);
+ *   - there is no CPU fallback: without a usable sm_100 device every device
+ *     entry point returns STMP_ECUDA.
+ */
+#ifndef STMP_B200_H
+#define STMP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STMP_OK 0
+#define STMP_EINVAL 1
+#define STMP_ESTALE 2
+#define STMP_ECUDA 3
+
+#define STMP_METHOD_MP 0      /* matching_pursuit step update, pursuit.py:219-220            */
+#define STMP_METHOD_OMP 1     /* omp_refit per iteration (pursuit.py:235-250)     */
+#define STMP_METHOD_SELECT 2  /* one selection per row, no update: stmp_select/exact_select   */
+
+#define STMP_MAX_K 128
+
+typedef struct stmp_dict stmp_dict;
+typedef struct stmp_tree stmp_tree;
+
+/* Library identification and error text (thread-local, valid until the next call). */
+const char* stmp_version(void);
+const char* stmp_last_error(void);
+
+/* FNV-1a 64 over a byte buffer, continuing from `state` (pass
+ * STMP_FNV_OFFSET to start).  Replaces the pure-Python `fnv1a64` +
+ * `Dictionary.fingerprint` (pkg/src/stmp/dictionary.py:32-37,105-109).     */
+#define STMP_FNV_OFFSET 0xCBF29CE484222325ULL
+uint64_t stmp_fnv1a64(const void* data, size_t len, uint64_t state);
+
+/* Upload a dictionary: m unit-norm atoms of dimension n, atom-major f32
+ * (the layout of `Dictionary.atoms`, pkg/src/stmp/dictionary.py:68-100).
+ * `atoms` is a host pointer when atoms_on_device == 0, else a device pointer.
+ * `fingerprint` is the FNV-1a of the f32 payload (stmp_fnv1a64) and binds
+ * trees to this dictionary.  Replaces `Dictionary.scoring_atoms`.           */
+int stmp_dict_create(const float* atoms, int64_t m, int32_t n, int32_t atoms_on_device,
+                     uint64_t fingerprint, void* stream, stmp_dict** out);
+void stmp_dict_free(stmp_dict* d);
+int stmp_dict_info(const stmp_dict* d, int64_t* m, int32_t* n, int32_t* ld, uint64_t* fingerprint);
+
+/* Upload a flattened cluster tree (host arrays, BFS order):
+ *   levels L = len(branching); internal nodes have global ids in BFS order,
+ *   level_offsets[L+2] delimits depths 0..L; child_begin/child_count per
+ *   internal node index the next depth's ids (depth < L) or leaf_atom
+ *   (depth L); centroids is num_internal x n f32.
+ * Replaces `ClusterTree`/`TreeNode.child_matrix`/`child_atom_indices`
+ * (pkg/src/stmp/clustering.py:217-264).  Returns STMP_ESTALE when
+ * `fingerprint` differs from the dictionary's (pursuit.py:181-185).        */
+int stmp_tree_create(const stmp_dict* d, int32_t levels, const int32_t* branching,
+                     const int64_t* level_offsets, const int32_t* child_begin,
+                     const int32_t* child_count, const float* centroids, int64_t num_leaves,
+                     const int32_t* leaf_atom, uint64_t fingerprint, void* stream,
+                     stmp_tree** out);
+void stmp_tree_free(stmp_tree* t);
+
+/* Batch encode N patches X[N x ldx] (f32, device).
+ *   tree == NULL selects exhaustively (ExactSelector, pursuit.py:165-172),
+ *   otherwise greedy tree descent (TreeSelector, pursuit.py:175-191); the
+ *   GPU supports greedy alpha only (retained_count(alpha, k_i) == 1 at every
+ *   level), anything else is STMP_EINVAL.
+ *   method: STMP_METHOD_MP / STMP_METHOD_OMP / STMP_METHOD_SELECT.
+ *   tol_abs < 0 means the reference default 1e-6 * ||x|| (pursuit.py:207-209).
+ * Outputs (device; optional ones may be NULL):
+ *   idx[N*K] int32 selected atoms in selection order (-1 padded),
+ *   coef[N*K] f32 (MP: step scores; OMP: final refit; SELECT: signed score),
+ *   count[N] int32 atoms selected, resnorm[N] f32 final ||r||,
+ *   path[N*K*L] int32 BFS node id kept at each level (optional),
+ *   ip[N*2] int32 {inner products, centroid inner products} per patch
+ *   (ScoreCounter, pkg/src/stmp/dictionary.py:40-65) (optional).
+ * Replaces `matching_pursuit` (pursuit.py:194-221) driven by the batch loop
+ * of `_code_patches` (pkg/src/stmp/pipelines.py:180-217).
+ * Workspace: stmp_encode_workspace() bytes of device memory, caller-owned.   */
+size_t stmp_encode_workspace(const stmp_dict* d, const stmp_tree* t, int64_t N, int32_t K,
+                             int32_t method);
+int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t N, int64_t ldx,
+                int32_t K, int32_t method, double alpha, double tol_abs, int32_t* idx,
+                float* coef, int32_t* count, float* resnorm, int32_t* path, int32_t* ip,
+                void* workspace, size_t workspace_bytes, void* stream);
+
+/* Host-buffer variant for end-to-end use: X and every output are HOST
+ * pointers (pinned memory recommended); the library stages chunks through
+ * device buffers, overlapping H2D copies, encode and D2H copies on its own
+ * streams, and returns after the results are on the host.                   */
+int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t N,
+                     int64_t ldx, int32_t K, int32_t method, double alpha, double tol_abs,
+                     int32_t* idx, float* coef, int32_t* count, float* resnorm, int32_t* ip,
+                     int64_t chunk);
+
+/* Device synchronisation helper for hosts without a CUDA runtime binding. */
+int stmp_stream_sync(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STMP_B200_H */

@@ -1,0 +1,354 @@
+// extern "C" boundary of the STMP B200 library (declared in include/stmp_b200.h).
+// Validation mirrors the reference's error behaviour:
+// ValueError cases -> STMP_EINVAL, fingerprint mismatch -> STMP_ESTALE,
+// CUDA failures -> STMP_ECUDA.  No CPU fallback exists.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/stmp_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+struct stmp_dict : stmp::DictHandle {};
+struct stmp_tree : stmp::TreeHandle {};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(STMP_ECUDA, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define STMP_CUDA(call, what)                   \
+  do {                                          \
+    cudaError_t _e = (call);                    \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+
+int check_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "no CUDA device (the B200 path has no CPU fallback)");
+  int major = 0;
+  e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  if (major != 10)
+    return fail(STMP_ECUDA, "device compute capability %d.x: this library is built for sm_100a only", major);
+  return STMP_OK;
+}
+
+// pursuit.py:29-33
+int retained_count(double alpha, int k) {
+  int c = (int)ceil(alpha * k - 1e-9);
+  return c < 1 ? 1 : c;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* stmp_version(void) { return "stmp_b200 0.1.0 (sm_100a)"; }
+
+const char* stmp_last_error(void) { return g_err.c_str(); }
+
+uint64_t stmp_fnv1a64(const void* data, size_t len, uint64_t h) {
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < len; ++i) {
+    h ^= p[i];
+    h *= 0x100000001B3ULL;
+  }
+  return h;
+}
+
+int stmp_stream_sync(void* stream) {
+  STMP_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "cudaStreamSynchronize");
+  return STMP_OK;
+}
+
+int stmp_dict_create(const float* atoms, int64_t m, int32_t n, int32_t atoms_on_device,
+                     uint64_t fingerprint, void* stream, stmp_dict** out) {
+  g_err.clear();
+  if (out == nullptr) return fail(STMP_EINVAL, "out handle pointer is NULL");
+  *out = nullptr;
+  if (atoms == nullptr || m <= 0 || n <= 0)
+    return fail(STMP_EINVAL, "atoms must form a non-empty 2-D array, got shape (%lld, %d)",
+                (long long)m, n);
+  if (m > 0x7fffffffLL) return fail(STMP_EINVAL, "atom count %lld exceeds 2^31-1", (long long)m);
+  const int vpl = stmp::fused_vpl_for(n);
+  if (vpl < 0) return fail(STMP_EINVAL, "atom dimension %d exceeds the supported maximum 2048", n);
+  if (int rc = check_device()) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  stmp_dict* d = new stmp_dict();
+  d->m = m;
+  d->n = n;
+  d->vpl = vpl;
+  d->ld = 32 * vpl;
+  d->fingerprint = fingerprint;
+  const size_t bytes = (size_t)m * d->ld * sizeof(float);
+  cudaError_t e = cudaMalloc(&d->atoms, bytes);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d->atoms, 0, bytes, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(d->atoms, d->ld * sizeof(float), atoms, (size_t)n * sizeof(float),
+                          (size_t)n * sizeof(float), (size_t)m,
+                          atoms_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    cudaFree(d->atoms);
+    delete d;
+    return cuda_fail(e, "dictionary upload");
+  }
+  *out = d;
+  return STMP_OK;
+}
+
+void stmp_dict_free(stmp_dict* d) {
+  if (d == nullptr) return;
+  cudaFree(d->atoms);
+  delete d;
+}
+
+int stmp_dict_info(const stmp_dict* d, int64_t* m, int32_t* n, int32_t* ld, uint64_t* fp) {
+  if (d == nullptr) return fail(STMP_EINVAL, "dictionary handle is NULL");
+  if (m) *m = d->m;
+  if (n) *n = d->n;
+  if (ld) *ld = d->ld;
+  if (fp) *fp = d->fingerprint;
+  return STMP_OK;
+}
+
+int stmp_tree_create(const stmp_dict* d, int32_t levels, const int32_t* branching,
+                     const int64_t* level_offsets, const int32_t* child_begin,
+                     const int32_t* child_count, const float* centroids, int64_t num_leaves,
+                     const int32_t* leaf_atom, uint64_t fingerprint, void* stream,
+                     stmp_tree** out) {
+  g_err.clear();
+  if (out == nullptr) return fail(STMP_EINVAL, "out handle pointer is NULL");
+  *out = nullptr;
+  if (d == nullptr) return fail(STMP_EINVAL, "dictionary handle is NULL");
+  if (fingerprint != d->fingerprint)
+    return fail(STMP_ESTALE, "tree fingerprint %#018llx does not match dictionary fingerprint %#018llx",
+                (unsigned long long)fingerprint, (unsigned long long)d->fingerprint);
+  if (levels < 1) return fail(STMP_EINVAL, "branching must name at least one level");
+  if (!branching || !level_offsets || !child_begin || !child_count || !centroids || !leaf_atom)
+    return fail(STMP_EINVAL, "tree arrays must not be NULL");
+  for (int l = 0; l < levels; ++l)
+    if (branching[l] < 2)
+      return fail(STMP_EINVAL, "branching entry %d at level %d must be at least 2", branching[l], l);
+  if (level_offsets[0] != 0 || level_offsets[1] != 1) return fail(STMP_EINVAL, "tree must have one root");
+  const int64_t ni = level_offsets[levels + 1];
+  // structural checks: BFS contiguity, non-empty nodes, leaf coverage
+  for (int dd = 0; dd <= levels; ++dd) {
+    int64_t expect = dd < levels ? level_offsets[dd + 1] : 0;
+    for (int64_t v = level_offsets[dd]; v < level_offsets[dd + 1]; ++v) {
+      if (child_count[v] < 1) return fail(STMP_EINVAL, "internal node %lld has no children", (long long)v);
+      if (child_begin[v] != expect)
+        return fail(STMP_EINVAL, "children of node %lld are not contiguous in BFS order", (long long)v);
+      expect += child_count[v];
+    }
+    const int64_t end = dd < levels ? level_offsets[dd + 2] : num_leaves;
+    if (expect != end) return fail(STMP_EINVAL, "child counts at depth %d do not cover the next level", dd);
+  }
+  for (int64_t j = 0; j < num_leaves; ++j)
+    if (leaf_atom[j] < 0 || leaf_atom[j] >= d->m)
+      return fail(STMP_EINVAL, "leaf atom index %d outside [0, %lld)", leaf_atom[j], (long long)d->m);
+  if (int rc = check_device()) return rc;
+
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  stmp_tree* t = new stmp_tree();
+  t->levels = levels;
+  t->branching.assign(branching, branching + levels);
+  t->level_offsets.assign(level_offsets, level_offsets + levels + 2);
+  t->num_internal = ni;
+  t->num_leaves = num_leaves;
+  t->n = d->n;
+  t->ld = d->ld;
+  t->fingerprint = fingerprint;
+  t->dict = d;
+  t->root_children = child_count[0];
+  for (int64_t v = 0; v < ni; ++v) t->max_children = std::max(t->max_children, child_count[v]);
+  for (int64_t v = level_offsets[levels]; v < ni; ++v)
+    t->max_leaf_children = std::max(t->max_leaf_children, child_count[v]);
+  cudaError_t e = cudaMalloc(&t->child_begin, ni * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&t->child_count, ni * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&t->leaf_atom, num_leaves * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&t->cent, (size_t)ni * t->ld * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t->child_begin, child_begin, ni * sizeof(int), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t->child_count, child_count, ni * sizeof(int), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t->leaf_atom, leaf_atom, num_leaves * sizeof(int), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(t->cent, 0, (size_t)ni * t->ld * sizeof(float), s);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(t->cent, t->ld * sizeof(float), centroids, (size_t)t->n * sizeof(float),
+                          (size_t)t->n * sizeof(float), (size_t)ni, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    stmp_tree_free(t);
+    return cuda_fail(e, "tree upload");
+  }
+  *out = t;
+  return STMP_OK;
+}
+
+void stmp_tree_free(stmp_tree* t) {
+  if (t == nullptr) return;
+  cudaFree(t->child_begin);
+  cudaFree(t->child_count);
+  cudaFree(t->leaf_atom);
+  cudaFree(t->cent);
+  delete t;
+}
+
+size_t stmp_encode_workspace(const stmp_dict*, const stmp_tree*, int64_t, int32_t, int32_t) {
+  return 0;
+}
+
+static int validate_encode(const stmp_dict* d, const stmp_tree* t, int64_t N, int64_t ldx,
+                           int32_t K, int32_t method, double alpha, double tol_abs) {
+  if (d == nullptr) return fail(STMP_EINVAL, "dictionary handle is NULL");
+  if (N < 0) return fail(STMP_EINVAL, "patch count must be non-negative, got %lld", (long long)N);
+  if (ldx < d->n) return fail(STMP_EINVAL, "row stride %lld below atom dimension %d", (long long)ldx, d->n);
+  if (K < 1) return fail(STMP_EINVAL, "sparsity K must be at least 1, got %d", K);
+  if (K > STMP_MAX_K) return fail(STMP_EINVAL, "sparsity K=%d exceeds the GPU maximum %d", K, STMP_MAX_K);
+  if (method != STMP_METHOD_MP && method != STMP_METHOD_OMP && method != STMP_METHOD_SELECT)
+    return fail(STMP_EINVAL, "unknown method %d", method);
+  if (method == STMP_METHOD_OMP && K > d->n)
+    return fail(STMP_EINVAL, "support size %d exceeds atom dimension %d", K, d->n);
+  if (std::isnan(tol_abs)) return fail(STMP_EINVAL, "residual tolerance is NaN");
+  if (t != nullptr) {
+    if (!(alpha > 0.0 && alpha <= 1.0)) return fail(STMP_EINVAL, "alpha must lie in (0, 1], got %g", alpha);
+    if (t->fingerprint != d->fingerprint)
+      return fail(STMP_ESTALE, "tree fingerprint %#018llx does not match dictionary fingerprint %#018llx",
+                  (unsigned long long)t->fingerprint, (unsigned long long)d->fingerprint);
+    if (t->dict != d && t->n != d->n) return fail(STMP_EINVAL, "tree dimension differs from dictionary");
+    for (int l = 0; l < t->levels; ++l)
+      if (retained_count(alpha, t->branching[l]) != 1)
+        return fail(STMP_EINVAL,
+                    "alpha=%g keeps %d branches at level %d; the GPU path implements greedy descent "
+                    "only (alpha <= 1/max(branching))",
+                    alpha, retained_count(alpha, t->branching[l]), l);
+  }
+  return STMP_OK;
+}
+
+int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t N, int64_t ldx,
+                int32_t K, int32_t method, double alpha, double tol_abs, int32_t* idx, float* coef,
+                int32_t* count, float* resnorm, int32_t* path, int32_t* ip, void* workspace,
+                size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (int rc = validate_encode(d, t, N, ldx, K, method, alpha, tol_abs)) return rc;
+  if (N == 0) return STMP_OK;
+  if (X == nullptr || idx == nullptr || coef == nullptr)
+    return fail(STMP_EINVAL, "X, idx and coef must be device pointers");
+  (void)workspace;
+  (void)workspace_bytes;
+  stmp::FusedArgs a{};
+  a.X = X;
+  a.N = N;
+  a.ldx = ldx;
+  a.n = d->n;
+  a.atoms = d->atoms;
+  a.m = d->m;
+  a.ld = d->ld;
+  a.vpl = d->vpl;
+  a.has_tree = t != nullptr;
+  if (t) a.tree = stmp::TreeView{t->child_begin, t->child_count, t->cent, t->leaf_atom, t->levels};
+  else a.tree = stmp::TreeView{nullptr, nullptr, nullptr, nullptr, 0};
+  a.K = K;
+  a.method = method;
+  a.tol_abs = tol_abs < 0 ? -1.f : (float)tol_abs;
+  a.idx = idx;
+  a.coef = coef;
+  a.count = count;
+  a.resnorm = resnorm;
+  a.path = t ? path : nullptr;
+  a.ip = ip;
+  const int wpb = 8;
+  const size_t atom_cache = (size_t)K * d->ld;
+  const size_t base_ws = (size_t)K * (K + 1) / 2 + 4 * (size_t)K;
+  a.cache_atoms = (method == STMP_METHOD_OMP && atom_cache * 4 <= 8192) ? 1 : 0;
+  a.warp_smem_floats = (int)(((base_ws + (a.cache_atoms ? atom_cache : 0)) + 3) / 4 * 4);
+  a.root_smem_rows = 0;
+  a.root_begin = 1;
+  if (t) {
+    const size_t root_bytes = (size_t)t->root_children * t->ld * 4;
+    if (root_bytes <= 48 * 1024) a.root_smem_rows = t->root_children;
+  }
+  const size_t smem = 4 * ((size_t)a.root_smem_rows * a.ld + (size_t)wpb * a.warp_smem_floats);
+  if (smem > 200 * 1024) return fail(STMP_EINVAL, "K=%d needs too much shared memory", K);
+  cudaError_t e = stmp::launch_encode_fused(a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "encode launch");
+  return STMP_OK;
+}
+
+int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t N,
+                     int64_t ldx, int32_t K, int32_t method, double alpha, double tol_abs,
+                     int32_t* idx, float* coef, int32_t* count, float* resnorm, int32_t* ip,
+                     int64_t chunk) {
+  g_err.clear();
+  if (int rc = validate_encode(d, t, N, ldx, K, method, alpha, tol_abs)) return rc;
+  if (N == 0) return STMP_OK;
+  if (X == nullptr || idx == nullptr || coef == nullptr)
+    return fail(STMP_EINVAL, "X, idx and coef must be host pointers");
+  if (chunk <= 0) chunk = 65536;
+  if (chunk > N) chunk = N;
+  const int NS = 2;
+  cudaStream_t st[NS];
+  float* dX[NS] = {};
+  int32_t* dI[NS] = {};
+  float* dC[NS] = {};
+  int32_t* dN[NS] = {};
+  float* dR[NS] = {};
+  int32_t* dP[NS] = {};
+  int rc = STMP_OK;
+  for (int i = 0; i < NS; ++i) {
+    STMP_CUDA(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking), "stream create");
+    STMP_CUDA(cudaMalloc(&dX[i], chunk * d->n * sizeof(float)), "staging alloc");
+    STMP_CUDA(cudaMalloc(&dI[i], chunk * K * sizeof(int32_t)), "staging alloc");
+    STMP_CUDA(cudaMalloc(&dC[i], chunk * K * sizeof(float)), "staging alloc");
+    STMP_CUDA(cudaMalloc(&dN[i], chunk * sizeof(int32_t)), "staging alloc");
+    STMP_CUDA(cudaMalloc(&dR[i], chunk * sizeof(float)), "staging alloc");
+    STMP_CUDA(cudaMalloc(&dP[i], chunk * 2 * sizeof(int32_t)), "staging alloc");
+  }
+  int64_t ci = 0;
+  for (int64_t s0 = 0; s0 < N && rc == STMP_OK; s0 += chunk, ++ci) {
+    const int b = (int)(ci % NS);
+    const int64_t rows = std::min(chunk, N - s0);
+    cudaError_t e = cudaMemcpy2DAsync(dX[b], d->n * sizeof(float), X + s0 * ldx, ldx * sizeof(float),
+                                      d->n * sizeof(float), rows, cudaMemcpyHostToDevice, st[b]);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
+    rc = stmp_encode(d, t, dX[b], rows, d->n, K, method, alpha, tol_abs, dI[b], dC[b], dN[b], dR[b],
+                     nullptr, dP[b], nullptr, 0, st[b]);
+    if (rc != STMP_OK) break;
+    e = cudaMemcpyAsync(idx + s0 * K, dI[b], rows * K * sizeof(int32_t), cudaMemcpyDeviceToHost, st[b]);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(coef + s0 * K, dC[b], rows * K * sizeof(float), cudaMemcpyDeviceToHost, st[b]);
+    if (e == cudaSuccess && count) e = cudaMemcpyAsync(count + s0, dN[b], rows * sizeof(int32_t), cudaMemcpyDeviceToHost, st[b]);
+    if (e == cudaSuccess && resnorm) e = cudaMemcpyAsync(resnorm + s0, dR[b], rows * sizeof(float), cudaMemcpyDeviceToHost, st[b]);
+    if (e == cudaSuccess && ip) e = cudaMemcpyAsync(ip + 2 * s0, dP[b], rows * 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st[b]);
+    if (e != cudaSuccess) rc = cuda_fail(e, "D2H");
+  }
+  for (int i = 0; i < NS; ++i) {
+    cudaError_t e = cudaStreamSynchronize(st[i]);
+    if (e != cudaSuccess && rc == STMP_OK) rc = cuda_fail(e, "encode_host sync");
+    cudaFree(dX[i]); cudaFree(dI[i]); cudaFree(dC[i]); cudaFree(dN[i]); cudaFree(dR[i]); cudaFree(dP[i]);
+    cudaStreamDestroy(st[i]);
+  }
+  return rc;
+}
+
+}  // extern "C"

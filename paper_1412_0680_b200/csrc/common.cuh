@@ -1,0 +1,91 @@
+// Shared device helpers and handle layouts for the STMP B200 library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace stmp {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr float kRidge = 1e-8f;     // pkg/src/stmp/pursuit.py:249
+constexpr float kRelTol = 1e-6f;    // pkg/src/stmp/pursuit.py:209
+
+struct DictHandle {
+  float* atoms = nullptr;  // [m, ld] f32, zero-padded columns n..ld
+  int64_t m = 0;
+  int n = 0;
+  int ld = 0;              // padded row stride = 32 * vpl
+  int vpl = 0;             // values per lane for the warp-per-patch kernels
+  uint64_t fingerprint = 0;
+};
+
+struct TreeHandle {
+  int levels = 0;
+  std::vector<int> branching;
+  std::vector<int64_t> level_offsets;  // L+2
+  int64_t num_internal = 0;
+  int64_t num_leaves = 0;
+  int* child_begin = nullptr;   // [num_internal]
+  int* child_count = nullptr;   // [num_internal]
+  float* cent = nullptr;        // [num_internal, ld]
+  int* leaf_atom = nullptr;     // [num_leaves]
+  int n = 0, ld = 0;
+  int root_children = 0;
+  int max_children = 0;         // over all internal nodes
+  int max_leaf_children = 0;    // over depth-L nodes
+  uint64_t fingerprint = 0;
+  const DictHandle* dict = nullptr;
+};
+
+// Device-side view passed to kernels by value.
+struct TreeView {
+  const int* child_begin;
+  const int* child_count;
+  const float* cent;
+  const int* leaf_atom;
+  int levels;
+};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(kFull, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// Ordering key for "max |score|, ties to the lowest id": |s| as IEEE bits is
+// order-preserving for non-negative floats; the low word inverts the id so a
+// larger key means a smaller id (pursuit.py:108,151,159-161).
+__device__ __forceinline__ unsigned long long score_key(float s, unsigned id) {
+  return ((unsigned long long)__float_as_uint(fabsf(s)) << 32) |
+         (unsigned long long)(0xFFFFFFFFu - id);
+}
+
+// Reduce-scatter of 32 per-lane partial sums: afterwards p[0] on lane l holds
+// the warp-wide sum of p[l].  31 shuffles instead of 32 x 5.
+__device__ __forceinline__ float reduce_scatter32(float (&p)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < o; ++j) {
+      const float send = upper ? p[j] : p[j + o];
+      const float keep = upper ? p[j + o] : p[j];
+      p[j] = keep + __shfl_xor_sync(kFull, send, o);
+    }
+  }
+  return p[0];
+}
+
+}  // namespace stmp

@@ -1,0 +1,41 @@
+// Kernel launch interfaces shared between the ABI layer and the kernel files.
+#pragma once
+
+#include "common.cuh"
+
+namespace stmp {
+
+constexpr int kMethodMP = 0;
+constexpr int kMethodOMP = 1;
+constexpr int kMethodSelect = 2;
+
+struct FusedArgs {
+  const float* X;
+  int64_t N;
+  int64_t ldx;
+  int n;
+  const float* atoms;
+  int64_t m;
+  int ld;
+  int vpl;
+  TreeView tree;
+  int has_tree;
+  int K;
+  int method;
+  float tol_abs;          // < 0: relative tolerance 1e-6 * ||x||
+  int32_t* idx;
+  float* coef;
+  int32_t* count;
+  float* resnorm;
+  int32_t* path;
+  int32_t* ip;
+  int root_smem_rows;     // > 0: the root's child centroids are staged in shared memory
+  int root_begin;
+  int cache_atoms;        // support atoms cached per warp in shared memory
+  int warp_smem_floats;   // per-warp shared scratch (OMP factor + optional atom cache)
+};
+
+int fused_vpl_for(int n);
+cudaError_t launch_encode_fused(const FusedArgs& a, cudaStream_t stream);
+
+}  // namespace stmp

@@ -1,0 +1,311 @@
+"""GPU parity: the sm_100a path through the C ABI vs the golden vectors and the
+CPU oracle (SURVEY §8c contract, comparator in tests/parity.py)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, flat_from_fixture, golden
+from oracle import stmp_oracle as O
+from parity import compare
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1412_0680_b200 import build
+    build.build()
+
+
+def P():
+    import paper_1412_0680_b200 as pkg
+    return pkg
+
+
+def as_np(res):
+    out = {k: getattr(res, k) for k in ("idx", "coef", "count", "resnorm", "ip", "path")}
+    return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in out.items() if v is not None}
+
+
+def oracle_pack(select, a64, X, K, method, tol=None):
+    return O.pack(O.encode_batch(select, a64, X, K, method, tol), K)
+
+
+def run(selector, X, K, method, tol=None, paths=True):
+    Xd = torch.as_tensor(np.ascontiguousarray(X, dtype=np.float32)).cuda()
+    res = P().encode(selector, Xd, K, method=method, tol=tol, paths=paths)
+    torch.cuda.synchronize()
+    return as_np(res)
+
+
+# ----------------------------------------------------------------- small fixtures
+
+def test_tree_select_small_matches_reference():
+    z = golden("select_small.npz")
+    flat = flat_from_fixture(z)
+    sel = P().TreeSelector(flat, z["atoms"], 0.1)
+    out = run(sel, z["Q"], 1, "select")
+    t = O.OracleTree.from_flat(flat)
+    a64 = z["atoms"].astype(np.float64)
+    gaps = np.array([O.tree_select(t, a64, q.astype(np.float64), 0.1)[5] for q in z["Q"]])
+    ok = (out["idx"][:, 0] == z["greedy_idx"]) | (gaps < 1e-5)
+    assert ok.all()
+    same = out["idx"][:, 0] == z["greedy_idx"]
+    np.testing.assert_allclose(out["coef"][same, 0], z["greedy_score"][same], rtol=1e-5, atol=1e-6)
+    np.testing.assert_array_equal(out["ip"], z["greedy_ip"])
+
+
+def test_exact_select_small_matches_reference():
+    z = golden("select_small.npz")
+    sel = P().ExactSelector(z["atoms"])
+    out = run(sel, z["Q"], 1, "select")
+    assert (out["idx"][:, 0] == z["exact_idx"]).mean() == 1.0
+    np.testing.assert_allclose(out["coef"][:, 0], z["exact_score"], rtol=1e-5, atol=1e-6)
+    assert (out["ip"][:, 0] == 500).all() and (out["ip"][:, 1] == 0).all()
+
+
+def test_ragged_tree_select_matches_reference():
+    z = golden("select_ragged.npz")
+    flat = flat_from_fixture(z)
+    sel = P().TreeSelector(flat, z["atoms"], 1 / 7)
+    out = run(sel, z["Q"], 1, "select")
+    np.testing.assert_array_equal(out["idx"][:, 0], z["idx"])
+    np.testing.assert_allclose(out["coef"][:, 0], z["score"], rtol=1e-5, atol=1e-6)
+    np.testing.assert_array_equal(out["ip"], z["ip"])
+
+
+@pytest.mark.parametrize("sel_kind", ["tree", "exact"])
+@pytest.mark.parametrize("method", ["omp", "mp"])
+def test_pursuit_small_matches_reference(sel_kind, method):
+    z = golden("pursuit_small.npz")
+    K = int(z["K"])
+    flat = flat_from_fixture(z)
+    a64 = z["atoms"].astype(np.float64)
+    if sel_kind == "tree":
+        sel = P().TreeSelector(flat, z["atoms"], 1 / 16)
+        osel = O.tree_selector(O.OracleTree.from_flat(flat), a64, 1 / 16)
+    else:
+        sel = P().ExactSelector(z["atoms"])
+        osel = O.exact_selector(a64)
+    out = run(sel, z["X"], K, method)
+    ref = oracle_pack(osel, a64, z["X"], K, method)
+    # the oracle itself equals the reference run recorded in the fixture
+    np.testing.assert_array_equal(ref["idx"], z[f"{sel_kind}_{method}_idx"])
+    rep = compare(out, ref, z["X"], check_path=sel_kind == "tree")
+    assert rep.ok, rep.summary()
+    assert rep.excused <= 2
+
+
+@pytest.mark.parametrize("tol_tag,tol", [("deftol", None), ("tol0", 0.0), ("tol05", 0.5)])
+@pytest.mark.parametrize("method", ["omp", "mp"])
+def test_edge_cases(tol_tag, tol, method):
+    z = golden("edge.npz")
+    p = golden("pursuit_small.npz")
+    sel = P().TreeSelector(flat_from_fixture(p), p["atoms"], 1 / 16)
+    out = run(sel, z["E"], 4, method, tol)
+    ref = {k.split("_", 2)[2]: z[k] for k in z.files if k.startswith(f"{method}_{tol_tag}_")}
+    ref["gaps"] = np.full((len(z["E"]), 4), np.inf)
+    rep = compare(out, ref, z["E"], check_path=False)
+    assert rep.ok, rep.summary()
+    # zero patch: empty code, zero residual (pursuit.py:214 with tolerance 0)
+    assert out["count"][0] == 0 and out["resnorm"][0] == 0.0
+
+
+def test_zero_residual_select_matches_reference():
+    z = golden("edge.npz")
+    p = golden("pursuit_small.npz")
+    sel = P().TreeSelector(flat_from_fixture(p), p["atoms"], 1 / 16)
+    out = run(sel, np.zeros((1, 24), np.float32), 1, "select")
+    assert out["idx"][0, 0] == int(z["zero_tree_select"][0])
+    assert out["coef"][0, 0] == 0.0
+    ex = P().ExactSelector(p["atoms"])
+    out = run(ex, np.zeros((1, 24), np.float32), 1, "select")
+    assert out["idx"][0, 0] == int(z["zero_exact_select"][0]) == 0
+
+
+def test_selector_protocol_drop_in():
+    """The GPU selector plugs into the reference's MP control flow unchanged
+    (pursuit.py:194-221, restated by the oracle loop) and gives the same codes."""
+    z = golden("pursuit_small.npz")
+    flat = flat_from_fixture(z)
+    sel = P().TreeSelector(flat, z["atoms"], 1 / 16)
+    a64 = z["atoms"].astype(np.float64)
+    counter = P().ScoreCounter()
+
+    def gpu_select(r):
+        before = (counter.inner_products, counter.centroid_inner_products)
+        i, s = sel.select(r, counter)
+        ci = counter.centroid_inner_products - before[1]
+        return i, s, ci, counter.inner_products - before[0] - ci, [], np.inf
+
+    for p_, x in enumerate(z["X"][:20]):
+        got = O.encode_one(gpu_select, a64, x, int(z["K"]), "mp")
+        assert got["indices"] == [int(i) for i in z["tree_mp_idx"][p_, :z["tree_mp_count"][p_]]]
+        np.testing.assert_allclose(got["coefs"], z["tree_mp_coef"][p_, :z["tree_mp_count"][p_]],
+                                   rtol=1e-4, atol=1e-5)
+        assert got["ip"] == int(z["tree_mp_ip"][p_, 0])
+    # single-patch API mirrors
+    code = P().matching_pursuit(sel, z["X"][0], P().SearchParams(K=int(z["K"])))
+    assert [i for i, _ in code.entries] == [int(i) for i in z["tree_mp_idx"][0, :z["tree_mp_count"][0]]]
+    code = P().orthogonal_matching_pursuit(sel, z["X"][0], P().SearchParams(K=int(z["K"])))
+    assert [i for i, _ in code.entries] == [int(i) for i in z["tree_omp_idx"][0, :z["tree_omp_count"][0]]]
+
+
+def test_error_behaviour_matches_reference():
+    z = golden("pursuit_small.npz")
+    flat = flat_from_fixture(z)
+    with pytest.raises(ValueError):
+        P().TreeSelector(flat, z["atoms"], 0.5)   # non-greedy: refused, not silently different
+    with pytest.raises(ValueError):
+        P().TreeSelector(flat, z["atoms"], 0.0)
+    other = np.ascontiguousarray(z["atoms"][::-1])
+    with pytest.raises(P().StaleTreeError):
+        P().TreeSelector(flat, other, 1 / 16)
+    sel = P().TreeSelector(flat, z["atoms"], 1 / 16)
+    X = torch.zeros((4, 24), device="cuda")
+    with pytest.raises(ValueError):
+        P().encode(sel, X, 0)
+    with pytest.raises(ValueError):
+        P().encode(sel, torch.zeros((4, 23), device="cuda"), 3)
+    with pytest.raises(ValueError):
+        P().encode(sel, X, 3, tol=-1.0)
+
+
+def test_encode_host_equals_device_path():
+    z = golden("pursuit_small.npz")
+    sel = P().TreeSelector(flat_from_fixture(z), z["atoms"], 1 / 16)
+    X = np.ascontiguousarray(np.tile(z["X"], (7, 1)))
+    dev = run(sel, X, int(z["K"]), "omp", paths=False)
+    host = P().encode_host(sel, X, int(z["K"]), "omp", chunk=200)
+    for k in ("idx", "coef", "count", "resnorm", "ip"):
+        np.testing.assert_array_equal(getattr(host, k), dev[k])
+
+
+# ----------------------------------------------------------------- benchmark configs
+
+def _config(cid):
+    from paper_1412_0680_b200 import tree as T
+    from paper_1412_0680_b200 import workloads as W
+    cfg = W.CONFIGS[cid]
+    path = os.path.join(GOLDEN, "trees", f"c{cid}.npz")
+    if not os.path.exists(path):
+        alt = os.path.join(os.path.dirname(GOLDEN), "..", "artifacts", "trees", f"c{cid}.npz")
+        if not os.path.exists(alt):
+            pytest.skip(f"tree structure for config {cid} not shipped")
+        path = alt
+    wl = W.make_dictionary(cfg)
+    flat = T.load_structure(path, wl.atoms)
+    return cfg, wl, flat
+
+
+_CACHE = {}
+
+
+def config(cid):
+    if cid not in _CACHE:
+        _CACHE[cid] = _config(cid)
+    return _CACHE[cid]
+
+
+@pytest.mark.parametrize("cid,rows,method", [
+    (0, 10_000, "omp"), (0, 10_000, "mp"), (1, 4096, "omp"), (1, 2048, "mp"),
+    (2, 1024, "omp"), (3, 2048, "omp"), (4, 128, "omp")])
+def test_config_tree_parity(cid, rows, method):
+    from paper_1412_0680_b200 import workloads as W
+    cfg, wl, flat = config(cid)
+    X = W.make_patches(wl, rows)
+    sel = P().TreeSelector(flat, wl.atoms, cfg.alpha)
+    out = run(sel, X, cfg.K, method)
+    a64 = wl.atoms.astype(np.float64)
+    ref = oracle_pack(O.tree_selector(O.OracleTree.from_flat(flat), a64, cfg.alpha), a64, X, cfg.K, method)
+    rep = compare(out, ref, X)
+    print(f"c{cid} {method}: {rep.summary()}")
+    assert rep.ok, rep.summary()
+    assert rep.excused <= max(2, rows // 500)
+
+
+def test_config0_golden_prefix():
+    """GPU vs the reference's own recorded runs on config 0 (no oracle in between)."""
+    cfg, wl, flat = config(0)
+    z = golden("c0_prefix.npz")
+    sel = P().TreeSelector(flat, wl.atoms, cfg.alpha)
+    esel = P().ExactSelector(wl.atoms)
+    a64 = wl.atoms.astype(np.float64)
+    t = O.OracleTree.from_flat(flat)
+    for tag, s, os_, method, rows in (("tree_omp", sel, O.tree_selector(t, a64, cfg.alpha), "omp", 1024),
+                                      ("tree_mp", sel, O.tree_selector(t, a64, cfg.alpha), "mp", 1024),
+                                      ("exact_omp", esel, O.exact_selector(a64), "omp", 128)):
+        X = z["X"][:rows]
+        out = run(s, X, cfg.K, method, paths=False)
+        ref = {k[len(tag) + 1:]: z[k][:rows] for k in z.files if k.startswith(tag + "_")}
+        ref["gaps"] = oracle_pack(os_, a64, X, cfg.K, method)["gaps"]
+        rep = compare(out, ref, X, check_path=False)
+        assert rep.ok, f"{tag}: {rep.summary()}"
+
+
+@pytest.mark.parametrize("cid,rows", [(1, 256), (4, 8)])
+def test_config_exhaustive_parity(cid, rows):
+    from paper_1412_0680_b200 import workloads as W
+    cfg, wl, flat = config(cid)
+    X = W.make_patches(wl, rows)
+    sel = P().ExactSelector(wl.atoms)
+    out = run(sel, X, cfg.K, "omp")
+    a64 = wl.atoms.astype(np.float64)
+    ref = oracle_pack(O.exact_selector(a64), a64, X, cfg.K, "omp")
+    rep = compare(out, ref, X, check_path=False)
+    assert rep.ok, rep.summary()
+
+
+def test_config1_full_size_properties():
+    """All 1,048,576 config-1 patches: size-independent invariants of OMP."""
+    from paper_1412_0680_b200 import workloads as W
+    cfg, wl, flat = config(1)
+    X = W.make_patches(wl)
+    sel = P().TreeSelector(flat, wl.atoms, cfg.alpha)
+    Xd = torch.as_tensor(X).cuda()
+    res = P().encode(sel, Xd, cfg.K, method="omp", paths=True)
+    torch.cuda.synchronize()
+    A = torch.as_tensor(wl.atoms).cuda().double()
+    idx, coef, cnt = res.idx.long(), res.coef.double(), res.count.long()
+    valid = idx >= 0
+    assert bool((valid.sum(1) == cnt).all())
+    assert bool((cnt >= 1).all()) and bool((cnt <= cfg.K).all())
+    # residual norm equals ||x - A_S c|| recomputed in f64 (all patches)
+    recon = torch.einsum("pk,pkn->pn", coef * valid, A[idx.clamp(min=0)])
+    r = Xd.double() - recon
+    rn = r.norm(dim=1)
+    rel = (rn - res.resnorm.double()).abs() / rn.clamp(min=1e-12)
+    assert float(rel.max()) < 1e-4
+    # OMP optimality: the residual is orthogonal to every selected atom
+    ortho = torch.einsum("pkn,pn->pk", A[idx.clamp(min=0)], r).abs() * valid
+    assert float((ortho.max(1).values / Xd.double().norm(dim=1)).max()) < 1e-4
+    # support atoms are distinct per patch
+    srt = torch.sort(torch.where(valid, idx, -torch.arange(1, cfg.K + 1, device="cuda")), dim=1).values
+    assert bool((srt[:, 1:] != srt[:, :-1]).all())
+    # paths follow the tree and end at the selected atom's leaf parent
+    cb = torch.as_tensor(flat.child_begin).cuda().long()
+    cc = torch.as_tensor(flat.child_count).cuda().long()
+    la = torch.as_tensor(flat.leaf_atom).cuda().long()
+    path = res.path.long()
+    prev = torch.zeros_like(idx)
+    for lvl in range(flat.levels):
+        node = path[:, :, lvl]
+        ok = (node >= cb[prev]) & (node < cb[prev] + cc[prev])
+        assert bool((ok | ~valid).all())
+        prev = node.clamp(min=0)
+    assert bool(((la[cb[prev]] == idx) | ~valid).all())  # single-atom leaves in config 1
+    # cost accounting: 32 + 32 + 16 centroids + 1 leaf atom per selection
+    sel_per = torch.div(res.ip[:, 0].long(), 81, rounding_mode="floor")
+    assert bool((res.ip[:, 0].long() % 81 == 0).all())
+    assert bool(((sel_per == cnt) | (sel_per == cnt + 1)).all())
+    assert bool((res.ip[:, 1].long() == sel_per * 80).all())
+    # the first rows equal an independent small-batch run (batch-size invariance)
+    head = run(sel, X[:3000], cfg.K, "omp", paths=False)
+    np.testing.assert_array_equal(head["idx"], res.idx[:3000].cpu().numpy())
+    np.testing.assert_array_equal(head["coef"], res.coef[:3000].cpu().numpy())
