@@ -360,7 +360,7 @@ def encode(selector, X, K: int, method: str = "omp", tol: float | None = None,
     ws_bytes = int(lib.stmp_encode_workspace(g.handle, th, N, K, _METHODS[method]))
     ws = torch.empty((max(ws_bytes, 1),), dtype=torch.uint8, device=dev)
     _lib.check(lib.stmp_encode(
-        g.handle, th, X.data_ptr(), N, X.stride(0), K, _METHODS[method],
+        g.handle, th, X.data_ptr(), N, X.stride(0) if N > 1 else g.n, K, _METHODS[method],
         float(selector.alpha), -1.0 if tol is None else float(tol),
         idx.data_ptr(), coef.data_ptr(), count.data_ptr(), resn.data_ptr(),
         path.data_ptr() if path is not None else None, ip.data_ptr(),

@@ -110,7 +110,10 @@ def test_edge_cases(tol_tag, tol, method):
     sel = P().TreeSelector(flat_from_fixture(p), p["atoms"], 1 / 16)
     out = run(sel, z["E"], 4, method, tol)
     ref = {k.split("_", 2)[2]: z[k] for k in z.files if k.startswith(f"{method}_{tol_tag}_")}
-    ref["gaps"] = np.full((len(z["E"]), 4), np.inf)
+    a64 = p["atoms"].astype(np.float64)
+    orc = oracle_pack(O.tree_selector(O.OracleTree.from_flat(flat_from_fixture(p)), a64, 1 / 16),
+                      a64, z["E"], 4, method, tol)
+    ref["gaps"], ref["rnorm_rel"] = orc["gaps"], orc["rnorm_rel"]
     rep = compare(out, ref, z["E"], check_path=False)
     assert rep.ok, rep.summary()
     # zero patch: empty code, zero residual (pursuit.py:214 with tolerance 0)
