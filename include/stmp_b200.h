@@ -112,6 +112,11 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
                      int32_t* idx, float* coef, int32_t* count, float* resnorm, int32_t* ip,
                      int64_t chunk);
 
+/* Process-wide tuning knobs (no reference counterpart):
+ *   "path": 0 auto (default), 1 fused warp-per-patch kernel, 2 staged tensor-core pipeline;
+ *   "staged_min_batch": batch size from which `auto` picks the staged pipeline.          */
+int stmp_set_option(const char* key, int64_t value);
+
 /* Device synchronisation helper for hosts without a CUDA runtime binding. */
 int stmp_stream_sync(void* stream);
 

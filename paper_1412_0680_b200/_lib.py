@@ -42,7 +42,14 @@ EXPORTS = {
                                    C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     "stmp_stream_sync": (C.c_int, [C.c_void_p]),
+    "stmp_set_option": (C.c_int, [C.c_char_p, C.c_int64]),
 }
+
+PATH_AUTO, PATH_FUSED, PATH_STAGED = 0, 1, 2
+
+
+def set_option(key: str, value: int) -> None:
+    check(load().stmp_set_option(key.encode(), int(value)))
 
 _lib = None
 

@@ -14,6 +14,7 @@
 #include "../../include/stmp_b200.h"
 #include "common.cuh"
 #include "kernels.cuh"
+#include "staged.cuh"
 
 struct stmp_dict : stmp::DictHandle {};
 struct stmp_tree : stmp::TreeHandle {};
@@ -21,6 +22,8 @@ struct stmp_tree : stmp::TreeHandle {};
 namespace {
 
 thread_local std::string g_err;
+int g_path_mode = 0;          // 0 auto, 1 fused warp-per-patch, 2 staged tensor-core
+int64_t g_staged_min = 16384; // auto: staged path from this batch size on
 
 int fail(int code, const char* fmt, ...) {
   char buf[1024];
@@ -201,6 +204,11 @@ int stmp_tree_create(const stmp_dict* d, int32_t levels, const int32_t* branchin
     stmp_tree_free(t);
     return cuda_fail(e, "tree upload");
   }
+  std::string berr;
+  if (!stmp::build_staged_tables(t, child_begin, child_count, centroids, s, &berr) && !berr.empty()) {
+    stmp_tree_free(t);
+    return fail(STMP_ECUDA, "staged table upload: %s", berr.c_str());
+  }
   *out = t;
   return STMP_OK;
 }
@@ -211,11 +219,36 @@ void stmp_tree_free(stmp_tree* t) {
   cudaFree(t->child_count);
   cudaFree(t->leaf_atom);
   cudaFree(t->cent);
+  stmp::free_staged_tables(t);
   delete t;
 }
 
-size_t stmp_encode_workspace(const stmp_dict*, const stmp_tree*, int64_t, int32_t, int32_t) {
-  return 0;
+static bool use_staged(const stmp_dict* d, const stmp_tree* t, int64_t N, int32_t K, int32_t method) {
+  if (g_path_mode == 1 || d == nullptr || t == nullptr) return false;
+  if (!stmp::staged_supported(d, t, K, method)) return false;
+  return g_path_mode == 2 || N >= g_staged_min;
+}
+
+int stmp_set_option(const char* key, int64_t value) {
+  g_err.clear();
+  if (key == nullptr) return fail(STMP_EINVAL, "option key is NULL");
+  if (strcmp(key, "path") == 0) {
+    if (value < 0 || value > 2) return fail(STMP_EINVAL, "path must be 0 (auto), 1 (fused) or 2 (staged)");
+    g_path_mode = (int)value;
+    return STMP_OK;
+  }
+  if (strcmp(key, "staged_min_batch") == 0) {
+    if (value < 1) return fail(STMP_EINVAL, "staged_min_batch must be positive");
+    g_staged_min = value;
+    return STMP_OK;
+  }
+  return fail(STMP_EINVAL, "unknown option '%s'", key);
+}
+
+size_t stmp_encode_workspace(const stmp_dict* d, const stmp_tree* t, int64_t N, int32_t K,
+                             int32_t method) {
+  if (!use_staged(d, t, N, K, method) || N <= 0) return 0;
+  return stmp::staged_workspace_bytes(d, t, N, K, method);
 }
 
 static int validate_encode(const stmp_dict* d, const stmp_tree* t, int64_t N, int64_t ldx,
@@ -255,8 +288,17 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
   if (N == 0) return STMP_OK;
   if (X == nullptr || idx == nullptr || coef == nullptr)
     return fail(STMP_EINVAL, "X, idx and coef must be device pointers");
-  (void)workspace;
-  (void)workspace_bytes;
+  if (use_staged(d, t, N, K, method)) {
+    const size_t need = stmp::staged_workspace_bytes(d, t, N, K, method);
+    if (workspace == nullptr || workspace_bytes < need)
+      return fail(STMP_EINVAL, "workspace of %zu bytes is below the required %zu (stmp_encode_workspace)",
+                  workspace_bytes, need);
+    cudaError_t e = stmp::run_staged(d, t, X, N, ldx, K, method, tol_abs < 0 ? -1.f : (float)tol_abs, idx,
+                                     coef, count, resnorm, path, ip, workspace, workspace_bytes,
+                                     static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "staged encode");
+    return STMP_OK;
+  }
   stmp::FusedArgs a{};
   a.X = X;
   a.N = N;
@@ -315,6 +357,8 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
   int32_t* dN[NS] = {};
   float* dR[NS] = {};
   int32_t* dP[NS] = {};
+  void* dW[NS] = {};
+  const size_t wsz = stmp_encode_workspace(d, t, chunk, K, method);
   int rc = STMP_OK;
   for (int i = 0; i < NS; ++i) {
     STMP_CUDA(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking), "stream create");
@@ -324,6 +368,7 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
     STMP_CUDA(cudaMalloc(&dN[i], chunk * sizeof(int32_t)), "staging alloc");
     STMP_CUDA(cudaMalloc(&dR[i], chunk * sizeof(float)), "staging alloc");
     STMP_CUDA(cudaMalloc(&dP[i], chunk * 2 * sizeof(int32_t)), "staging alloc");
+    if (wsz) STMP_CUDA(cudaMalloc(&dW[i], wsz), "workspace alloc");
   }
   int64_t ci = 0;
   for (int64_t s0 = 0; s0 < N && rc == STMP_OK; s0 += chunk, ++ci) {
@@ -333,7 +378,7 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
                                       d->n * sizeof(float), rows, cudaMemcpyHostToDevice, st[b]);
     if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
     rc = stmp_encode(d, t, dX[b], rows, d->n, K, method, alpha, tol_abs, dI[b], dC[b], dN[b], dR[b],
-                     nullptr, dP[b], nullptr, 0, st[b]);
+                     nullptr, dP[b], dW[b], wsz, st[b]);
     if (rc != STMP_OK) break;
     e = cudaMemcpyAsync(idx + s0 * K, dI[b], rows * K * sizeof(int32_t), cudaMemcpyDeviceToHost, st[b]);
     if (e == cudaSuccess) e = cudaMemcpyAsync(coef + s0 * K, dC[b], rows * K * sizeof(float), cudaMemcpyDeviceToHost, st[b]);
@@ -345,7 +390,7 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
   for (int i = 0; i < NS; ++i) {
     cudaError_t e = cudaStreamSynchronize(st[i]);
     if (e != cudaSuccess && rc == STMP_OK) rc = cuda_fail(e, "encode_host sync");
-    cudaFree(dX[i]); cudaFree(dI[i]); cudaFree(dC[i]); cudaFree(dN[i]); cudaFree(dR[i]); cudaFree(dP[i]);
+    cudaFree(dX[i]); cudaFree(dI[i]); cudaFree(dC[i]); cudaFree(dN[i]); cudaFree(dR[i]); cudaFree(dP[i]); cudaFree(dW[i]);
     cudaStreamDestroy(st[i]);
   }
   return rc;

@@ -22,7 +22,14 @@ struct DictHandle {
   uint64_t fingerprint = 0;
 };
 
+struct StagedLevel {
+  int npad = 0;       // children per node padded to the UMMA N granularity (16)
+  int tmem_cols = 0;  // TMEM columns allocated for the [128 x npad] f32 accumulator
+};
+
 struct TreeHandle {
+  std::vector<float*> staged_tables;        // per level: [nodes][kchunks][hi|lo][npad x 32] SW128
+  std::vector<StagedLevel> staged_levels;
   int levels = 0;
   std::vector<int> branching;
   std::vector<int64_t> level_offsets;  // L+2

@@ -1,0 +1,71 @@
+// Argument blocks and entry points of the staged (level-synchronous) encoder.
+#pragma once
+
+#include "common.cuh"
+
+namespace stmp {
+
+struct ScoreArgs {
+  const float* R;        // residual rows [N, ld]
+  int ld;
+  const int* perm;       // patch ids grouped by bin
+  const int4* items;     // {bin, start in perm, rows, 0}
+  const int* num_items;
+  const float* table;    // per-bin SW128 hi/lo child-centroid blocks
+  int npad, kchunks, tmem_cols;
+  int level, level_base;
+  const int* child_begin;
+  const int* child_count;
+  int* path_ws;          // [N, L] node chosen at each level this iteration
+  int* path_out;         // optional [N, K, L]
+  const int* count;      // current support size per patch (path slot)
+  int K, L;
+  int* next_counts;      // bin counters of the next level (nullptr at the last level)
+  int next_base;
+  int* rank;             // rank of the patch inside its next-level bin
+};
+
+struct UpdateArgs {
+  const float* X;        // caller's patches (row stride ldx, n valid columns)
+  int64_t ldx;
+  int n;
+  float* R;              // residual [N, ld]
+  int ld;
+  const float* X2;       // padded copy of X used by the OMP rebuild (OMP only)
+  int ld2;
+  const float* atoms;    // padded dictionary [m, ld]
+  const int* child_begin;
+  const int* child_count;
+  const int* leaf_atom;
+  int L;
+  const int* path_ws;
+  int K, method;
+  float tol_abs;
+  int32_t* idx;
+  float* coef;
+  int32_t* count;
+  float* resnorm;
+  int32_t* ip;
+  int32_t* path_out;
+  float* Lf;             // packed Cholesky factor per patch
+  float* yv;             // forward-substituted rhs per patch
+  float* tol;
+  int* active;
+  int* rank;
+  int* root_count;
+  int64_t N;
+};
+
+size_t score_smem_bytes(int kchunks, int npad);
+bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
+size_t staged_workspace_bytes(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method);
+cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X, int64_t N,
+                       int64_t ldx, int K, int method, float tol_abs, int32_t* idx, float* coef,
+                       int32_t* count, float* resnorm, int32_t* path, int32_t* ip, void* ws,
+                       size_t ws_bytes, cudaStream_t st);
+// host-side construction of the per-level SW128 hi/lo tables
+bool build_staged_tables(TreeHandle* t, const int32_t* child_begin, const int32_t* child_count,
+                         const float* centroids, cudaStream_t st, std::string* err);
+void free_staged_tables(TreeHandle* t);
+
+}  // namespace stmp

@@ -28,6 +28,15 @@ def P():
     return pkg
 
 
+@pytest.fixture(params=["fused", "staged"])
+def path(request):
+    """Force one encoder implementation (the C ABI 'path' option) for the test."""
+    from paper_1412_0680_b200 import _lib
+    _lib.set_option("path", {"fused": _lib.PATH_FUSED, "staged": _lib.PATH_STAGED}[request.param])
+    yield request.param
+    _lib.set_option("path", _lib.PATH_AUTO)
+
+
 def as_np(res):
     out = {k: getattr(res, k) for k in ("idx", "coef", "count", "resnorm", "ip", "path")}
     return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in out.items() if v is not None}
@@ -82,7 +91,7 @@ def test_ragged_tree_select_matches_reference():
 
 @pytest.mark.parametrize("sel_kind", ["tree", "exact"])
 @pytest.mark.parametrize("method", ["omp", "mp"])
-def test_pursuit_small_matches_reference(sel_kind, method):
+def test_pursuit_small_matches_reference(sel_kind, method, path):
     z = golden("pursuit_small.npz")
     K = int(z["K"])
     flat = flat_from_fixture(z)
@@ -104,7 +113,7 @@ def test_pursuit_small_matches_reference(sel_kind, method):
 
 @pytest.mark.parametrize("tol_tag,tol", [("deftol", None), ("tol0", 0.0), ("tol05", 0.5)])
 @pytest.mark.parametrize("method", ["omp", "mp"])
-def test_edge_cases(tol_tag, tol, method):
+def test_edge_cases(tol_tag, tol, method, path):
     z = golden("edge.npz")
     p = golden("pursuit_small.npz")
     sel = P().TreeSelector(flat_from_fixture(p), p["atoms"], 1 / 16)
@@ -180,7 +189,7 @@ def test_error_behaviour_matches_reference():
         P().encode(sel, X, 3, tol=-1.0)
 
 
-def test_encode_host_equals_device_path():
+def test_encode_host_equals_device_path(path):
     z = golden("pursuit_small.npz")
     sel = P().TreeSelector(flat_from_fixture(z), z["atoms"], 1 / 16)
     X = np.ascontiguousarray(np.tile(z["X"], (7, 1)))
@@ -219,7 +228,7 @@ def config(cid):
 @pytest.mark.parametrize("cid,rows,method", [
     (0, 10_000, "omp"), (0, 10_000, "mp"), (1, 4096, "omp"), (1, 2048, "mp"),
     (2, 1024, "omp"), (3, 2048, "omp"), (4, 128, "omp")])
-def test_config_tree_parity(cid, rows, method):
+def test_config_tree_parity(cid, rows, method, path):
     from paper_1412_0680_b200 import workloads as W
     cfg, wl, flat = config(cid)
     X = W.make_patches(wl, rows)
@@ -265,7 +274,8 @@ def test_config_exhaustive_parity(cid, rows):
     assert rep.ok, rep.summary()
 
 
-def test_config1_full_size_properties():
+@pytest.mark.parametrize("path", ["staged"], indirect=True)
+def test_config1_full_size_properties(path):
     """All 1,048,576 config-1 patches: size-independent invariants of OMP."""
     from paper_1412_0680_b200 import workloads as W
     cfg, wl, flat = config(1)
