@@ -86,17 +86,29 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
     loaded_bin = bin;
     __syncthreads();
 
-    // gather the tile's residual rows into the SW128 K-major hi/lo planes
+    // gather the tile's residual rows straight into their SW128 K-major slots
+    // with fire-and-forget cp.async (all of a thread's 16-B pieces in flight at
+    // once; rows past the tile end are zero-filled), then split hi/lo in place.
     for (int e = tid; e < kTile * F; e += kScoreThreads) {
       const int row = e / F;
       const int c = e - row * F;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (row < rows) v = __ldg(reinterpret_cast<const float4*>(a.R + (int64_t)s_rows[row] * a.ld) + c);
+      const uint32_t off = (uint32_t)(c >> 3) * (kTile * 128u) + sw128_offset(row, c & 7);
+      const bool ok = row < rows;
+      const float* src = a.R + (ok ? (int64_t)s_rows[row] * a.ld + 4 * c : 0);
+      cp_async16(a_hi_s + off, src, ok ? 16u : 0u);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    for (int e = tid; e < kTile * F; e += kScoreThreads) {
+      const int row = e / F;
+      const int c = e - row * F;
+      const uint32_t off = (uint32_t)(c >> 3) * (kTile * 128u) + sw128_offset(row, c & 7);
+      float4* ph = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Ahi) + off);
+      const float4 v = *ph;
       float4 h, l;
       h.x = tf32_hi(v.x); h.y = tf32_hi(v.y); h.z = tf32_hi(v.z); h.w = tf32_hi(v.w);
       l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
-      const uint32_t off = (uint32_t)(c >> 3) * (kTile * 128u) + sw128_offset(row, c & 7);
-      *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Ahi) + off) = h;
+      *ph = h;
       *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Alo) + off) = l;
     }
     fence_proxy_async_smem();
@@ -231,275 +243,6 @@ __global__ void scatter_kernel(int64_t N, const int* rank, const int* path_ws, i
   perm[offsets[bin] + r] = (int)p;
 }
 
-// ------------------------------------------------------------------ group helpers
-template <int G>
-__device__ __forceinline__ float group_sum(float v) {
-#pragma unroll
-  for (int o = G >> 1; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  return v;
-}
-
-// warp-aggregated rank in the single root bin for lanes with `act` (group leaders only)
-__device__ __forceinline__ int root_rank(bool act, int* counter) {
-  const unsigned m = __ballot_sync(kFull, act);
-  const int lane = threadIdx.x & 31;
-  int base = 0;
-  if (m) {
-    const int leader = __ffs(m) - 1;
-    if (lane == leader) base = atomicAdd(counter, __popc(m));
-    base = __shfl_sync(kFull, base, leader);
-  }
-  return base + __popc(m & ((1u << lane) - 1u));
-}
-
-template <int E>
-__device__ __forceinline__ void load_vec(const float* __restrict__ src, float (&v)[E]) {
-  if constexpr (E % 4 == 0) {
-#pragma unroll
-    for (int i = 0; i < E / 4; ++i) {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(src) + i);
-      v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < E / 2; ++i) {
-      const float2 q = __ldg(reinterpret_cast<const float2*>(src) + i);
-      v[2 * i] = q.x; v[2 * i + 1] = q.y;
-    }
-  }
-}
-
-template <int E>
-__device__ __forceinline__ void store_vec(float* dst, const float (&v)[E]) {
-  if constexpr (E % 4 == 0) {
-#pragma unroll
-    for (int i = 0; i < E / 4; ++i)
-      reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < E / 2; ++i) reinterpret_cast<float2*>(dst)[i] = make_float2(v[2 * i], v[2 * i + 1]);
-  }
-}
-
-template <int E>
-__device__ __forceinline__ float dot_vec(const float (&a)[E], const float (&b)[E]) {
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < E; ++i) s = fmaf(a[i], b[i], s);
-  return s;
-}
-
-// ------------------------------------------------------------------ init
-template <int G, int E>
-__global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
-  const int gpb = blockDim.x / G;
-  const int64_t p = (int64_t)blockIdx.x * gpb + threadIdx.x / G;
-  const int gl = threadIdx.x % G;
-  const bool inb = p < a.N;
-  float x[E];
-  float ss = 0.f;
-  if (inb) {
-    const float* xp = a.X + p * a.ldx;
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int d = gl * E + i;
-      x[i] = d < a.n ? __ldg(xp + d) : 0.f;
-      ss = fmaf(x[i], x[i], ss);
-    }
-    store_vec<E>(a.R + p * a.ld + gl * E, x);
-    if (a.X2) store_vec<E>(const_cast<float*>(a.X2) + p * a.ld2 + gl * E, x);
-  }
-  ss = group_sum<G>(ss);
-  const float xn = sqrtf(ss);
-  bool act = false;
-  if (inb) {
-    const float tol = a.tol_abs >= 0.f ? a.tol_abs : kRelTol * xn;
-    act = xn > tol;
-    if (gl == 0) {
-      a.tol[p] = tol;
-      a.resnorm[p] = xn;
-      a.count[p] = 0;
-      a.active[p] = act ? 1 : 0;
-      if (a.ip) { a.ip[2 * p] = 0; a.ip[2 * p + 1] = 0; }
-    }
-    for (int j = gl; j < a.K; j += G) { a.idx[p * a.K + j] = -1; a.coef[p * a.K + j] = 0.f; }
-    if (a.path_out)
-      for (int j = gl; j < a.K * a.L; j += G) a.path_out[p * a.K * a.L + j] = -1;
-  }
-  const int r = root_rank(act && gl == 0, a.root_count);
-  if (inb && gl == 0) a.rank[p] = act ? r : -1;
-}
-
-// ------------------------------------------------------------------ update
-template <int G, int E>
-__global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
-  extern __shared__ float upd_smem[];
-  const int gpb = blockDim.x / G;
-  const int grp = threadIdx.x / G;
-  const int64_t p = (int64_t)blockIdx.x * gpb + grp;
-  const int gl = threadIdx.x % G;
-  const int K = a.K;
-  float* wv = upd_smem + grp * 2 * K;   // new Cholesky row w (then reused)
-  float* cv = wv + K;                    // coefficients
-  const bool inb = p < a.N;
-  bool act = inb && a.active[p];
-  const int64_t off = (int64_t)gl * E;
-  if (act) {
-    const int t = a.count[p];
-    const int* pw = a.path_ws + p * a.L;
-    const int nodeL = pw[a.L - 1];
-    const int cb = __ldg(a.child_begin + nodeL);
-    const int cc = __ldg(a.child_count + nodeL);
-    int ipc = __ldg(a.child_count + 0);
-    for (int l = 1; l < a.L; ++l) ipc += __ldg(a.child_count + pw[l - 1]);
-    if (gl == 0 && a.ip) { a.ip[2 * p] += ipc + cc; a.ip[2 * p + 1] += ipc; }
-
-    float r[E];
-    const bool need_r = a.method == kMethodMP || cc > 1;
-    if (need_r) load_vec<E>(a.R + p * a.ld + off, r);
-    // ---- leaf choice: max |a . r| over the node's atoms, ties to the lowest atom index
-    int atom = __ldg(a.leaf_atom + cb);
-    if (cc > 1) {
-      float bestv = -1.f;
-      for (int j = 0; j < cc; ++j) {
-        const int aj = __ldg(a.leaf_atom + cb + j);
-        float av[E];
-        load_vec<E>(a.atoms + (int64_t)aj * a.ld + off, av);
-        const float m = fabsf(group_sum<G>(dot_vec<E>(av, r)));
-        if (m > bestv || (m == bestv && aj < atom)) { bestv = m; atom = aj; }
-      }
-    }
-    float av[E];
-    load_vec<E>(a.atoms + (int64_t)atom * a.ld + off, av);
-    int32_t* S = a.idx + p * K;
-    if (a.method == kMethodMP) {
-      const float s = group_sum<G>(dot_vec<E>(av, r));
-      if (s == 0.f) {
-        act = false;
-      } else {
-        float s2 = 0.f;
-#pragma unroll
-        for (int i = 0; i < E; ++i) { r[i] = fmaf(-s, av[i], r[i]); s2 = fmaf(r[i], r[i], s2); }
-        store_vec<E>(a.R + p * a.ld + off, r);
-        const float rn = sqrtf(group_sum<G>(s2));
-        if (gl == 0) {
-          S[t] = atom;
-          a.coef[p * K + t] = s;
-          a.count[p] = t + 1;
-          a.resnorm[p] = rn;
-        }
-        act = (t + 1 < K) && rn > a.tol[p];
-      }
-    } else {
-      bool dup = false;
-      for (int j = 0; j < t; ++j) dup |= (S[j] == atom);
-      float x[E];
-      load_vec<E>(a.X2 + p * a.ld2 + off, x);
-      const float bt = group_sum<G>(dot_vec<E>(av, x));
-      const float gtt = group_sum<G>(dot_vec<E>(av, av));
-      float* Lp = a.Lf + p * (int64_t)(K * (K + 1) / 2);
-      float* yp = a.yv + p * (int64_t)K;
-      float* Lt = Lp + t * (t + 1) / 2;
-      // Gram column against the current support; forward substitution row by row
-      float wsum = 0.f, gc = 0.f;
-      for (int j = 0; j < t; ++j) {
-        float sj[E];
-        load_vec<E>(a.atoms + (int64_t)S[j] * a.ld + off, sj);
-        const float g = group_sum<G>(dot_vec<E>(sj, av));
-        gc = fmaf(g, a.coef[p * K + j], gc);   // a . A_S c_prev  (score identity)
-        const float* Lj = Lp + j * (j + 1) / 2;
-        float v = g;
-        for (int k = 0; k < j; ++k) v = fmaf(-Lj[k], wv[k], v);
-        v /= Lj[j];
-        wv[j] = v;
-        wsum = fmaf(v, v, wsum);
-      }
-      const float score = bt - gc;   // a . r with r = x - A_S c (pursuit.py:217 check)
-      if (dup || score == 0.f) {
-        act = false;
-      } else {
-        const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
-        float yy = bt;
-        for (int j = 0; j < t; ++j) yy = fmaf(-wv[j], yp[j], yy);
-        yy /= dg;
-        // back substitution L^T c = y over the t+1 unknowns; row t of L is (w, dg)
-        for (int j = t; j >= 0; --j) {
-          float v = j == t ? yy : yp[j];
-          for (int k = j + 1; k <= t; ++k) {
-            const float Lkj = k == t ? wv[j] : Lp[k * (k + 1) / 2 + j];
-            v = fmaf(-Lkj, cv[k], v);
-          }
-          cv[j] = v / (j == t ? dg : Lp[j * (j + 1) / 2 + j]);
-        }
-        // residual r = x - A_S c, rebuilt with the new atom
-#pragma unroll
-        for (int i = 0; i < E; ++i) r[i] = fmaf(-cv[t], av[i], x[i]);
-        for (int j = 0; j < t; ++j) {
-          float sj[E];
-          load_vec<E>(a.atoms + (int64_t)S[j] * a.ld + off, sj);
-          const float cj = cv[j];
-#pragma unroll
-          for (int i = 0; i < E; ++i) r[i] = fmaf(-cj, sj[i], r[i]);
-        }
-        store_vec<E>(a.R + p * a.ld + off, r);
-        float s2 = 0.f;
-#pragma unroll
-        for (int i = 0; i < E; ++i) s2 = fmaf(r[i], r[i], s2);
-        const float rn = sqrtf(group_sum<G>(s2));
-        if (gl == 0) {
-          for (int j = 0; j < t; ++j) Lt[j] = wv[j];
-          Lt[t] = dg;
-          yp[t] = yy;
-          S[t] = atom;
-          for (int j = 0; j <= t; ++j) a.coef[p * K + j] = cv[j];
-          a.count[p] = t + 1;
-          a.resnorm[p] = rn;
-        }
-        act = (t + 1 < K) && rn > a.tol[p];
-      }
-    }
-    if (gl == 0) a.active[p] = act ? 1 : 0;
-  }
-  const int rr = root_rank(act && gl == 0, a.root_count);
-  if (inb && gl == 0) a.rank[p] = act ? rr : -1;
-}
-
-// ------------------------------------------------------------------ dispatch helpers
-struct GE {
-  int G, E;
-};
-
-bool pick_ge(int ld, GE& ge) {
-  static const GE table[] = {{1, 32}, {2, 32}, {2, 48}, {4, 32}, {4, 40}, {4, 48}, {8, 32}, {8, 40},
-                             {8, 48}, {16, 32}, {16, 40}, {16, 48}, {32, 32}, {32, 40}, {32, 48}, {32, 50}};
-  for (const GE& g : table)
-    if (g.G * g.E == ld) { ge = g; return true; }
-  return false;
-}
-
-#define STMP_GE_SWITCH(ge, KERNEL, ...)                                                  \
-  do {                                                                                   \
-    switch (ge.G * 1000 + ge.E) {                                                        \
-      case 1032: KERNEL<1, 32> __VA_ARGS__; break;                                       \
-      case 2032: KERNEL<2, 32> __VA_ARGS__; break;                                       \
-      case 2048: KERNEL<2, 48> __VA_ARGS__; break;                                       \
-      case 4032: KERNEL<4, 32> __VA_ARGS__; break;                                       \
-      case 4040: KERNEL<4, 40> __VA_ARGS__; break;                                       \
-      case 4048: KERNEL<4, 48> __VA_ARGS__; break;                                       \
-      case 8032: KERNEL<8, 32> __VA_ARGS__; break;                                       \
-      case 8040: KERNEL<8, 40> __VA_ARGS__; break;                                       \
-      case 8048: KERNEL<8, 48> __VA_ARGS__; break;                                       \
-      case 16032: KERNEL<16, 32> __VA_ARGS__; break;                                     \
-      case 16040: KERNEL<16, 40> __VA_ARGS__; break;                                     \
-      case 16048: KERNEL<16, 48> __VA_ARGS__; break;                                     \
-      case 32032: KERNEL<32, 32> __VA_ARGS__; break;                                     \
-      case 32040: KERNEL<32, 40> __VA_ARGS__; break;                                     \
-      case 32048: KERNEL<32, 48> __VA_ARGS__; break;                                     \
-      case 32050: KERNEL<32, 50> __VA_ARGS__; break;                                     \
-      default: return cudaErrorInvalidValue;                                             \
-    }                                                                                    \
-  } while (0)
-
 }  // namespace
 
 size_t score_smem_bytes(int kchunks, int npad) {
@@ -509,8 +252,8 @@ size_t score_smem_bytes(int kchunks, int npad) {
 
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method) {
   if (t == nullptr || (method != kMethodMP && method != kMethodOMP)) return false;
-  GE ge;
-  if (!pick_ge(d->ld, ge)) return false;
+  UpdateCfg uc;
+  if (!update_config(d->ld, K, uc)) return false;
   if (t->staged_tables.empty()) return false;
   if (K > 64) return false;
   return true;
@@ -518,8 +261,8 @@ bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int metho
 
 bool build_staged_tables(TreeHandle* t, const int32_t* child_begin, const int32_t* child_count,
                          const float* centroids, cudaStream_t st, std::string* err) {
-  GE ge;
-  if (!pick_ge(t->ld, ge)) return false;
+  UpdateCfg uc;
+  if (!update_config(t->ld, 1, uc)) return false;
   const int L = t->levels;
   const int kch = t->ld / 32;
   std::vector<StagedLevel> levels(L);
@@ -642,8 +385,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)sumbins * 4, st);
   if (e != cudaSuccess) return e;
 
-  GE ge;
-  pick_ge(d->ld, ge);
+  UpdateCfg uc;
+  update_config(d->ld, K, uc);
   UpdateArgs u{};
   u.X = X; u.ldx = ldx; u.n = d->n; u.R = R; u.ld = d->ld;
   u.X2 = Xpad; u.ld2 = d->ld;  // OMP rebuilds r from this padded copy of x
@@ -653,12 +396,11 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   u.ip = ip; u.path_out = path; u.Lf = Lf; u.yv = yv; u.tol = tol; u.active = active;
   u.rank = rank; u.root_count = counts; u.N = N;
 
-  const int gpb = 128 / ge.G;
+  const int gpb = 128 / uc.G;
   const int ublocks = (int)((N + gpb - 1) / gpb);
   // init writes the padded x into R (and into Xpad for OMP, whose update
   // rebuilds r = x - A_S c every iteration)
-  STMP_GE_SWITCH(ge, init_kernel, <<<ublocks, 128, 0, st>>>(u));
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = launch_init(uc, u, ublocks, st)) != cudaSuccess) return e;
 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -691,8 +433,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       score_tc_kernel<<<grid, kScoreThreads, smem, st>>>(s);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    STMP_GE_SWITCH(ge, update_kernel, <<<ublocks, 128, usmem, st>>>(u));
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_update(uc, u, ublocks, usmem, st)) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }

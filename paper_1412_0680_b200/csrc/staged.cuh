@@ -56,6 +56,17 @@ struct UpdateArgs {
   int64_t N;
 };
 
+struct UpdateCfg {
+  int G = 0;   // lanes per patch
+  int E = 0;   // row elements per lane (G * E == ld)
+  int KC = 0;  // support atoms cached in registers (0: reload)
+};
+
+bool update_config(int ld, int K, UpdateCfg& c);
+cudaError_t launch_init(const UpdateCfg& c, const UpdateArgs& a, int blocks, cudaStream_t st);
+cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, size_t smem,
+                          cudaStream_t st);
+
 size_t score_smem_bytes(int kchunks, int npad);
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
 size_t staged_workspace_bytes(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method);
