@@ -167,6 +167,16 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
       a.path_ws[(int64_t)p * a.L + a.level] = child;
       if (a.path_out) a.path_out[((int64_t)p * a.K + a.count[p]) * a.L + a.level] = child;
       if (a.next_counts) local = atomicAdd(&s_hist[best], 1);
+      int leaf_ips = 0;
+      if (a.leaf_sel) {  // last level: resolve single-atom leaves here (pursuit.py:155-162)
+        const int lc = __ldg(a.child_count + child);
+        a.leaf_sel[p] = lc == 1 ? __ldg(a.leaf_atom + __ldg(a.child_begin + child)) : -1 - child;
+        leaf_ips = lc;
+      }
+      if (a.ip) {  // ScoreCounter: cc centroids at this level (+ the leaf atoms)
+        a.ip[2 * (int64_t)p] += cc + leaf_ips;
+        a.ip[2 * (int64_t)p + 1] += cc;
+      }
     }
     if (a.next_counts) {
       __syncthreads();
@@ -337,6 +347,7 @@ size_t staged_workspace_bytes(const DictHandle* d, const TreeHandle* t, int64_t 
   add((size_t)N * 4);                      // rank
   add((size_t)N * 4);                      // perm
   add((size_t)N * L * 4);                  // path_ws
+  add((size_t)N * 4);                      // leaf_sel
   add((size_t)N * K * (K + 1) / 2 * 4);    // Cholesky factors
   add((size_t)N * K * 4);                  // y
   add((size_t)sumbins * 4);                // per-level bin counts
@@ -374,6 +385,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   int* rank = (int*)take((size_t)N * 4);
   int* perm = (int*)take((size_t)N * 4);
   int* path_ws = (int*)take((size_t)N * L * 4);
+  int* leaf_sel = (int*)take((size_t)N * 4);
   float* Lf = (float*)take((size_t)N * K * (K + 1) / 2 * 4);
   float* yv = (float*)take((size_t)N * K * 4);
   int* counts = (int*)take((size_t)sumbins * 4);
@@ -394,7 +406,9 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   u.leaf_atom = t->leaf_atom; u.L = L; u.path_ws = path_ws; u.K = K; u.method = method;
   u.tol_abs = tol_abs; u.idx = idx; u.coef = coef; u.count = count; u.resnorm = resnorm;
   u.ip = ip; u.path_out = path; u.Lf = Lf; u.yv = yv; u.tol = tol; u.active = active;
-  u.rank = rank; u.root_count = counts; u.N = N;
+  u.rank = rank; u.root_count = counts; u.N = N; u.leaf_sel = leaf_sel;
+  // stage the support atoms in shared memory when 16 patch groups fit comfortably
+  u.cache_atoms = update_smem_bytes(uc, K, d->ld, true) <= 96 * 1024 ? 1 : 0;
 
   const int gpb = 128 / uc.G;
   const int ublocks = (int)((N + gpb - 1) / gpb);
@@ -406,7 +420,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int scatter_blocks = (int)((N + 255) / 256);
-  const size_t usmem = (size_t)gpb * 2 * K * 4;
+  const size_t usmem = update_smem_bytes(uc, K, d->ld, u.cache_atoms != 0);
 
   for (int it = 0; it < K; ++it) {
     for (int l = 0; l < L; ++l) {
@@ -420,10 +434,12 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       s.table = t->staged_tables[l]; s.npad = lv.npad; s.kchunks = d->ld / 32; s.tmem_cols = lv.tmem_cols;
       s.level = l; s.level_base = (int)t->level_offsets[l]; s.child_begin = t->child_begin;
       s.child_count = t->child_count; s.path_ws = path_ws; s.path_out = path; s.count = count;
-      s.K = K; s.L = L; s.rank = rank;
+      s.K = K; s.L = L; s.rank = rank; s.ip = ip; s.leaf_atom = t->leaf_atom;
       if (l + 1 < L) {
         s.next_counts = counts + bin_off[l + 1];
         s.next_base = (int)t->level_offsets[l + 1];
+      } else {
+        s.leaf_sel = leaf_sel;
       }
       const size_t smem = score_smem_bytes(s.kchunks, lv.npad);
       e = cudaFuncSetAttribute(score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -2,25 +2,30 @@
 // tolerance, root bucketing) and update (leaf choice + MP step or OMP refit).
 //
 // A group of G lanes owns one patch; lane gl holds elements [gl*E, gl*E+E) of
-// the padded row.  For OMP the support atoms are loaded once per iteration as
-// one batch into registers (KC-entry cache) and reused by both the Gram
-// column and the residual rebuild, so an iteration costs two dependent
-// global round trips instead of 2t.  The small triangular solves run
-// redundantly on the G lanes (no shuffles); dot products are group
-// reductions.  Semantics: pkg/src/stmp/pursuit.py:207-221 (MP) and the
+// the padded row.  For OMP the patch's solver state and its support atoms are
+// pulled into shared memory as one batch of independent (async) loads and
+// reused by both the Gram column and the residual rebuild, so an iteration
+// costs a few dependent global round trips instead of 2t.  The small
+// triangular solves run redundantly on the G lanes (no shuffles); dot
+// products are group reductions.  Semantics: pkg/src/stmp/pursuit.py:207-221 (MP) and the
 // SURVEY §8c OMP restatement over omp_refit (pursuit.py:235-250).
 #include "common.cuh"
 #include "kernels.cuh"
+#include "sm100.cuh"
 #include "staged.cuh"
 
 namespace stmp {
 
 namespace {
 
+// Sum over the G lanes of this patch group.  The mask names only the group's
+// own lanes: groups of one warp diverge (different patches stop at different
+// iterations), so a full-warp mask would wait for lanes that never arrive.
 template <int G>
 __device__ __forceinline__ float group_sum(float v) {
+  const unsigned mask = G >= 32 ? kFull : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
 #pragma unroll
-  for (int o = G >> 1; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  for (int o = G >> 1; o; o >>= 1) v += __shfl_xor_sync(mask, v, o);
   return v;
 }
 
@@ -123,48 +128,90 @@ __global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
 }
 
 // ------------------------------------------------------------------ update
-template <int G, int E, int KC>
+// Shared scratch per patch group (floats):
+//   S[K] | c[K] | y[K] | L[K(K+1)/2] | w[K] | cn[K] | support atoms [K][ld] (optional)
+__host__ __device__ inline int upd_scalar_floats(int K) { return (5 * K + K * (K + 1) / 2 + 3) & ~3; }
+
+template <int E>
+__device__ __forceinline__ void load_gen(const float* src, float (&v)[E]) {
+  if constexpr (E % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < E / 4; ++i) {
+      const float4 q = reinterpret_cast<const float4*>(src)[i];
+      v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = src[i];
+  }
+}
+
+template <int G, int E>
 __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
-  extern __shared__ float upd_smem[];
+  extern __shared__ __align__(16) float upd_smem[];
   const int gpb = blockDim.x / G;
   const int grp = threadIdx.x / G;
   const int64_t p = (int64_t)blockIdx.x * gpb + grp;
   const int gl = threadIdx.x % G;
+  const unsigned gmask = G >= 32 ? kFull : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
   const int K = a.K;
-  float* wv = upd_smem + grp * 2 * K;   // new Cholesky row w (identical on the G lanes)
-  float* cv = wv + K;                    // refit coefficients
+  const int sfl = upd_scalar_floats(K);
+  float* gs = upd_smem + grp * (sfl + (a.cache_atoms ? K * a.ld : 0));
+  int* S_s = reinterpret_cast<int*>(gs);
+  float* c_s = gs + K;
+  float* y_s = c_s + K;
+  float* L_s = y_s + K;
+  float* w_s = L_s + K * (K + 1) / 2;
+  float* cn_s = w_s + K;
+  float* A_s = gs + sfl;
   const bool inb = p < a.N;
   bool act = inb && a.active[p];
   const int64_t off = (int64_t)gl * E;
   if (act) {
     const int t = a.count[p];
-    const int* pw = a.path_ws + p * a.L;
-    const int nodeL = pw[a.L - 1];
-    const int cb = __ldg(a.child_begin + nodeL);
-    const int cc = __ldg(a.child_count + nodeL);
-    int ipc = __ldg(a.child_count + 0);
-    for (int l = 1; l < a.L; ++l) ipc += __ldg(a.child_count + pw[l - 1]);
-    if (gl == 0 && a.ip) { a.ip[2 * p] += ipc + cc; a.ip[2 * p + 1] += ipc; }
-    int32_t* S = a.idx + p * K;
-
-    float r[E];
-    const bool need_r = a.method == kMethodMP || cc > 1;
-    if (need_r) load_vec<E>(a.R + p * a.ld + off, r);
-    // ---- leaf choice: max |a . r| over the node's atoms, ties to the lowest atom index
-    int atom = __ldg(a.leaf_atom + cb);
-    if (cc > 1) {
+    const int lsel = a.leaf_sel[p];
+    const bool omp = a.method == kMethodOMP;
+    float r[E], x[E];
+    if (!omp || lsel < 0) load_vec<E>(a.R + p * a.ld + off, r);
+    if (omp) {
+      load_vec<E>(a.X2 + p * a.ld2 + off, x);
+      // the patch's solver state -> shared, as one batch of independent loads
+      for (int i = gl; i < t; i += G) {
+        S_s[i] = a.idx[p * K + i];
+        c_s[i] = a.coef[p * K + i];
+        y_s[i] = a.yv[p * K + i];
+      }
+      const float* Lp = a.Lf + p * (int64_t)(K * (K + 1) / 2);
+      for (int i = gl; i < t * (t + 1) / 2; i += G) L_s[i] = Lp[i];
+      __syncwarp(gmask);
+      if (a.cache_atoms) {  // support atoms -> shared with async copies, all in flight at once
+        const int F = a.ld >> 2;
+        for (int e = gl; e < t * F; e += G) {
+          const int j = e / F, q = e - j * F;
+          sm100::cp_async16(sm100::smem_u32(A_s + j * a.ld + 4 * q), a.atoms + (int64_t)S_s[j] * a.ld + 4 * q, 16u);
+        }
+      }
+    }
+    // leaf choice: single-atom leaves were resolved by the last score pass;
+    // otherwise max |a . r| over the node's atoms, ties to the lowest atom index
+    int atom = lsel;
+    if (lsel < 0) {
+      const int node = -1 - lsel;
+      const int cb = __ldg(a.child_begin + node), cc = __ldg(a.child_count + node);
       float bestv = -1.f;
+      atom = __ldg(a.leaf_atom + cb);
       for (int j = 0; j < cc; ++j) {
         const int aj = __ldg(a.leaf_atom + cb + j);
-        float av[E];
-        load_vec<E>(a.atoms + (int64_t)aj * a.ld + off, av);
-        const float m = fabsf(group_sum<G>(dot_vec<E>(av, r)));
+        float v[E];
+        load_vec<E>(a.atoms + (int64_t)aj * a.ld + off, v);
+        const float m = fabsf(group_sum<G>(dot_vec<E>(v, r)));
         if (m > bestv || (m == bestv && aj < atom)) { bestv = m; atom = aj; }
       }
     }
     float av[E];
     load_vec<E>(a.atoms + (int64_t)atom * a.ld + off, av);
-    if (a.method == kMethodMP) {
+    int32_t* S = a.idx + p * K;
+    if (!omp) {
       const float s = group_sum<G>(dot_vec<E>(av, r));
       if (s == 0.f) {
         act = false;   // pursuit.py:217
@@ -183,48 +230,25 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
         act = (t + 1 < K) && rn > a.tol[p];
       }
     } else {
-      // support indices and (when cached) the support atoms, all loads issued together
-      int sidx[KC > 0 ? KC : 1];
-      float sat[KC > 0 ? KC : 1][E];
+      if (a.cache_atoms) sm100::cp_async_wait_all();
+      __syncwarp(gmask);
       bool dup = false;
-      if constexpr (KC > 0) {
-#pragma unroll
-        for (int j = 0; j < KC; ++j) sidx[j] = j < t ? S[j] : -1;
-#pragma unroll
-        for (int j = 0; j < KC; ++j)
-          if (j < t) load_vec<E>(a.atoms + (int64_t)sidx[j] * a.ld + off, sat[j]);
-#pragma unroll
-        for (int j = 0; j < KC; ++j) dup |= (sidx[j] == atom);
-      } else {
-        for (int j = 0; j < t; ++j) dup |= (S[j] == atom);
-      }
-      float x[E];
-      load_vec<E>(a.X2 + p * a.ld2 + off, x);
+      for (int j = 0; j < t; ++j) dup |= (S_s[j] == atom);
       const float bt = group_sum<G>(dot_vec<E>(av, x));
       const float gtt = group_sum<G>(dot_vec<E>(av, av));
-      const float* Lp = a.Lf + p * (int64_t)(K * (K + 1) / 2);
-      const float* yp = a.yv + p * (int64_t)K;
-      // Gram column of the new atom against the support, forward substitution
+      // Gram column of the new atom against the support + forward substitution
       float wsum = 0.f, gc = 0.f;
       for (int j = 0; j < t; ++j) {
-        float g;
-        if constexpr (KC > 0) {
-          float part = 0.f;
-#pragma unroll
-          for (int q = 0; q < KC; ++q)
-            if (q == j) part = dot_vec<E>(sat[q], av);
-          g = group_sum<G>(part);
-        } else {
-          float sj[E];
-          load_vec<E>(a.atoms + (int64_t)S[j] * a.ld + off, sj);
-          g = group_sum<G>(dot_vec<E>(sj, av));
-        }
-        gc = fmaf(g, a.coef[p * K + j], gc);   // a . (A_S c_prev)
-        const float* Lj = Lp + j * (j + 1) / 2;
+        float sv[E];
+        if (a.cache_atoms) load_gen<E>(A_s + j * a.ld + off, sv);
+        else load_vec<E>(a.atoms + (int64_t)S_s[j] * a.ld + off, sv);
+        const float g = group_sum<G>(dot_vec<E>(sv, av));
+        gc = fmaf(g, c_s[j], gc);   // a . (A_S c_prev)
+        const float* Lj = L_s + j * (j + 1) / 2;
         float v = g;
-        for (int k = 0; k < j; ++k) v = fmaf(-Lj[k], wv[k], v);
+        for (int k = 0; k < j; ++k) v = fmaf(-Lj[k], w_s[k], v);
         v /= Lj[j];
-        wv[j] = v;
+        w_s[j] = v;
         wsum = fmaf(v, v, wsum);
       }
       const float score = bt - gc;   // a . r for r = x - A_S c_prev (pursuit.py:217 check)
@@ -233,50 +257,42 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
       } else {
         const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
         float yy = bt;
-        for (int j = 0; j < t; ++j) yy = fmaf(-wv[j], yp[j], yy);
+        for (int j = 0; j < t; ++j) yy = fmaf(-w_s[j], y_s[j], yy);
         yy /= dg;
         // back substitution L^T c = y; row t of L is (w, dg)
         for (int j = t; j >= 0; --j) {
-          float v = j == t ? yy : yp[j];
+          float v = j == t ? yy : y_s[j];
           for (int k = j + 1; k <= t; ++k) {
-            const float Lkj = k == t ? wv[j] : Lp[k * (k + 1) / 2 + j];
-            v = fmaf(-Lkj, cv[k], v);
+            const float Lkj = k == t ? w_s[j] : L_s[k * (k + 1) / 2 + j];
+            v = fmaf(-Lkj, cn_s[k], v);
           }
-          cv[j] = v / (j == t ? dg : Lp[j * (j + 1) / 2 + j]);
+          cn_s[j] = v / (j == t ? dg : L_s[j * (j + 1) / 2 + j]);
         }
         // residual r = x - A_S c with the new atom
+        const float ct = cn_s[t];
 #pragma unroll
-        for (int i = 0; i < E; ++i) r[i] = fmaf(-cv[t], av[i], x[i]);
-        if constexpr (KC > 0) {
+        for (int i = 0; i < E; ++i) r[i] = fmaf(-ct, av[i], x[i]);
+        for (int j = 0; j < t; ++j) {
+          float sv[E];
+          if (a.cache_atoms) load_gen<E>(A_s + j * a.ld + off, sv);
+          else load_vec<E>(a.atoms + (int64_t)S_s[j] * a.ld + off, sv);
+          const float cj = cn_s[j];
 #pragma unroll
-          for (int j = 0; j < KC; ++j) {
-            if (j < t) {
-              const float cj = cv[j];
-#pragma unroll
-              for (int i = 0; i < E; ++i) r[i] = fmaf(-cj, sat[j][i], r[i]);
-            }
-          }
-        } else {
-          for (int j = 0; j < t; ++j) {
-            float sj[E];
-            load_vec<E>(a.atoms + (int64_t)S[j] * a.ld + off, sj);
-            const float cj = cv[j];
-#pragma unroll
-            for (int i = 0; i < E; ++i) r[i] = fmaf(-cj, sj[i], r[i]);
-          }
+          for (int i = 0; i < E; ++i) r[i] = fmaf(-cj, sv[i], r[i]);
         }
         store_vec<E>(a.R + p * a.ld + off, r);
         float s2 = 0.f;
 #pragma unroll
         for (int i = 0; i < E; ++i) s2 = fmaf(r[i], r[i], s2);
         const float rn = sqrtf(group_sum<G>(s2));
+        float* Lt = a.Lf + p * (int64_t)(K * (K + 1) / 2) + t * (t + 1) / 2;
+        for (int i = gl; i <= t; i += G) {
+          Lt[i] = i < t ? w_s[i] : dg;
+          a.coef[p * K + i] = cn_s[i];
+        }
         if (gl == 0) {
-          float* Lt = a.Lf + p * (int64_t)(K * (K + 1) / 2) + t * (t + 1) / 2;
-          for (int j = 0; j < t; ++j) Lt[j] = wv[j];
-          Lt[t] = dg;
           a.yv[p * (int64_t)K + t] = yy;
           S[t] = atom;
-          for (int j = 0; j <= t; ++j) a.coef[p * K + j] = cv[j];
           a.count[p] = t + 1;
           a.resnorm[p] = rn;
         }
@@ -301,8 +317,6 @@ bool update_config(int ld, int K, UpdateCfg& c) {
   c.G = G;
   c.E = ld / G;
   c.KC = 0;
-  if (c.E <= 8 && K <= 16) c.KC = K <= 8 ? 8 : 16;
-  else if (c.E <= 16 && K <= 8) c.KC = 8;
   return true;
 }
 
@@ -321,16 +335,25 @@ cudaError_t launch_init(const UpdateCfg& c, const UpdateArgs& a, int blocks, cud
 }
 
 cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, size_t smem, cudaStream_t st) {
-  switch ((c.G * 1000 + c.E) * 100 + c.KC) {
-#define STMP_UPD_CASE(g, e)                                                                     \
-  case (g * 1000 + e) * 100 + 0: update_kernel<g, e, 0><<<blocks, 128, smem, st>>>(a); break;  \
-  case (g * 1000 + e) * 100 + 8: update_kernel<g, e, (e <= 16 ? 8 : 0)><<<blocks, 128, smem, st>>>(a); break; \
-  case (g * 1000 + e) * 100 + 16: update_kernel<g, e, (e <= 8 ? 16 : 0)><<<blocks, 128, smem, st>>>(a); break;
+  switch (c.G * 1000 + c.E) {
+#define STMP_UPD_CASE(g, e)                                                         \
+  case g * 1000 + e: {                                                              \
+    cudaError_t err = cudaFuncSetAttribute(update_kernel<g, e>,                     \
+        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                    \
+    if (err != cudaSuccess) return err;                                             \
+    update_kernel<g, e><<<blocks, 128, smem, st>>>(a);                              \
+    break;                                                                          \
+  }
     STMP_UPD_CASES(STMP_UPD_CASE)
 #undef STMP_UPD_CASE
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+size_t update_smem_bytes(const UpdateCfg& c, int K, int ld, bool cache_atoms) {
+  const int groups = 128 / c.G;
+  return (size_t)groups * (upd_scalar_floats(K) + (cache_atoms ? K * ld : 0)) * 4;
 }
 
 }  // namespace stmp

@@ -23,6 +23,9 @@ struct ScoreArgs {
   int* next_counts;      // bin counters of the next level (nullptr at the last level)
   int next_base;
   int* rank;             // rank of the patch inside its next-level bin
+  int32_t* ip;           // optional per-patch {inner products, centroid inner products}
+  int* leaf_sel;         // last level: the single leaf atom, or -1-node for multi-atom leaves
+  const int* leaf_atom;
 };
 
 struct UpdateArgs {
@@ -53,6 +56,8 @@ struct UpdateArgs {
   int* active;
   int* rank;
   int* root_count;
+  const int* leaf_sel;   // written by the last score pass
+  int cache_atoms;       // stage the support atoms in shared memory
   int64_t N;
 };
 
@@ -66,6 +71,7 @@ bool update_config(int ld, int K, UpdateCfg& c);
 cudaError_t launch_init(const UpdateCfg& c, const UpdateArgs& a, int blocks, cudaStream_t st);
 cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, size_t smem,
                           cudaStream_t st);
+size_t update_smem_bytes(const UpdateCfg& c, int K, int ld, bool cache_atoms);
 
 size_t score_smem_bytes(int kchunks, int npad);
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
