@@ -205,7 +205,7 @@ int stmp_tree_create(const stmp_dict* d, int32_t levels, const int32_t* branchin
     return cuda_fail(e, "tree upload");
   }
   std::string berr;
-  if (!stmp::build_staged_tables(t, child_begin, child_count, centroids, s, &berr) && !berr.empty()) {
+  if (!stmp::build_staged_tables(t, child_begin, child_count, centroids, leaf_atom, s, &berr) && !berr.empty()) {
     stmp_tree_free(t);
     return fail(STMP_ECUDA, "staged table upload: %s", berr.c_str());
   }

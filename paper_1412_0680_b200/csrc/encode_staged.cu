@@ -8,11 +8,13 @@
 //                           tensor cores (tcgen05.mma kind::tf32, 3xTF32 split
 //                           for fp32 accuracy, accumulator in TMEM), argmax
 //                           epilogue straight out of TMEM (one thread per
-//                           patch row), bucket the winners for the next level;
-//   update: leaf choice + MP step or OMP incremental-Cholesky refit, residual
-//           rebuilt and written once.
+//                           patch row), count the winners for the next level;
+//   update: MP step or OMP incremental-Cholesky refit, residual rebuilt and
+//           written once (encode_update.cu).
 // Reference semantics are the same as encode_fused.cu (see its header).
 #include <cub/block/block_scan.cuh>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -28,6 +30,27 @@ namespace {
 constexpr int kTile = 128;          // patches per work item (= UMMA M)
 constexpr int kScoreThreads = 128;  // 4 warps: warp w owns TMEM lanes 32w..32w+31
 
+// Per-bin table block: [kchunks][hi|lo][npad rows x 128 B] SW128, then (last
+// level only) npad ints leaf_info (single leaf atom, or -1-child) and npad
+// ints leaf count.
+__host__ __device__ inline uint32_t table_bytes(int kch, int npad, bool last) {
+  return (uint32_t)kch * 2u * npad * 128u + (last ? 8u * npad : 0u);
+}
+
+__device__ __forceinline__ void issue_gather(const ScoreArgs& a, const int* rows_ids, int rows,
+                                             uint32_t a_hi_s, int tid) {
+  const int F = a.ld >> 2;
+  for (int e = tid; e < kTile * F; e += kScoreThreads) {
+    const int row = e / F;
+    const int c = e - row * F;
+    const uint32_t off = (uint32_t)(c >> 3) * (kTile * 128u) + sw128_offset(row, c & 7);
+    const bool ok = row < rows;
+    const float* src = a.R + (ok ? (int64_t)rows_ids[row] * a.ld + 4 * c : 0);
+    cp_async16(a_hi_s + off, src, ok ? 16u : 0u);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ score (tcgen05)
 __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -37,15 +60,17 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
   const int warp = tid >> 5;
   const int kch = a.kchunks;
   const int npad = a.npad;
+  const bool last = a.leaf_sel != nullptr;
   float* Ahi = reinterpret_cast<float*>(base);
   float* Alo = Ahi + kch * kTile * 32;
-  float* Btab = Alo + kch * kTile * 32;
-  const uint32_t tab_bytes = (uint32_t)kch * 2u * npad * 128u;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(Btab) + tab_bytes);
+  uint8_t* Btab = reinterpret_cast<uint8_t*>(Alo + kch * kTile * 32);
+  const uint32_t tbytes = table_bytes(kch, npad, last);
+  const int* s_leaf_info = reinterpret_cast<const int*>(Btab + (size_t)kch * 2 * npad * 128);
+  const int* s_leaf_cnt = s_leaf_info + npad;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Btab + ((tbytes + 15u) & ~15u));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
-  int* s_rows = reinterpret_cast<int*>(tmem_slot + 4);
-  int* s_hist = s_rows + kTile;      // [npad] local counts of the winning child
-  int* s_base = s_hist + 256;        // [npad] global base rank per child
+  int* s_rows = reinterpret_cast<int*>(tmem_slot + 4);  // [2][kTile] double-buffered patch ids
+  int* s_hist = s_rows + 2 * kTile;                      // [256] local counts of the winning child
 
   if (warp == 0) tmem_alloc(tmem_slot, a.tmem_cols);
   if (tid == 0) {
@@ -63,42 +88,39 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
   const int per = (num_items + gridDim.x - 1) / gridDim.x;
   const int i0 = blockIdx.x * per;
   const int i1 = min(num_items, i0 + per);
-  int loaded_bin = -1;
-  uint32_t tab_phase = 0, mma_phase = 0;
-  const int F = a.ld >> 2;  // float4 per residual row
   const uint32_t idesc = idesc_tf32(kTile, npad);
   const uint32_t a_hi_s = smem_u32(Ahi), a_lo_s = smem_u32(Alo), b_s = smem_u32(Btab);
+  const int F = a.ld >> 2;
+  uint32_t tab_phase = 0, mma_phase = 0;
+  int loaded_bin = -1;
+
+  // prologue: first item's rows, table and gather in flight
+  int4 it = i0 < i1 ? a.items[i0] : make_int4(0, 0, 0, 0);
+  if (i0 < i1) {
+    if (tid < it.z) s_rows[tid] = a.perm[it.y + tid];
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bars[0], tbytes);
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(a.table) + (size_t)it.x * tbytes;
+      for (uint32_t off = 0; off < tbytes; off += 65536u)
+        bulk_g2s(Btab + off, src + off, min(65536u, tbytes - off), &bars[0]);
+    }
+    loaded_bin = it.x;
+    __syncthreads();
+    issue_gather(a, s_rows, it.z, a_hi_s, tid);
+  }
+  bool table_pending = i0 < i1;
 
   for (int item = i0; item < i1; ++item) {
-    const int4 it = a.items[item];
-    const int bin = it.x, start = it.y, rows = it.z;
-    if (tid < rows) s_rows[tid] = a.perm[start + tid];
-    const bool new_tab = bin != loaded_bin;
-    if (new_tab && tid == 0) {
-      mbar_arrive_expect_tx(&bars[0], tab_bytes);
-      const uint8_t* src = reinterpret_cast<const uint8_t*>(a.table) + (size_t)bin * tab_bytes;
-      // chunked bulk copies (each <= 64 KB)
-      for (uint32_t off = 0; off < tab_bytes; off += 65536u) {
-        const uint32_t sz = min(65536u, tab_bytes - off);
-        bulk_g2s(reinterpret_cast<uint8_t*>(Btab) + off, src + off, sz, &bars[0]);
-      }
-    }
-    loaded_bin = bin;
-    __syncthreads();
+    const int buf = (item - i0) & 1;
+    const int* rows_ids = s_rows + buf * kTile;
+    const int bin = it.x, rows = it.z;
+    const int gnode = a.level_base + bin;
+    const int cb = __ldg(a.child_begin + gnode);
+    const int cc = __ldg(a.child_count + gnode);
 
-    // gather the tile's residual rows straight into their SW128 K-major slots
-    // with fire-and-forget cp.async (all of a thread's 16-B pieces in flight at
-    // once; rows past the tile end are zero-filled), then split hi/lo in place.
-    for (int e = tid; e < kTile * F; e += kScoreThreads) {
-      const int row = e / F;
-      const int c = e - row * F;
-      const uint32_t off = (uint32_t)(c >> 3) * (kTile * 128u) + sw128_offset(row, c & 7);
-      const bool ok = row < rows;
-      const float* src = a.R + (ok ? (int64_t)s_rows[row] * a.ld + 4 * c : 0);
-      cp_async16(a_hi_s + off, src, ok ? 16u : 0u);
-    }
-    cp_async_wait_all();
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
+    // split the gathered rows into tf32 hi / lo planes in place
     for (int e = tid; e < kTile * F; e += kScoreThreads) {
       const int row = e / F;
       const int c = e - row * F;
@@ -115,7 +137,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
     __syncthreads();
 
     if (tid == 0) {
-      if (new_tab) {
+      if (table_pending) {
         mbar_wait(&bars[0], tab_phase);
         tab_phase ^= 1u;
       }
@@ -135,15 +157,21 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
       }
       mma_commit(&bars[1]);
     }
+    table_pending = false;
     __syncwarp();
     mbar_wait(&bars[1], mma_phase);
     mma_phase ^= 1u;
     tc_fence_after();
 
-    // epilogue: thread = patch row, argmax |score| over the node's children
-    const int gnode = a.level_base + bin;
-    const int cb = __ldg(a.child_begin + gnode);
-    const int cc = __ldg(a.child_count + gnode);
+    // A planes are free again: start the next item's gather (and its table if
+    // the bin changes) before this item's epilogue, so the loads overlap it
+    int4 nit = make_int4(0, 0, 0, 0);
+    const bool has_next = item + 1 < i1;
+    int nperm = 0;
+    if (has_next) {
+      nit = a.items[item + 1];
+      if (tid < nit.z) nperm = a.perm[nit.y + tid];  // consumed after the argmax
+    }
     int best = 0;
     float bestv = -1.f;
     for (int col0 = 0; col0 < npad; col0 += 32) {
@@ -160,36 +188,50 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
     }
     const int row = tid;
     const bool valid = row < rows;
-    const int p = valid ? s_rows[row] : 0;
+    const int p = valid ? rows_ids[row] : 0;
     const int child = cb + best;
-    int local = 0;
+    int leaf_info = 0, leaf_cnt = 0;
+    if (last && valid) {  // read before a table refill overwrites the block
+      leaf_info = s_leaf_info[best];
+      leaf_cnt = s_leaf_cnt[best];
+    }
+    if (has_next && tid < nit.z) s_rows[(buf ^ 1) * kTile + tid] = nperm;
+    __syncthreads();  // s_rows of the next item visible; leaf metadata read
+    if (has_next) {
+      const bool new_tab = nit.x != loaded_bin;
+      if (new_tab && tid == 0) {
+        mbar_arrive_expect_tx(&bars[0], tbytes);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.table) + (size_t)nit.x * tbytes;
+        for (uint32_t off = 0; off < tbytes; off += 65536u)
+          bulk_g2s(Btab + off, src + off, min(65536u, tbytes - off), &bars[0]);
+      }
+      table_pending = new_tab;
+      loaded_bin = nit.x;
+      issue_gather(a, s_rows + (buf ^ 1) * kTile, nit.z, a_hi_s, tid);
+    }
+
     if (valid) {
       a.path_ws[(int64_t)p * a.L + a.level] = child;
       if (a.path_out) a.path_out[((int64_t)p * a.K + a.count[p]) * a.L + a.level] = child;
-      if (a.next_counts) local = atomicAdd(&s_hist[best], 1);
-      int leaf_ips = 0;
-      if (a.leaf_sel) {  // last level: resolve single-atom leaves here (pursuit.py:155-162)
-        const int lc = __ldg(a.child_count + child);
-        a.leaf_sel[p] = lc == 1 ? __ldg(a.leaf_atom + __ldg(a.child_begin + child)) : -1 - child;
-        leaf_ips = lc;
-      }
-      if (a.ip) {  // ScoreCounter: cc centroids at this level (+ the leaf atoms)
-        a.ip[2 * (int64_t)p] += cc + leaf_ips;
-        a.ip[2 * (int64_t)p + 1] += cc;
+      if (a.next_counts) atomicAdd(&s_hist[best], 1);
+      if (last) a.leaf_sel[p] = leaf_info;
+      if (a.ip) {  // ScoreCounter: cc centroids at this level (+ the leaf atoms), fire-and-forget
+        atomicAdd(&a.ip[2 * (int64_t)p], cc + leaf_cnt);
+        atomicAdd(&a.ip[2 * (int64_t)p + 1], cc);
       }
     }
     if (a.next_counts) {
       __syncthreads();
       for (int j = tid; j < cc; j += kScoreThreads) {
         const int h = s_hist[j];
-        if (h) s_base[j] = atomicAdd(&a.next_counts[cb + j - a.next_base], h);
+        if (h) atomicAdd(&a.next_counts[cb + j - a.next_base], h);
         s_hist[j] = 0;
       }
-      __syncthreads();
-      if (valid) a.rank[p] = s_base[best] + local;
     }
     tc_fence_before();
+    it = nit;
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   tc_fence_after();
   if (warp == 0) tmem_dealloc(tmem, a.tmem_cols);
@@ -200,7 +242,7 @@ constexpr int kScanThreads = 1024;
 
 __global__ void __launch_bounds__(kScanThreads) scan_kernel(int* counts, int nbins, int* offsets,
                                                              int4* items, int* num_items,
-                                                             int* tile_off) {
+                                                             int* tile_off, int* cursor) {
   using Scan = cub::BlockScan<int, kScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry[2];
@@ -217,6 +259,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(int* counts, int nbi
     if (b < nbins) {
       offsets[b] = carry[0] + pre_c;
       tile_off[b] = carry[1] + pre_t;
+      cursor[b] = 0;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -243,21 +286,28 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(int* counts, int nbi
 }
 
 // ------------------------------------------------------------------ scatter
-__global__ void scatter_kernel(int64_t N, const int* rank, const int* path_ws, int L, int level,
-                               int level_base, const int* offsets, int* perm) {
+// perm[offsets[bin] + slot] = p, slots claimed with one atomic per (warp, bin).
+__global__ void scatter_kernel(int64_t N, const int* active, const int* path_ws, int L, int level,
+                               int level_base, const int* offsets, int* cursor, int* perm) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= N) return;
-  const int r = rank[p];
-  if (r < 0) return;
-  const int bin = level == 0 ? 0 : path_ws[p * L + level - 1] - level_base;
-  perm[offsets[bin] + r] = (int)p;
+  const int lane = threadIdx.x & 31;
+  const bool act = p < N && active[p];
+  const int bin = act ? (level == 0 ? 0 : path_ws[p * L + level - 1] - level_base) : -1;
+  const unsigned peers = __match_any_sync(kFull, bin);
+  if (act) {
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&cursor[bin], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    perm[offsets[bin] + base + __popc(peers & ((1u << lane) - 1u))] = (int)p;
+  }
 }
 
 }  // namespace
 
 size_t score_smem_bytes(int kchunks, int npad) {
-  return 1024 + (size_t)kchunks * kTile * 128 * 2 + (size_t)kchunks * 2 * npad * 128 + 16 + 16 +
-         (kTile + 512) * 4;
+  return 1024 + (size_t)kchunks * kTile * 128 * 2 + table_bytes(kchunks, npad, true) + 16 + 16 + 16 +
+         (2 * kTile + 256) * 4;
 }
 
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method) {
@@ -270,7 +320,8 @@ bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int metho
 }
 
 bool build_staged_tables(TreeHandle* t, const int32_t* child_begin, const int32_t* child_count,
-                         const float* centroids, cudaStream_t st, std::string* err) {
+                         const float* centroids, const int32_t* leaf_atom, cudaStream_t st,
+                         std::string* err) {
   UpdateCfg uc;
   if (!update_config(t->ld, 1, uc)) return false;
   const int L = t->levels;
@@ -289,8 +340,9 @@ bool build_staged_tables(TreeHandle* t, const int32_t* child_begin, const int32_
   std::vector<float*> tables(L, nullptr);
   for (int l = 0; l < L; ++l) {
     const int npad = levels[l].npad;
+    const bool last = l == L - 1;
     const int64_t nodes = t->level_offsets[l + 1] - t->level_offsets[l];
-    const size_t per_node = (size_t)kch * 2 * npad * 32;  // floats
+    const size_t per_node = table_bytes(kch, npad, last) / 4;  // 4-byte words
     std::vector<float> host(per_node * nodes, 0.f);
     for (int64_t i = 0; i < nodes; ++i) {
       const int64_t v = t->level_offsets[l] + i;
@@ -307,6 +359,16 @@ bool build_staged_tables(TreeHandle* t, const int32_t* child_begin, const int32_
           float* plane = blk + (size_t)kc * 2 * npad * 32;
           plane[off] = hi;
           plane[npad * 32 + off] = lo;
+        }
+      }
+      if (last) {  // leaf metadata of each child (a depth-L node): pursuit.py:155-162
+        int32_t* info = reinterpret_cast<int32_t*>(blk + (size_t)kch * 2 * npad * 32);
+        int32_t* cnt = info + npad;
+        for (int j = 0; j < cc; ++j) {
+          const int child = cb + j;
+          const int lc = child_count[child];
+          info[j] = lc == 1 ? leaf_atom[child_begin[child]] : -1 - child;
+          cnt[j] = lc;
         }
       }
     }
@@ -330,71 +392,83 @@ void free_staged_tables(TreeHandle* t) {
   t->staged_levels.clear();
 }
 
-size_t staged_workspace_bytes(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method) {
+namespace {
+
+struct WsLayout {
+  size_t total = 0;
+  size_t R, Xpad, tol, active, perm, path_ws, leaf_sel, Lf, yv, counts, offsets, tile_off, cursor, items,
+      num_items;
+};
+
+WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method,
+                std::vector<int64_t>* bin_off_out, int64_t* maxbins_out) {
   const int L = t->levels;
-  int64_t maxbins = 1, sumbins = 0;
+  int64_t maxbins = 1;
+  std::vector<int64_t> bin_off(L + 1, 0);
   for (int l = 0; l < L; ++l) {
     const int64_t b = t->level_offsets[l + 1] - t->level_offsets[l];
-    maxbins = b > maxbins ? b : maxbins;
-    sumbins += b;
+    maxbins = std::max(maxbins, b);
+    bin_off[l + 1] = bin_off[l] + b;
   }
-  size_t s = 0;
-  auto add = [&](size_t bytes) { s += (bytes + 255) & ~(size_t)255; };
-  add((size_t)N * d->ld * 4);              // R
-  if (method == kMethodOMP) add((size_t)N * d->ld * 4);  // padded copy of X
-  add((size_t)N * 4);                      // tol
-  add((size_t)N * 4);                      // active
-  add((size_t)N * 4);                      // rank
-  add((size_t)N * 4);                      // perm
-  add((size_t)N * L * 4);                  // path_ws
-  add((size_t)N * 4);                      // leaf_sel
-  add((size_t)N * K * (K + 1) / 2 * 4);    // Cholesky factors
-  add((size_t)N * K * 4);                  // y
-  add((size_t)sumbins * 4);                // per-level bin counts
-  add((size_t)(maxbins + 1) * 4);          // offsets
-  add((size_t)(maxbins + 1) * 4);          // tile offsets
-  add((size_t)(N / kTile + maxbins + 2) * 16);  // items
-  add(16);                                 // num_items
-  return s;
+  WsLayout w;
+  auto add = [&](size_t bytes) {
+    const size_t at = w.total;
+    w.total += (bytes + 255) & ~(size_t)255;
+    return at;
+  };
+  w.R = add((size_t)N * d->ld * 4);
+  w.Xpad = method == kMethodOMP ? add((size_t)N * d->ld * 4) : 0;
+  w.tol = add((size_t)N * 4);
+  w.active = add((size_t)N * 4);
+  w.perm = add((size_t)N * 4);
+  w.path_ws = add((size_t)N * L * 4);
+  w.leaf_sel = add((size_t)N * 4);
+  w.Lf = add((size_t)N * K * (K + 1) / 2 * 4);
+  w.yv = add((size_t)N * K * 4);
+  w.counts = add((size_t)bin_off[L] * 4);
+  w.offsets = add((size_t)(maxbins + 1) * 4);
+  w.tile_off = add((size_t)(maxbins + 1) * 4);
+  w.cursor = add((size_t)(maxbins + 1) * 4);
+  w.items = add((size_t)(N / kTile + maxbins + 2) * 16);
+  w.num_items = add(16);
+  if (bin_off_out) *bin_off_out = bin_off;
+  if (maxbins_out) *maxbins_out = maxbins;
+  return w;
+}
+
+}  // namespace
+
+size_t staged_workspace_bytes(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method) {
+  return layout(d, t, N, K, method, nullptr, nullptr).total;
 }
 
 cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X, int64_t N,
                        int64_t ldx, int K, int method, float tol_abs, int32_t* idx, float* coef,
                        int32_t* count, float* resnorm, int32_t* path, int32_t* ip, void* ws,
                        size_t ws_bytes, cudaStream_t st) {
-  if (ws == nullptr || ws_bytes < staged_workspace_bytes(d, t, N, K, method)) return cudaErrorInvalidValue;
+  std::vector<int64_t> bin_off;
+  int64_t maxbins = 1;
+  const WsLayout w = layout(d, t, N, K, method, &bin_off, &maxbins);
+  if (ws == nullptr || ws_bytes < w.total) return cudaErrorInvalidValue;
   const int L = t->levels;
-  uint8_t* w = static_cast<uint8_t*>(ws);
-  auto take = [&](size_t bytes) {
-    void* p = w;
-    w += (bytes + 255) & ~(size_t)255;
-    return p;
-  };
-  int64_t maxbins = 1, sumbins = 0;
-  std::vector<int64_t> bin_off(L + 1, 0);
-  for (int l = 0; l < L; ++l) {
-    const int64_t b = t->level_offsets[l + 1] - t->level_offsets[l];
-    maxbins = b > maxbins ? b : maxbins;
-    bin_off[l + 1] = bin_off[l] + b;
-  }
-  sumbins = bin_off[L];
-  float* R = (float*)take((size_t)N * d->ld * 4);
-  float* Xpad = method == kMethodOMP ? (float*)take((size_t)N * d->ld * 4) : nullptr;
-  float* tol = (float*)take((size_t)N * 4);
-  int* active = (int*)take((size_t)N * 4);
-  int* rank = (int*)take((size_t)N * 4);
-  int* perm = (int*)take((size_t)N * 4);
-  int* path_ws = (int*)take((size_t)N * L * 4);
-  int* leaf_sel = (int*)take((size_t)N * 4);
-  float* Lf = (float*)take((size_t)N * K * (K + 1) / 2 * 4);
-  float* yv = (float*)take((size_t)N * K * 4);
-  int* counts = (int*)take((size_t)sumbins * 4);
-  int* offsets = (int*)take((size_t)(maxbins + 1) * 4);
-  int* tile_off = (int*)take((size_t)(maxbins + 1) * 4);
-  int4* items = (int4*)take((size_t)(N / kTile + maxbins + 2) * 16);
-  int* num_items = (int*)take(16);
+  uint8_t* b = static_cast<uint8_t*>(ws);
+  float* R = (float*)(b + w.R);
+  float* Xpad = method == kMethodOMP ? (float*)(b + w.Xpad) : nullptr;
+  float* tol = (float*)(b + w.tol);
+  int* active = (int*)(b + w.active);
+  int* perm = (int*)(b + w.perm);
+  int* path_ws = (int*)(b + w.path_ws);
+  int* leaf_sel = (int*)(b + w.leaf_sel);
+  float* Lf = (float*)(b + w.Lf);
+  float* yv = (float*)(b + w.yv);
+  int* counts = (int*)(b + w.counts);
+  int* offsets = (int*)(b + w.offsets);
+  int* tile_off = (int*)(b + w.tile_off);
+  int* cursor = (int*)(b + w.cursor);
+  int4* items = (int4*)(b + w.items);
+  int* num_items = (int*)(b + w.num_items);
 
-  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)sumbins * 4, st);
+  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)bin_off[L] * 4, st);
   if (e != cudaSuccess) return e;
 
   UpdateCfg uc;
@@ -406,8 +480,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   u.leaf_atom = t->leaf_atom; u.L = L; u.path_ws = path_ws; u.K = K; u.method = method;
   u.tol_abs = tol_abs; u.idx = idx; u.coef = coef; u.count = count; u.resnorm = resnorm;
   u.ip = ip; u.path_out = path; u.Lf = Lf; u.yv = yv; u.tol = tol; u.active = active;
-  u.rank = rank; u.root_count = counts; u.N = N; u.leaf_sel = leaf_sel;
-  // stage the support atoms in shared memory when 16 patch groups fit comfortably
+  u.root_count = counts; u.N = N; u.leaf_sel = leaf_sel;
+  // stage the support atoms in shared memory when the patch groups fit comfortably
   u.cache_atoms = update_smem_bytes(uc, K, d->ld, true) <= 96 * 1024 ? 1 : 0;
 
   const int gpb = 128 / uc.G;
@@ -426,15 +500,16 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
     for (int l = 0; l < L; ++l) {
       const StagedLevel& lv = t->staged_levels[l];
       const int nb = (int)(t->level_offsets[l + 1] - t->level_offsets[l]);
-      scan_kernel<<<1, kScanThreads, 0, st>>>(counts + bin_off[l], nb, offsets, items, num_items, tile_off);
-      scatter_kernel<<<scatter_blocks, 256, 0, st>>>(N, rank, path_ws, L, l, (int)t->level_offsets[l],
-                                                    offsets, perm);
+      scan_kernel<<<1, kScanThreads, 0, st>>>(counts + bin_off[l], nb, offsets, items, num_items, tile_off,
+                                               cursor);
+      scatter_kernel<<<scatter_blocks, 256, 0, st>>>(N, active, path_ws, L, l, (int)t->level_offsets[l],
+                                                    offsets, cursor, perm);
       ScoreArgs s{};
       s.R = R; s.ld = d->ld; s.perm = perm; s.items = items; s.num_items = num_items;
       s.table = t->staged_tables[l]; s.npad = lv.npad; s.kchunks = d->ld / 32; s.tmem_cols = lv.tmem_cols;
       s.level = l; s.level_base = (int)t->level_offsets[l]; s.child_begin = t->child_begin;
       s.child_count = t->child_count; s.path_ws = path_ws; s.path_out = path; s.count = count;
-      s.K = K; s.L = L; s.rank = rank; s.ip = ip; s.leaf_atom = t->leaf_atom;
+      s.K = K; s.L = L; s.ip = ip; s.leaf_atom = t->leaf_atom;
       if (l + 1 < L) {
         s.next_counts = counts + bin_off[l + 1];
         s.next_base = (int)t->level_offsets[l + 1];
@@ -444,8 +519,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       const size_t smem = score_smem_bytes(s.kchunks, lv.npad);
       e = cudaFuncSetAttribute(score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      const int per_sm = (int)((227 * 1024) / smem) > 0 ? (int)((227 * 1024) / smem) : 1;
-      const int grid = sms * (per_sm > 2 ? 2 : per_sm);
+      const int per_sm = std::max(1, (int)((227 * 1024) / smem));
+      const int grid = sms * std::min(per_sm, 2);
       score_tc_kernel<<<grid, kScoreThreads, smem, st>>>(s);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }

@@ -29,18 +29,12 @@ __device__ __forceinline__ float group_sum(float v) {
   return v;
 }
 
-// warp-aggregated rank in the single root bin (called by every lane; `act`
-// must be true on at most one lane per patch group)
-__device__ __forceinline__ int root_rank(bool act, int* counter) {
+// Count the patches that stay active into the single root bin: one
+// fire-and-forget atomic per warp (called by every lane; `act` true on at
+// most one lane per patch group).  Slots are assigned later by the scatter.
+__device__ __forceinline__ void count_root(bool act, int* counter) {
   const unsigned m = __ballot_sync(kFull, act);
-  const int lane = threadIdx.x & 31;
-  int base = 0;
-  if (m) {
-    const int leader = __ffs(m) - 1;
-    if (lane == leader) base = atomicAdd(counter, __popc(m));
-    base = __shfl_sync(kFull, base, leader);
-  }
-  return base + __popc(m & ((1u << lane) - 1u));
+  if (m && (int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(counter, __popc(m));
 }
 
 template <int E>
@@ -123,8 +117,7 @@ __global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
     if (a.path_out)
       for (int j = gl; j < a.K * a.L; j += G) a.path_out[p * a.K * a.L + j] = -1;
   }
-  const int r = root_rank(act && gl == 0, a.root_count);
-  if (inb && gl == 0) a.rank[p] = act ? r : -1;
+  count_root(act && gl == 0, a.root_count);
 }
 
 // ------------------------------------------------------------------ update
@@ -176,13 +169,14 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
     if (omp) {
       load_vec<E>(a.X2 + p * a.ld2 + off, x);
       // the patch's solver state -> shared, as one batch of independent loads
-      for (int i = gl; i < t; i += G) {
+      // (bounded by K, not t, so they do not wait for the count load)
+      for (int i = gl; i < K; i += G) {
         S_s[i] = a.idx[p * K + i];
         c_s[i] = a.coef[p * K + i];
         y_s[i] = a.yv[p * K + i];
       }
       const float* Lp = a.Lf + p * (int64_t)(K * (K + 1) / 2);
-      for (int i = gl; i < t * (t + 1) / 2; i += G) L_s[i] = Lp[i];
+      for (int i = gl; i < K * (K + 1) / 2; i += G) L_s[i] = Lp[i];
       __syncwarp(gmask);
       if (a.cache_atoms) {  // support atoms -> shared with async copies, all in flight at once
         const int F = a.ld >> 2;
@@ -301,8 +295,7 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
     }
     if (gl == 0) a.active[p] = act ? 1 : 0;
   }
-  const int rr = root_rank(act && gl == 0, a.root_count);
-  if (inb && gl == 0) a.rank[p] = act ? rr : -1;
+  count_root(act && gl == 0, a.root_count);
 }
 
 }  // namespace

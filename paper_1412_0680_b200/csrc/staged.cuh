@@ -22,7 +22,7 @@ struct ScoreArgs {
   int K, L;
   int* next_counts;      // bin counters of the next level (nullptr at the last level)
   int next_base;
-  int* rank;             // rank of the patch inside its next-level bin
+
   int32_t* ip;           // optional per-patch {inner products, centroid inner products}
   int* leaf_sel;         // last level: the single leaf atom, or -1-node for multi-atom leaves
   const int* leaf_atom;
@@ -54,7 +54,7 @@ struct UpdateArgs {
   float* yv;             // forward-substituted rhs per patch
   float* tol;
   int* active;
-  int* rank;
+
   int* root_count;
   const int* leaf_sel;   // written by the last score pass
   int cache_atoms;       // stage the support atoms in shared memory
@@ -82,7 +82,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
                        size_t ws_bytes, cudaStream_t st);
 // host-side construction of the per-level SW128 hi/lo tables
 bool build_staged_tables(TreeHandle* t, const int32_t* child_begin, const int32_t* child_count,
-                         const float* centroids, cudaStream_t st, std::string* err);
+                         const float* centroids, const int32_t* leaf_atom, cudaStream_t st,
+                         std::string* err);
 void free_staged_tables(TreeHandle* t);
 
 }  // namespace stmp
