@@ -37,9 +37,11 @@ __host__ __device__ inline uint32_t table_bytes(int kch, int npad, bool last) {
   return (uint32_t)kch * 2u * npad * 128u + (last ? 8u * npad : 0u);
 }
 
+template <int KCH>
 __device__ __forceinline__ void issue_gather(const ScoreArgs& a, const int* rows_ids, int rows,
                                              uint32_t a_hi_s, int tid) {
-  const int F = a.ld >> 2;
+  constexpr int F = 8 * KCH;  // float4 per residual row
+#pragma unroll 4
   for (int e = tid; e < kTile * F; e += kScoreThreads) {
     const int row = e / F;
     const int c = e - row * F;
@@ -52,13 +54,14 @@ __device__ __forceinline__ void issue_gather(const ScoreArgs& a, const int* rows
 }
 
 // ------------------------------------------------------------------ score (tcgen05)
+template <int KCH>
 __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* base = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  const int kch = a.kchunks;
+  constexpr int kch = KCH;
   const int npad = a.npad;
   const bool last = a.leaf_sel != nullptr;
   float* Ahi = reinterpret_cast<float*>(base);
@@ -90,7 +93,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
   const int i1 = min(num_items, i0 + per);
   const uint32_t idesc = idesc_tf32(kTile, npad);
   const uint32_t a_hi_s = smem_u32(Ahi), a_lo_s = smem_u32(Alo), b_s = smem_u32(Btab);
-  const int F = a.ld >> 2;
+  constexpr int F = 8 * KCH;
   uint32_t tab_phase = 0, mma_phase = 0;
   int loaded_bin = -1;
 
@@ -106,7 +109,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
     }
     loaded_bin = it.x;
     __syncthreads();
-    issue_gather(a, s_rows, it.z, a_hi_s, tid);
+    issue_gather<KCH>(a, s_rows, it.z, a_hi_s, tid);
   }
   bool table_pending = i0 < i1;
 
@@ -121,6 +124,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     // split the gathered rows into tf32 hi / lo planes in place
+#pragma unroll 4
     for (int e = tid; e < kTile * F; e += kScoreThreads) {
       const int row = e / F;
       const int c = e - row * F;
@@ -142,6 +146,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
         tab_phase ^= 1u;
       }
       tc_fence_after();
+#pragma unroll
       for (int kc = 0; kc < kch; ++kc) {
         const uint32_t ah = a_hi_s + kc * (kTile * 128u);
         const uint32_t al = a_lo_s + kc * (kTile * 128u);
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
       }
       table_pending = new_tab;
       loaded_bin = nit.x;
-      issue_gather(a, s_rows + (buf ^ 1) * kTile, nit.z, a_hi_s, tid);
+      issue_gather<KCH>(a, s_rows + (buf ^ 1) * kTile, nit.z, a_hi_s, tid);
     }
 
     if (valid) {
@@ -301,6 +306,41 @@ __global__ void scatter_kernel(int64_t N, const int* active, const int* path_ws,
     base = __shfl_sync(peers, base, leader);
     perm[offsets[bin] + base + __popc(peers & ((1u << lane) - 1u))] = (int)p;
   }
+}
+
+// Root level: a single bin holding every active patch.  One atomic per CTA.
+__global__ void __launch_bounds__(256) scatter_root_kernel(int64_t N, const int* active, const int* offsets,
+                                                           int* cursor, int* perm) {
+  __shared__ int warp_off[8];
+  __shared__ int base;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool act = p < N && active[p];
+  const unsigned m = __ballot_sync(kFull, act);
+  if (lane == 0) warp_off[warp] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      const int c = warp_off[w];
+      warp_off[w] = s;
+      s += c;
+    }
+    base = s ? atomicAdd(cursor, s) : 0;
+  }
+  __syncthreads();
+  if (act) perm[offsets[0] + base + warp_off[warp] + __popc(m & ((1u << lane) - 1u))] = (int)p;
+}
+
+template <int KCH>
+cudaError_t launch_score(const ScoreArgs& s, int sms, cudaStream_t st) {
+  const size_t smem = score_smem_bytes(KCH, s.npad);
+  cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<KCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int per_sm = std::max(1, (int)((227 * 1024) / smem));
+  const int grid = sms * std::min(per_sm, 2);
+  score_tc_kernel<KCH><<<grid, kScoreThreads, smem, st>>>(s);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -502,8 +542,11 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       const int nb = (int)(t->level_offsets[l + 1] - t->level_offsets[l]);
       scan_kernel<<<1, kScanThreads, 0, st>>>(counts + bin_off[l], nb, offsets, items, num_items, tile_off,
                                                cursor);
-      scatter_kernel<<<scatter_blocks, 256, 0, st>>>(N, active, path_ws, L, l, (int)t->level_offsets[l],
-                                                    offsets, cursor, perm);
+      if (l == 0)
+        scatter_root_kernel<<<scatter_blocks, 256, 0, st>>>(N, active, offsets, cursor, perm);
+      else
+        scatter_kernel<<<scatter_blocks, 256, 0, st>>>(N, active, path_ws, L, l, (int)t->level_offsets[l],
+                                                      offsets, cursor, perm);
       ScoreArgs s{};
       s.R = R; s.ld = d->ld; s.perm = perm; s.items = items; s.num_items = num_items;
       s.table = t->staged_tables[l]; s.npad = lv.npad; s.kchunks = d->ld / 32; s.tmem_cols = lv.tmem_cols;
@@ -516,13 +559,17 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       } else {
         s.leaf_sel = leaf_sel;
       }
-      const size_t smem = score_smem_bytes(s.kchunks, lv.npad);
-      e = cudaFuncSetAttribute(score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      switch (s.kchunks) {
+        case 1: e = launch_score<1>(s, sms, st); break;
+        case 2: e = launch_score<2>(s, sms, st); break;
+        case 3: e = launch_score<3>(s, sms, st); break;
+        case 4: e = launch_score<4>(s, sms, st); break;
+        case 5: e = launch_score<5>(s, sms, st); break;
+        case 6: e = launch_score<6>(s, sms, st); break;
+        case 8: e = launch_score<8>(s, sms, st); break;
+        default: e = cudaErrorInvalidValue;
+      }
       if (e != cudaSuccess) return e;
-      const int per_sm = std::max(1, (int)((227 * 1024) / smem));
-      const int grid = sms * std::min(per_sm, 2);
-      score_tc_kernel<<<grid, kScoreThreads, smem, st>>>(s);
-      if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if ((e = launch_update(uc, u, ublocks, usmem, st)) != cudaSuccess) return e;
   }

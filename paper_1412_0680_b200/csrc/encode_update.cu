@@ -230,13 +230,21 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
       for (int j = 0; j < t; ++j) dup |= (S_s[j] == atom);
       const float bt = group_sum<G>(dot_vec<E>(av, x));
       const float gtt = group_sum<G>(dot_vec<E>(av, av));
-      // Gram column of the new atom against the support + forward substitution
-      float wsum = 0.f, gc = 0.f;
+      // Gram column of the new atom against the support (independent dots, the
+      // row loads of several j in flight at once), then forward substitution
+      float* g_s = cn_s;  // cn is produced only after the Gram column is consumed
+#pragma unroll 4
       for (int j = 0; j < t; ++j) {
         float sv[E];
         if (a.cache_atoms) load_gen<E>(A_s + j * a.ld + off, sv);
         else load_vec<E>(a.atoms + (int64_t)S_s[j] * a.ld + off, sv);
         const float g = group_sum<G>(dot_vec<E>(sv, av));
+        if (gl == 0) g_s[j] = g;
+      }
+      __syncwarp(gmask);
+      float wsum = 0.f, gc = 0.f;
+      for (int j = 0; j < t; ++j) {
+        const float g = g_s[j];
         gc = fmaf(g, c_s[j], gc);   // a . (A_S c_prev)
         const float* Lj = L_s + j * (j + 1) / 2;
         float v = g;
@@ -246,6 +254,7 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
         wsum = fmaf(v, v, wsum);
       }
       const float score = bt - gc;   // a . r for r = x - A_S c_prev (pursuit.py:217 check)
+      __syncwarp(gmask);  // every lane has read g_s before cn_s is overwritten
       if (dup || score == 0.f) {
         act = false;   // re-selection (or a zero score) ends the loop
       } else {
@@ -266,6 +275,7 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
         const float ct = cn_s[t];
 #pragma unroll
         for (int i = 0; i < E; ++i) r[i] = fmaf(-ct, av[i], x[i]);
+#pragma unroll 4
         for (int j = 0; j < t; ++j) {
           float sv[E];
           if (a.cache_atoms) load_gen<E>(A_s + j * a.ld + off, sv);
@@ -305,8 +315,10 @@ bool update_config(int ld, int K, UpdateCfg& c) {
   bool ok = false;
   for (int v : kLd) ok |= (v == ld);
   if (!ok) return false;
+  // few lanes per patch: the scalar triangular solves run once per G lanes, so
+  // small groups keep the warp instruction count per patch low
   int G = 1;
-  while (G < 32 && ld / G > 8) G <<= 1;
+  while (G < 32 && ld / G > 32) G <<= 1;
   c.G = G;
   c.E = ld / G;
   c.KC = 0;
@@ -314,7 +326,7 @@ bool update_config(int ld, int K, UpdateCfg& c) {
 }
 
 #define STMP_UPD_CASES(X) \
-  X(4, 8) X(8, 8) X(16, 6) X(16, 8) X(32, 5) X(32, 6) X(32, 8) X(32, 16) X(32, 32) X(32, 50) X(32, 64)
+  X(1, 32) X(2, 32) X(4, 24) X(4, 32) X(8, 20) X(8, 24) X(8, 32) X(16, 32) X(32, 32) X(32, 50) X(32, 64)
 
 cudaError_t launch_init(const UpdateCfg& c, const UpdateArgs& a, int blocks, cudaStream_t st) {
   switch (c.G * 1000 + c.E) {
