@@ -1,14 +1,14 @@
 // Per-patch kernels of the staged encoder: init (padded residual copy,
-// tolerance, root bucketing) and update (leaf choice + MP step or OMP refit).
+// tolerance, root bin count) and update (leaf choice + MP step or OMP refit).
 //
-// A group of G lanes owns one patch; lane gl holds elements [gl*E, gl*E+E) of
-// the padded row.  For OMP the patch's solver state and its support atoms are
-// pulled into shared memory as one batch of independent (async) loads and
-// reused by both the Gram column and the residual rebuild, so an iteration
-// costs a few dependent global round trips instead of 2t.  The small
-// triangular solves run redundantly on the G lanes (no shuffles); dot
-// products are group reductions.  Semantics: pkg/src/stmp/pursuit.py:207-221 (MP) and the
-// SURVEY §8c OMP restatement over omp_refit (pursuit.py:235-250).
+// A group of G = 8 (or 32 for wide rows) lanes owns one patch.  Rows are
+// read in an interleaved layout -- lane gl touches the 16-B chunks gl, gl+G,
+// gl+2G, ... -- so one warp load instruction covers whole 128-B lines of a
+// few rows (the L1 wavefront count per row is minimal).  Dot products are
+// group reductions; the small triangular solves of the OMP refit are
+// column sweeps in which lane j owns rows j, j+G, ... of the Cholesky factor.
+// Semantics: pkg/src/stmp/pursuit.py:207-221 (MP) and the SURVEY §8c OMP
+// restatement over omp_refit (pursuit.py:235-250).
 #include "common.cuh"
 #include "kernels.cuh"
 #include "sm100.cuh"
@@ -18,12 +18,17 @@ namespace stmp {
 
 namespace {
 
+template <int G>
+__device__ __forceinline__ unsigned group_mask() {
+  return G >= 32 ? kFull : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+}
+
 // Sum over the G lanes of this patch group.  The mask names only the group's
 // own lanes: groups of one warp diverge (different patches stop at different
 // iterations), so a full-warp mask would wait for lanes that never arrive.
 template <int G>
 __device__ __forceinline__ float group_sum(float v) {
-  const unsigned mask = G >= 32 ? kFull : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  const unsigned mask = group_mask<G>();
 #pragma unroll
   for (int o = G >> 1; o; o >>= 1) v += __shfl_xor_sync(mask, v, o);
   return v;
@@ -37,68 +42,58 @@ __device__ __forceinline__ void count_root(bool act, int* counter) {
   if (m && (int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(counter, __popc(m));
 }
 
-template <int E>
-__device__ __forceinline__ void load_vec(const float* __restrict__ src, float (&v)[E]) {
-  if constexpr (E % 4 == 0) {
+// Row slice of this lane: chunks gl + G*i (i < CPL) of F 16-byte chunks.
+template <int G, int CPL>
+struct Slice {
+  float v[CPL * 4];
+
+  __device__ __forceinline__ void load(const float* __restrict__ row, int gl, int F) {
 #pragma unroll
-    for (int i = 0; i < E / 4; ++i) {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(src) + i);
+    for (int i = 0; i < CPL; ++i) {
+      const int c = gl + G * i;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < F) q = __ldg(reinterpret_cast<const float4*>(row) + c);
       v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
     }
-  } else if constexpr (E % 2 == 0) {
+  }
+  __device__ __forceinline__ void store(float* row, int gl, int F) const {
 #pragma unroll
-    for (int i = 0; i < E / 2; ++i) {
-      const float2 q = __ldg(reinterpret_cast<const float2*>(src) + i);
-      v[2 * i] = q.x; v[2 * i + 1] = q.y;
+    for (int i = 0; i < CPL; ++i) {
+      const int c = gl + G * i;
+      if (c < F) reinterpret_cast<float4*>(row)[c] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     }
-  } else {
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = __ldg(src + i);
   }
-}
-
-template <int E>
-__device__ __forceinline__ void store_vec(float* dst, const float (&v)[E]) {
-  if constexpr (E % 4 == 0) {
+  __device__ __forceinline__ float dot(const Slice& o) const {
+    float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < E / 4; ++i)
-      reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-  } else if constexpr (E % 2 == 0) {
-#pragma unroll
-    for (int i = 0; i < E / 2; ++i) reinterpret_cast<float2*>(dst)[i] = make_float2(v[2 * i], v[2 * i + 1]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < E; ++i) dst[i] = v[i];
+    for (int i = 0; i < CPL * 4; ++i) s = fmaf(v[i], o.v[i], s);
+    return s;
   }
-}
-
-template <int E>
-__device__ __forceinline__ float dot_vec(const float (&a)[E], const float (&b)[E]) {
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < E; ++i) s = fmaf(a[i], b[i], s);
-  return s;
-}
+};
 
 // ------------------------------------------------------------------ init
-template <int G, int E>
+template <int G, int CPL>
 __global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
   const int gpb = blockDim.x / G;
   const int64_t p = (int64_t)blockIdx.x * gpb + threadIdx.x / G;
   const int gl = threadIdx.x % G;
+  const int F = a.ld >> 2;
   const bool inb = p < a.N;
-  float x[E];
+  Slice<G, CPL> x;
   float ss = 0.f;
   if (inb) {
     const float* xp = a.X + p * a.ldx;
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int d = gl * E + i;
-      x[i] = d < a.n ? __ldg(xp + d) : 0.f;
-      ss = fmaf(x[i], x[i], ss);
+    for (int i = 0; i < CPL; ++i) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int d = 4 * (gl + G * i) + k;
+        x.v[4 * i + k] = d < a.n ? __ldg(xp + d) : 0.f;
+        ss = fmaf(x.v[4 * i + k], x.v[4 * i + k], ss);
+      }
     }
-    store_vec<E>(a.R + p * a.ld + gl * E, x);
-    if (a.X2) store_vec<E>(const_cast<float*>(a.X2) + p * a.ld2 + gl * E, x);
+    x.store(a.R + p * a.ld, gl, F);
+    if (a.X2) x.store(const_cast<float*>(a.X2) + p * a.ld2, gl, F);
   }
   ss = group_sum<G>(ss);
   const float xn = sqrtf(ss);
@@ -121,54 +116,38 @@ __global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
 }
 
 // ------------------------------------------------------------------ update
-// Shared scratch per patch group (floats):
-//   S[K] | c[K] | y[K] | L[K(K+1)/2] | w[K] | cn[K] | support atoms [K][ld] (optional)
+// Shared scratch per patch group (floats): S[K] | c[K] | y[K] | L[K(K+1)/2] | g[K] | cn[K]
 __host__ __device__ inline int upd_scalar_floats(int K) { return (5 * K + K * (K + 1) / 2 + 3) & ~3; }
 
-template <int E>
-__device__ __forceinline__ void load_gen(const float* src, float (&v)[E]) {
-  if constexpr (E % 4 == 0) {
-#pragma unroll
-    for (int i = 0; i < E / 4; ++i) {
-      const float4 q = reinterpret_cast<const float4*>(src)[i];
-      v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = src[i];
-  }
-}
-
-template <int G, int E>
+template <int G, int CPL>
 __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
   extern __shared__ __align__(16) float upd_smem[];
   const int gpb = blockDim.x / G;
   const int grp = threadIdx.x / G;
   const int64_t p = (int64_t)blockIdx.x * gpb + grp;
   const int gl = threadIdx.x % G;
-  const unsigned gmask = G >= 32 ? kFull : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  const unsigned gmask = group_mask<G>();
   const int K = a.K;
-  const int sfl = upd_scalar_floats(K);
-  float* gs = upd_smem + grp * (sfl + (a.cache_atoms ? K * a.ld : 0));
+  const int F = a.ld >> 2;
+  float* gs = upd_smem + grp * upd_scalar_floats(K);
   int* S_s = reinterpret_cast<int*>(gs);
-  float* c_s = gs + K;
-  float* y_s = c_s + K;
-  float* L_s = y_s + K;
-  float* w_s = L_s + K * (K + 1) / 2;
-  float* cn_s = w_s + K;
-  float* A_s = gs + sfl;
+  float* c_s = gs + K;       // previous coefficients
+  float* y_s = c_s + K;      // L y = A_S x (forward-substituted rhs); reused as the back-sweep rhs
+  float* L_s = y_s + K;      // packed Cholesky factor, rows 0..t-1
+  float* g_s = L_s + K * (K + 1) / 2;  // Gram column -> new row w of L
+  float* cn_s = g_s + K;     // new coefficients
   const bool inb = p < a.N;
   bool act = inb && a.active[p];
-  const int64_t off = (int64_t)gl * E;
+  using Sl = Slice<G, CPL>;
   if (act) {
     const int t = a.count[p];
     const int lsel = a.leaf_sel[p];
     const bool omp = a.method == kMethodOMP;
-    float r[E], x[E];
-    if (!omp || lsel < 0) load_vec<E>(a.R + p * a.ld + off, r);
+    Sl r, x;
+    if (!omp || lsel < 0) r.load(a.R + p * a.ld, gl, F);
     if (omp) {
-      load_vec<E>(a.X2 + p * a.ld2 + off, x);
-      // the patch's solver state -> shared, as one batch of independent loads
+      x.load(a.X2 + p * a.ld2, gl, F);
+      // the patch's solver state -> shared, one batch of independent loads
       // (bounded by K, not t, so they do not wait for the count load)
       for (int i = gl; i < K; i += G) {
         S_s[i] = a.idx[p * K + i];
@@ -177,14 +156,6 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
       }
       const float* Lp = a.Lf + p * (int64_t)(K * (K + 1) / 2);
       for (int i = gl; i < K * (K + 1) / 2; i += G) L_s[i] = Lp[i];
-      __syncwarp(gmask);
-      if (a.cache_atoms) {  // support atoms -> shared with async copies, all in flight at once
-        const int F = a.ld >> 2;
-        for (int e = gl; e < t * F; e += G) {
-          const int j = e / F, q = e - j * F;
-          sm100::cp_async16(sm100::smem_u32(A_s + j * a.ld + 4 * q), a.atoms + (int64_t)S_s[j] * a.ld + 4 * q, 16u);
-        }
-      }
     }
     // leaf choice: single-atom leaves were resolved by the last score pass;
     // otherwise max |a . r| over the node's atoms, ties to the lowest atom index
@@ -196,24 +167,24 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
       atom = __ldg(a.leaf_atom + cb);
       for (int j = 0; j < cc; ++j) {
         const int aj = __ldg(a.leaf_atom + cb + j);
-        float v[E];
-        load_vec<E>(a.atoms + (int64_t)aj * a.ld + off, v);
-        const float m = fabsf(group_sum<G>(dot_vec<E>(v, r)));
+        Sl v;
+        v.load(a.atoms + (int64_t)aj * a.ld, gl, F);
+        const float m = fabsf(group_sum<G>(v.dot(r)));
         if (m > bestv || (m == bestv && aj < atom)) { bestv = m; atom = aj; }
       }
     }
-    float av[E];
-    load_vec<E>(a.atoms + (int64_t)atom * a.ld + off, av);
+    Sl av;
+    av.load(a.atoms + (int64_t)atom * a.ld, gl, F);
     int32_t* S = a.idx + p * K;
     if (!omp) {
-      const float s = group_sum<G>(dot_vec<E>(av, r));
+      const float s = group_sum<G>(av.dot(r));
       if (s == 0.f) {
         act = false;   // pursuit.py:217
       } else {
         float s2 = 0.f;
 #pragma unroll
-        for (int i = 0; i < E; ++i) { r[i] = fmaf(-s, av[i], r[i]); s2 = fmaf(r[i], r[i], s2); }
-        store_vec<E>(a.R + p * a.ld + off, r);
+        for (int i = 0; i < CPL * 4; ++i) { r.v[i] = fmaf(-s, av.v[i], r.v[i]); s2 = fmaf(r.v[i], r.v[i], s2); }
+        r.store(a.R + p * a.ld, gl, F);
         const float rn = sqrtf(group_sum<G>(s2));
         if (gl == 0) {
           S[t] = atom;
@@ -224,74 +195,79 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
         act = (t + 1 < K) && rn > a.tol[p];
       }
     } else {
-      if (a.cache_atoms) sm100::cp_async_wait_all();
       __syncwarp(gmask);
       bool dup = false;
       for (int j = 0; j < t; ++j) dup |= (S_s[j] == atom);
-      const float bt = group_sum<G>(dot_vec<E>(av, x));
-      const float gtt = group_sum<G>(dot_vec<E>(av, av));
-      // Gram column of the new atom against the support (independent dots, the
-      // row loads of several j in flight at once), then forward substitution
-      float* g_s = cn_s;  // cn is produced only after the Gram column is consumed
+      const float bt = group_sum<G>(av.dot(x));
+      const float gtt = group_sum<G>(av.dot(av));
+      // Gram column of the new atom against the support: independent dots,
+      // several rows' loads in flight at once
 #pragma unroll 4
       for (int j = 0; j < t; ++j) {
-        float sv[E];
-        if (a.cache_atoms) load_gen<E>(A_s + j * a.ld + off, sv);
-        else load_vec<E>(a.atoms + (int64_t)S_s[j] * a.ld + off, sv);
-        const float g = group_sum<G>(dot_vec<E>(sv, av));
-        if (gl == 0) g_s[j] = g;
+        Sl sv;
+        sv.load(a.atoms + (int64_t)S_s[j] * a.ld, gl, F);
+        const float g = group_sum<G>(sv.dot(av));
+        if (gl == (j % G)) g_s[j] = g;
       }
       __syncwarp(gmask);
-      float wsum = 0.f, gc = 0.f;
-      for (int j = 0; j < t; ++j) {
-        const float g = g_s[j];
-        gc = fmaf(g, c_s[j], gc);   // a . (A_S c_prev)
-        const float* Lj = L_s + j * (j + 1) / 2;
-        float v = g;
-        for (int k = 0; k < j; ++k) v = fmaf(-Lj[k], w_s[k], v);
-        v /= Lj[j];
-        w_s[j] = v;
-        wsum = fmaf(v, v, wsum);
-      }
+      float gc = 0.f;
+      for (int j = gl; j < t; j += G) gc = fmaf(g_s[j], c_s[j], gc);
+      gc = group_sum<G>(gc);         // a . (A_S c_prev)
       const float score = bt - gc;   // a . r for r = x - A_S c_prev (pursuit.py:217 check)
-      __syncwarp(gmask);  // every lane has read g_s before cn_s is overwritten
       if (dup || score == 0.f) {
         act = false;   // re-selection (or a zero score) ends the loop
       } else {
+        // forward substitution L w = g (column sweep; lane j owns rows j, j+G, ...)
+        for (int k = 0; k < t; ++k) {
+          if (gl == (k % G)) g_s[k] = g_s[k] / L_s[k * (k + 1) / 2 + k];
+          __syncwarp(gmask);
+          const float wk = g_s[k];
+          for (int j = k + 1 + ((gl - (k + 1) % G + G) % G); j < t; j += G)
+            g_s[j] = fmaf(-L_s[j * (j + 1) / 2 + k], wk, g_s[j]);
+          __syncwarp(gmask);
+        }
+        float wsum = 0.f, wy = 0.f;
+        for (int j = gl; j < t; j += G) {
+          wsum = fmaf(g_s[j], g_s[j], wsum);
+          wy = fmaf(g_s[j], y_s[j], wy);
+        }
+        wsum = group_sum<G>(wsum);
+        wy = group_sum<G>(wy);
         const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
-        float yy = bt;
-        for (int j = 0; j < t; ++j) yy = fmaf(-w_s[j], y_s[j], yy);
-        yy /= dg;
-        // back substitution L^T c = y; row t of L is (w, dg)
-        for (int j = t; j >= 0; --j) {
-          float v = j == t ? yy : y_s[j];
-          for (int k = j + 1; k <= t; ++k) {
-            const float Lkj = k == t ? w_s[j] : L_s[k * (k + 1) / 2 + j];
-            v = fmaf(-Lkj, cn_s[k], v);
-          }
-          cn_s[j] = v / (j == t ? dg : L_s[j * (j + 1) / 2 + j]);
+        const float yy = (bt - wy) / dg;
+        // back substitution L^T c = y (column sweep from the last row; row t is (w, dg)).
+        // cn_s doubles as the running right-hand side.
+        for (int j = gl; j < t; j += G) cn_s[j] = y_s[j];
+        if (gl == (t % G)) cn_s[t] = yy;
+        __syncwarp(gmask);
+        for (int k = t; k >= 0; --k) {
+          if (gl == (k % G)) cn_s[k] = cn_s[k] / (k == t ? dg : L_s[k * (k + 1) / 2 + k]);
+          __syncwarp(gmask);
+          const float ck = cn_s[k];
+          for (int j = gl; j < k; j += G)
+            cn_s[j] = fmaf(-(k == t ? g_s[j] : L_s[k * (k + 1) / 2 + j]), ck, cn_s[j]);
+          __syncwarp(gmask);
         }
         // residual r = x - A_S c with the new atom
         const float ct = cn_s[t];
 #pragma unroll
-        for (int i = 0; i < E; ++i) r[i] = fmaf(-ct, av[i], x[i]);
+        for (int i = 0; i < CPL * 4; ++i) r.v[i] = fmaf(-ct, av.v[i], x.v[i]);
 #pragma unroll 4
         for (int j = 0; j < t; ++j) {
-          float sv[E];
-          if (a.cache_atoms) load_gen<E>(A_s + j * a.ld + off, sv);
-          else load_vec<E>(a.atoms + (int64_t)S_s[j] * a.ld + off, sv);
+          Sl sv;
+          sv.load(a.atoms + (int64_t)S_s[j] * a.ld, gl, F);
           const float cj = cn_s[j];
 #pragma unroll
-          for (int i = 0; i < E; ++i) r[i] = fmaf(-cj, sv[i], r[i]);
+          for (int i = 0; i < CPL * 4; ++i) r.v[i] = fmaf(-cj, sv.v[i], r.v[i]);
         }
-        store_vec<E>(a.R + p * a.ld + off, r);
+        r.store(a.R + p * a.ld, gl, F);
         float s2 = 0.f;
 #pragma unroll
-        for (int i = 0; i < E; ++i) s2 = fmaf(r[i], r[i], s2);
+        for (int i = 0; i < CPL * 4; ++i) s2 = fmaf(r.v[i], r.v[i], s2);
         const float rn = sqrtf(group_sum<G>(s2));
         float* Lt = a.Lf + p * (int64_t)(K * (K + 1) / 2) + t * (t + 1) / 2;
         for (int i = gl; i <= t; i += G) {
-          Lt[i] = i < t ? w_s[i] : dg;
+          Lt[i] = i < t ? g_s[i] : dg;
           a.coef[p * K + i] = cn_s[i];
         }
         if (gl == 0) {
@@ -311,27 +287,30 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
 }  // namespace
 
 bool update_config(int ld, int K, UpdateCfg& c) {
-  static const int kLd[] = {32, 64, 96, 128, 160, 192, 256, 512, 1024, 1600, 2048};
-  bool ok = false;
-  for (int v : kLd) ok |= (v == ld);
-  if (!ok) return false;
-  // few lanes per patch: the scalar triangular solves run once per G lanes, so
-  // small groups keep the warp instruction count per patch low
-  int G = 1;
-  while (G < 32 && ld / G > 32) G <<= 1;
-  c.G = G;
-  c.E = ld / G;
+  (void)K;
+  const int F = ld / 4;
+  if (ld % 32 != 0 || ld > 2048) return false;
+  c.G = F <= 64 ? 8 : 32;
+  c.E = (F + c.G - 1) / c.G;   // chunks per lane (CPL)
   c.KC = 0;
-  return true;
+  switch (c.G * 100 + c.E) {
+    case 801: case 802: case 803: case 804: case 805: case 806: case 807: case 808:
+    case 3203: case 3204: case 3205: case 3206: case 3207: case 3208: case 3209: case 3210: case 3211:
+    case 3212: case 3213: case 3214: case 3215: case 3216:
+      return true;
+    default:
+      return false;
+  }
 }
 
-#define STMP_UPD_CASES(X) \
-  X(1, 32) X(2, 32) X(4, 24) X(4, 32) X(8, 20) X(8, 24) X(8, 32) X(16, 32) X(32, 32) X(32, 50) X(32, 64)
+#define STMP_UPD_CASES(X)                                                                              \
+  X(8, 1) X(8, 2) X(8, 3) X(8, 4) X(8, 5) X(8, 6) X(8, 7) X(8, 8) X(32, 3) X(32, 4) X(32, 5) X(32, 6) \
+  X(32, 7) X(32, 8) X(32, 9) X(32, 10) X(32, 11) X(32, 12) X(32, 13) X(32, 14) X(32, 15) X(32, 16)
 
 cudaError_t launch_init(const UpdateCfg& c, const UpdateArgs& a, int blocks, cudaStream_t st) {
-  switch (c.G * 1000 + c.E) {
+  switch (c.G * 100 + c.E) {
 #define STMP_INIT_CASE(g, e) \
-  case g * 1000 + e: init_kernel<g, e><<<blocks, 128, 0, st>>>(a); break;
+  case g * 100 + e: init_kernel<g, e><<<blocks, 128, 0, st>>>(a); break;
     STMP_UPD_CASES(STMP_INIT_CASE)
 #undef STMP_INIT_CASE
     default: return cudaErrorInvalidValue;
@@ -340,9 +319,9 @@ cudaError_t launch_init(const UpdateCfg& c, const UpdateArgs& a, int blocks, cud
 }
 
 cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, size_t smem, cudaStream_t st) {
-  switch (c.G * 1000 + c.E) {
+  switch (c.G * 100 + c.E) {
 #define STMP_UPD_CASE(g, e)                                                         \
-  case g * 1000 + e: {                                                              \
+  case g * 100 + e: {                                                               \
     cudaError_t err = cudaFuncSetAttribute(update_kernel<g, e>,                     \
         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                    \
     if (err != cudaSuccess) return err;                                             \
@@ -357,8 +336,9 @@ cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, s
 }
 
 size_t update_smem_bytes(const UpdateCfg& c, int K, int ld, bool cache_atoms) {
-  const int groups = 128 / c.G;
-  return (size_t)groups * (upd_scalar_floats(K) + (cache_atoms ? K * ld : 0)) * 4;
+  (void)ld;
+  (void)cache_atoms;
+  return (size_t)(128 / c.G) * upd_scalar_floats(K) * 4;
 }
 
 }  // namespace stmp
