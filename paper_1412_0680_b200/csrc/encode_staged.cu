@@ -308,6 +308,42 @@ __global__ void scatter_kernel(int64_t N, const int* active, const int* path_ws,
   }
 }
 
+// Levels with few bins: block-local histogram in shared memory, one global
+// atomic per (block, bin); each block covers kScatterPer patches.
+constexpr int kScatterThreads = 512;
+constexpr int kScatterPer = 8;
+
+__global__ void __launch_bounds__(kScatterThreads) scatter_hist_kernel(
+    int64_t N, const int* active, const int* path_ws, int L, int level, int level_base, int nbins,
+    const int* offsets, int* cursor, int* perm) {
+  extern __shared__ int sh[];  // [nbins] local counts, then [nbins] global bases
+  int* base = sh + nbins;
+  for (int b = threadIdx.x; b < nbins; b += kScatterThreads) sh[b] = 0;
+  __syncthreads();
+  int bins[kScatterPer], local[kScatterPer];
+  const int64_t p0 = (int64_t)blockIdx.x * kScatterThreads * kScatterPer + threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < kScatterPer; ++i) {
+    const int64_t p = p0 + (int64_t)i * kScatterThreads;
+    const bool act = p < N && active[p];
+    bins[i] = act ? path_ws[p * L + level - 1] - level_base : -1;
+    local[i] = act ? atomicAdd(&sh[bins[i]], 1) : 0;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += kScatterThreads) {
+    const int c = sh[b];
+    base[b] = c ? atomicAdd(&cursor[b], c) : 0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kScatterPer; ++i) {
+    if (bins[i] >= 0) {
+      const int64_t p = p0 + (int64_t)i * kScatterThreads;
+      perm[offsets[bins[i]] + base[bins[i]] + local[i]] = (int)p;
+    }
+  }
+}
+
 // Root level: a single bin holding every active patch.  One atomic per CTA.
 __global__ void __launch_bounds__(256) scatter_root_kernel(int64_t N, const int* active, const int* offsets,
                                                            int* cursor, int* perm) {
@@ -544,6 +580,11 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
                                                cursor);
       if (l == 0)
         scatter_root_kernel<<<scatter_blocks, 256, 0, st>>>(N, active, offsets, cursor, perm);
+      else if (nb <= 4096)
+        scatter_hist_kernel<<<(int)((N + kScatterThreads * kScatterPer - 1) / (kScatterThreads * kScatterPer)),
+                              kScatterThreads, (size_t)nb * 8, st>>>(N, active, path_ws, L, l,
+                                                                     (int)t->level_offsets[l], nb, offsets,
+                                                                     cursor, perm);
       else
         scatter_kernel<<<scatter_blocks, 256, 0, st>>>(N, active, path_ws, L, l, (int)t->level_offsets[l],
                                                       offsets, cursor, perm);

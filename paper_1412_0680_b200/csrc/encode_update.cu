@@ -116,8 +116,8 @@ __global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
 }
 
 // ------------------------------------------------------------------ update
-// Shared scratch per patch group (floats): S[K] | c[K] | y[K] | L[K(K+1)/2] | g[K] | cn[K]
-__host__ __device__ inline int upd_scalar_floats(int K) { return (5 * K + K * (K + 1) / 2 + 3) & ~3; }
+// Shared scratch per patch group (floats): S[K] | c[K] | y[K] | M[K(K+1)/2] | g[K] | w[K] | cn[K]
+__host__ __device__ inline int upd_scalar_floats(int K) { return (6 * K + K * (K + 1) / 2 + 3) & ~3; }
 
 template <int G, int CPL>
 __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
@@ -133,9 +133,10 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
   int* S_s = reinterpret_cast<int*>(gs);
   float* c_s = gs + K;       // previous coefficients
   float* y_s = c_s + K;      // L y = A_S x (forward-substituted rhs); reused as the back-sweep rhs
-  float* L_s = y_s + K;      // packed Cholesky factor, rows 0..t-1
-  float* g_s = L_s + K * (K + 1) / 2;  // Gram column -> new row w of L
-  float* cn_s = g_s + K;     // new coefficients
+  float* L_s = y_s + K;      // packed inverse Cholesky factor M = L^{-1}, rows 0..t-1
+  float* g_s = L_s + K * (K + 1) / 2;  // Gram column of the new atom
+  float* w_s = g_s + K;      // w = M g
+  float* cn_s = w_s + K;     // new coefficients
   const bool inb = p < a.N;
   bool act = inb && a.active[p];
   using Sl = Slice<G, CPL>;
@@ -217,37 +218,46 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
       if (dup || score == 0.f) {
         act = false;   // re-selection (or a zero score) ends the loop
       } else {
-        // forward substitution L w = g (column sweep; lane j owns rows j, j+G, ...)
-        for (int k = 0; k < t; ++k) {
-          if (gl == (k % G)) g_s[k] = g_s[k] / L_s[k * (k + 1) / 2 + k];
-          __syncwarp(gmask);
-          const float wk = g_s[k];
-          for (int j = k + 1 + ((gl - (k + 1) % G + G) % G); j < t; j += G)
-            g_s[j] = fmaf(-L_s[j * (j + 1) / 2 + k], wk, g_s[j]);
-          __syncwarp(gmask);
+        // Inverse-Cholesky refit: M = L^{-1} is kept per patch (G_S^{-1} = M^T M),
+        // so every step is a small mat-vec that the G lanes share instead of a
+        // sequential triangular sweep.
+        //   w = M g,  d = sqrt(a.a + ridge - w.w),  y_t = (b_t - w.y) / d,
+        //   new row of M: (-(1/d) w^T M, 1/d),  c = M^T y.
+        for (int j = gl; j < t; j += G) {
+          const float* Mj = L_s + j * (j + 1) / 2;
+          float acc = 0.f;
+          for (int k = 0; k <= j; ++k) acc = fmaf(Mj[k], g_s[k], acc);
+          w_s[j] = acc;
         }
+        __syncwarp(gmask);
         float wsum = 0.f, wy = 0.f;
         for (int j = gl; j < t; j += G) {
-          wsum = fmaf(g_s[j], g_s[j], wsum);
-          wy = fmaf(g_s[j], y_s[j], wy);
+          wsum = fmaf(w_s[j], w_s[j], wsum);
+          wy = fmaf(w_s[j], y_s[j], wy);
         }
         wsum = group_sum<G>(wsum);
         wy = group_sum<G>(wy);
         const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
-        const float yy = (bt - wy) / dg;
-        // back substitution L^T c = y (column sweep from the last row; row t is (w, dg)).
-        // cn_s doubles as the running right-hand side.
-        for (int j = gl; j < t; j += G) cn_s[j] = y_s[j];
-        if (gl == (t % G)) cn_s[t] = yy;
-        __syncwarp(gmask);
-        for (int k = t; k >= 0; --k) {
-          if (gl == (k % G)) cn_s[k] = cn_s[k] / (k == t ? dg : L_s[k * (k + 1) / 2 + k]);
-          __syncwarp(gmask);
-          const float ck = cn_s[k];
-          for (int j = gl; j < k; j += G)
-            cn_s[j] = fmaf(-(k == t ? g_s[j] : L_s[k * (k + 1) / 2 + j]), ck, cn_s[j]);
-          __syncwarp(gmask);
+        const float inv_d = 1.f / dg;
+        const float yy = (bt - wy) * inv_d;
+        float* Mt = a.Lf + p * (int64_t)(K * (K + 1) / 2) + t * (t + 1) / 2;
+        for (int k = gl; k <= t; k += G) {
+          float mk = inv_d, ck = 0.f;
+          if (k < t) {
+            float s1 = 0.f;
+            for (int j = k; j < t; ++j) {
+              const float Mjk = L_s[j * (j + 1) / 2 + k];
+              s1 = fmaf(w_s[j], Mjk, s1);
+              ck = fmaf(Mjk, y_s[j], ck);
+            }
+            mk = -inv_d * s1;
+          }
+          ck = fmaf(mk, yy, ck);
+          Mt[k] = mk;
+          cn_s[k] = ck;
+          a.coef[p * K + k] = ck;
         }
+        __syncwarp(gmask);
         // residual r = x - A_S c with the new atom
         const float ct = cn_s[t];
 #pragma unroll
@@ -265,11 +275,6 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
 #pragma unroll
         for (int i = 0; i < CPL * 4; ++i) s2 = fmaf(r.v[i], r.v[i], s2);
         const float rn = sqrtf(group_sum<G>(s2));
-        float* Lt = a.Lf + p * (int64_t)(K * (K + 1) / 2) + t * (t + 1) / 2;
-        for (int i = gl; i <= t; i += G) {
-          Lt[i] = i < t ? g_s[i] : dg;
-          a.coef[p * K + i] = cn_s[i];
-        }
         if (gl == 0) {
           a.yv[p * (int64_t)K + t] = yy;
           S[t] = atom;
