@@ -198,17 +198,26 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
     } else {
       __syncwarp(gmask);
       bool dup = false;
-      for (int j = 0; j < t; ++j) dup |= (S_s[j] == atom);
+      for (int j = gl; j < t; j += G) dup |= (S_s[j] == atom);
+      dup = __any_sync(gmask, dup);
       const float bt = group_sum<G>(av.dot(x));
-      const float gtt = group_sum<G>(av.dot(av));
-      // Gram column of the new atom against the support: independent dots,
-      // several rows' loads in flight at once
+      float gtt;
+      if (a.gram != nullptr) {
+        // Gram column from the precomputed atom Gram matrix: t independent scalar loads
+        const float* grow = a.gram + (int64_t)atom * a.m;
+        for (int j = gl; j < t; j += G) g_s[j] = __ldg(grow + S_s[j]);
+        gtt = __ldg(grow + atom);
+      } else {
+        gtt = group_sum<G>(av.dot(av));
+        // Gram column of the new atom against the support: independent dots,
+        // several rows' loads in flight at once
 #pragma unroll 4
-      for (int j = 0; j < t; ++j) {
-        Sl sv;
-        sv.load(a.atoms + (int64_t)S_s[j] * a.ld, gl, F);
-        const float g = group_sum<G>(sv.dot(av));
-        if (gl == (j % G)) g_s[j] = g;
+        for (int j = 0; j < t; ++j) {
+          Sl sv;
+          sv.load(a.atoms + (int64_t)S_s[j] * a.ld, gl, F);
+          const float g = group_sum<G>(sv.dot(av));
+          if (gl == (j % G)) g_s[j] = g;
+        }
       }
       __syncwarp(gmask);
       float gc = 0.f;
