@@ -124,7 +124,6 @@ int stmp_dict_create(const float* atoms, int64_t m, int32_t n, int32_t atoms_on_
 void stmp_dict_free(stmp_dict* d) {
   if (d == nullptr) return;
   cudaFree(d->atoms);
-  cudaFree(d->gram);
   delete d;
 }
 

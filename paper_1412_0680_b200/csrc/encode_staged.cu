@@ -558,7 +558,6 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   u.ip = ip; u.path_out = path; u.Lf = Lf; u.yv = yv; u.tol = tol; u.active = active;
   u.root_count = counts; u.N = N; u.leaf_sel = leaf_sel;
   u.m = d->m;
-  u.gram = method == kMethodOMP ? ensure_gram(const_cast<DictHandle*>(d), st) : nullptr;
   // stage the support atoms in shared memory when the patch groups fit comfortably
   u.cache_atoms = update_smem_bytes(uc, K, d->ld, true) <= 96 * 1024 ? 1 : 0;
 

@@ -57,7 +57,6 @@ struct UpdateArgs {
 
   int* root_count;
   const int* leaf_sel;   // written by the last score pass
-  const float* gram;     // optional [m, m] atom Gram matrix
   int64_t m;
   int cache_atoms;       // stage the support atoms in shared memory
   int64_t N;
@@ -76,9 +75,6 @@ cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, s
 size_t update_smem_bytes(const UpdateCfg& c, int K, int ld, bool cache_atoms);
 
 size_t score_smem_bytes(int kchunks, int npad);
-// Build the [m, m] Gram matrix of the (padded) dictionary on `st`; returns nullptr if
-// m exceeds kGramMaxAtoms or memory is short (the update then computes the dots).
-const float* ensure_gram(DictHandle* d, cudaStream_t st);
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
 size_t staged_workspace_bytes(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method);
 cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X, int64_t N,
