@@ -122,7 +122,6 @@ __host__ __device__ inline int upd_scalar_floats(int K) { return (6 * K + K * (K
 template <int G, int CPL>
 __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
   extern __shared__ __align__(16) float upd_smem[];
-  constexpr int kPre = 8;   // support rows prefetched into registers (rest reloaded)
   const int gpb = blockDim.x / G;
   const int grp = threadIdx.x / G;
   const int64_t p = (int64_t)blockIdx.x * gpb + grp;
@@ -133,22 +132,25 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
   float* gs = upd_smem + grp * upd_scalar_floats(K);
   int* S_s = reinterpret_cast<int*>(gs);
   float* c_s = gs + K;       // previous coefficients
-  float* y_s = c_s + K;      // y = M A_S x
+  float* y_s = c_s + K;      // L y = A_S x (forward-substituted rhs); reused as the back-sweep rhs
   float* L_s = y_s + K;      // packed inverse Cholesky factor M = L^{-1}, rows 0..t-1
   float* g_s = L_s + K * (K + 1) / 2;  // Gram column of the new atom
   float* w_s = g_s + K;      // w = M g
   float* cn_s = w_s + K;     // new coefficients
   const bool inb = p < a.N;
-  const int64_t pc = inb ? p : 0;
+  bool act = inb && a.active[p];
   using Sl = Slice<G, CPL>;
-  const bool omp = a.method == kMethodOMP;
-  // every independent load of the patch is issued up front (one round trip)
-  bool act = inb && a.active[pc];
+  // every independent load of the patch is issued before the active test
+  // (one round trip instead of two); out-of-range groups read patch 0
+  const int64_t pc = inb ? p : 0;
   const int t = a.count[pc];
   const int lsel = a.leaf_sel[pc];
+  const bool omp = a.method == kMethodOMP;
   Sl r, x;
   if (omp) {
     x.load(a.X2 + pc * a.ld2, gl, F);
+    // the patch's solver state -> shared (bounded by K, not t, so the loads
+    // do not wait for the count)
     for (int i = gl; i < K; i += G) {
       S_s[i] = a.idx[pc * K + i];
       c_s[i] = a.coef[pc * K + i];
@@ -198,25 +200,14 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
       }
     } else {
       __syncwarp(gmask);
-      // the support rows, all in flight together, kept for both the Gram
-      // column and the residual rebuild
-      Sl pre[kPre];
-#pragma unroll
-      for (int j = 0; j < kPre; ++j)
-        if (j < t) pre[j].load(a.atoms + (int64_t)S_s[j] * a.ld, gl, F);
       bool dup = false;
-      for (int j = gl; j < t; j += G) dup |= (S_s[j] == atom);
-      dup = __any_sync(gmask, dup);
+      for (int j = 0; j < t; ++j) dup |= (S_s[j] == atom);
       const float bt = group_sum<G>(av.dot(x));
       const float gtt = group_sum<G>(av.dot(av));
-#pragma unroll
-      for (int j = 0; j < kPre; ++j) {
-        if (j < t) {
-          const float g = group_sum<G>(pre[j].dot(av));
-          if (gl == (j % G)) g_s[j] = g;
-        }
-      }
-      for (int j = kPre; j < t; ++j) {
+      // Gram column of the new atom against the support: independent dots,
+      // several rows' loads in flight at once
+#pragma unroll 4
+      for (int j = 0; j < t; ++j) {
         Sl sv;
         sv.load(a.atoms + (int64_t)S_s[j] * a.ld, gl, F);
         const float g = group_sum<G>(sv.dot(av));
@@ -274,15 +265,8 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
         const float ct = cn_s[t];
 #pragma unroll
         for (int i = 0; i < CPL * 4; ++i) r.v[i] = fmaf(-ct, av.v[i], x.v[i]);
-#pragma unroll
-        for (int j = 0; j < kPre; ++j) {
-          if (j < t) {
-            const float cj = cn_s[j];
-#pragma unroll
-            for (int i = 0; i < CPL * 4; ++i) r.v[i] = fmaf(-cj, pre[j].v[i], r.v[i]);
-          }
-        }
-        for (int j = kPre; j < t; ++j) {
+#pragma unroll 4
+        for (int j = 0; j < t; ++j) {
           Sl sv;
           sv.load(a.atoms + (int64_t)S_s[j] * a.ld, gl, F);
           const float cj = cn_s[j];
