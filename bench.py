@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--score-kernel", type=int, default=1, choices=[0, 1],
+                    help="1: warp-specialized multi-stage tcgen05 score pass, 0: single-role kernel")
     return ap.parse_args()
 
 
@@ -218,6 +220,8 @@ def main():
     import paper_1412_0680_b200 as P
     from paper_1412_0680_b200 import build
     build.build()
+    from paper_1412_0680_b200 import _lib
+    _lib.set_option("score_kernel", args.score_kernel)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:

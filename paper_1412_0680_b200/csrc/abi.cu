@@ -237,6 +237,11 @@ int stmp_set_option(const char* key, int64_t value) {
     g_path_mode = (int)value;
     return STMP_OK;
   }
+  if (strcmp(key, "score_kernel") == 0) {
+    if (value < 0 || value > 1) return fail(STMP_EINVAL, "score_kernel must be 0 (single-role) or 1 (warp-specialized)");
+    stmp::g_score_ws = (int)value;
+    return STMP_OK;
+  }
   if (strcmp(key, "staged_min_batch") == 0) {
     if (value < 1) return fail(STMP_EINVAL, "staged_min_batch must be positive");
     g_staged_min = value;

@@ -25,17 +25,13 @@ namespace stmp {
 
 using namespace sm100;
 
+int g_score_ws = 1;  // 1: warp-specialized multi-stage score pass (score_ws.cu) when it fits
+
 namespace {
 
 constexpr int kTile = 128;          // patches per work item (= UMMA M)
 constexpr int kScoreThreads = 128;  // 4 warps: warp w owns TMEM lanes 32w..32w+31
 
-// Per-bin table block: [kchunks][hi|lo][npad rows x 128 B] SW128, then (last
-// level only) npad ints leaf_info (single leaf atom, or -1-child) and npad
-// ints leaf count.
-__host__ __device__ inline uint32_t table_bytes(int kch, int npad, bool last) {
-  return (uint32_t)kch * 2u * npad * 128u + (last ? 8u * npad : 0u);
-}
 
 template <int KCH>
 __device__ __forceinline__ void issue_gather(const ScoreArgs& a, const int* rows_ids, int rows,
@@ -601,7 +597,13 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       } else {
         s.leaf_sel = leaf_sel;
       }
-      switch (s.kchunks) {
+      s.tmem_cols = lv.tmem_cols;
+      if (g_score_ws && score_ws_fits(s.kchunks, lv.npad, l + 1 == L)) {
+        int cols = 32;
+        while (cols < 2 * lv.npad) cols <<= 1;
+        s.tmem_cols = cols;
+        e = launch_score_ws(s, sms, st);
+      } else switch (s.kchunks) {
         case 1: e = launch_score<1>(s, sms, st); break;
         case 2: e = launch_score<2>(s, sms, st); break;
         case 3: e = launch_score<3>(s, sms, st); break;

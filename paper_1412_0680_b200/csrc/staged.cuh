@@ -75,6 +75,17 @@ cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, s
 size_t update_smem_bytes(const UpdateCfg& c, int K, int ld, bool cache_atoms);
 
 size_t score_smem_bytes(int kchunks, int npad);
+
+// Per-bin table block: [kchunks][hi|lo][npad rows x 128 B] SW128, then (last
+// level only) npad ints leaf_info (single leaf atom, or -1-child) and npad
+// ints leaf count.
+__host__ __device__ inline uint32_t table_bytes(int kch, int npad, bool last) {
+  return (uint32_t)kch * 2u * npad * 128u + (last ? 8u * npad : 0u);
+}
+
+extern int g_score_ws;
+bool score_ws_fits(int kchunks, int npad, bool last);
+cudaError_t launch_score_ws(const ScoreArgs& s, int sms, cudaStream_t st);
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
 size_t staged_workspace_bytes(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method);
 cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X, int64_t N,

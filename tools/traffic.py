@@ -1,0 +1,47 @@
+"""Per-step DRAM traffic and time share from an ncu launch list
+(--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum) of
+`bench.py --steps 1 --warmup 1`: the second of the two encodes is the timed step."""
+import collections
+import csv
+import json
+import sys
+
+
+def load(path):
+    rows = list(csv.reader(open(path)))
+    hdr, data = None, []
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            data.append(dict(zip(hdr, r)))
+    launches = collections.OrderedDict()
+    for d in data:
+        launches.setdefault(d["ID"], {"name": d["Kernel Name"]})[d["Metric Name"]] = float(d["Metric Value"])
+    return list(launches.values())
+
+
+def main(path, out_json, patches, method="omp", selector="tree"):
+    ls = load(path)
+    half = len(ls) // 2
+    step = ls[half:]           # second encode = the timed step
+    t = sum(l.get("gpu__time_duration.sum", 0) for l in step)
+    rd = sum(l.get("dram__bytes_read.sum", 0) for l in step)
+    wr = sum(l.get("dram__bytes_write.sum", 0) for l in step)
+    per = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for l in step:
+        k = l["name"].split("(")[0].replace("void ", "")[:48]
+        per[k][0] += 1
+        per[k][1] += l.get("gpu__time_duration.sum", 0)
+        per[k][2] += l.get("dram__bytes_read.sum", 0) + l.get("dram__bytes_write.sum", 0)
+    summary = {"patches": patches, "method": method, "selector": selector, "launches": len(step),
+               "bytes_per_launch": rd + wr, "serialized_ns": t,
+               "note": "dram bytes summed over every kernel of one staged step (ncu, cold caches, serialised)",
+               "kernels": {k: {"launches": c, "time_share": tt / t, "dram_bytes": b} for k, (c, tt, b) in per.items()}}
+    json.dump(summary, open(out_json, "w"), indent=1)
+    print(json.dumps(summary, indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]))
