@@ -25,7 +25,7 @@ namespace stmp {
 
 using namespace sm100;
 
-int g_score_ws = 1;  // 1: warp-specialized multi-stage score pass (score_ws.cu) when it fits
+int g_score_ws = 0;  // 1: warp-specialized multi-stage score pass (score_ws.cu) when it fits
 
 namespace {
 

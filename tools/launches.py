@@ -15,6 +15,8 @@ def summarize(path, encodes=1):
             data.append(dict(zip(hdr, r)))
     agg = collections.defaultdict(lambda: [0, 0.0])
     for d in data:
+        if d.get("Metric Name") != "gpu__time_duration.sum":
+            continue
         k = d["Kernel Name"][:60]
         agg[k][0] += 1
         agg[k][1] += float(d["Metric Value"])
