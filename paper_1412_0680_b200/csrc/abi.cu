@@ -124,6 +124,7 @@ int stmp_dict_create(const float* atoms, int64_t m, int32_t n, int32_t atoms_on_
 void stmp_dict_free(stmp_dict* d) {
   if (d == nullptr) return;
   cudaFree(d->atoms);
+  cudaFree(d->gram);
   delete d;
 }
 
@@ -235,6 +236,11 @@ int stmp_set_option(const char* key, int64_t value) {
   if (strcmp(key, "path") == 0) {
     if (value < 0 || value > 2) return fail(STMP_EINVAL, "path must be 0 (auto), 1 (fused) or 2 (staged)");
     g_path_mode = (int)value;
+    return STMP_OK;
+  }
+  if (strcmp(key, "update_kernel") == 0) {
+    if (value < 0 || value > 1) return fail(STMP_EINVAL, "update_kernel must be 0 (generic) or 1 (K<=8 Gram-table OMP)");
+    stmp::g_update_omp8 = (int)value;
     return STMP_OK;
   }
   if (strcmp(key, "score_kernel") == 0) {

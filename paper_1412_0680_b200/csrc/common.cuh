@@ -20,7 +20,12 @@ struct DictHandle {
   int ld = 0;              // padded row stride = 32 * vpl
   int vpl = 0;             // values per lane for the warp-per-patch kernels
   uint64_t fingerprint = 0;
+  float* gram = nullptr;   // optional [m, m] f32 atom Gram matrix (built lazily, small m only)
+  bool gram_tried = false;
 };
+
+// Gram table policy: m^2 floats must stay below this (c0: 64 MB, c1: 1 GB).
+constexpr int64_t kGramMaxAtoms = 32768;
 
 
 struct StagedLevel {

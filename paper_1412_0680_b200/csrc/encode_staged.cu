@@ -25,6 +25,7 @@ namespace stmp {
 
 using namespace sm100;
 
+int g_update_omp8 = 1;  // 1: K <= 8 OMP update with the Gram table (encode_update.cu)
 int g_score_ws = 0;  // 1: warp-specialized multi-stage score pass (score_ws.cu) when it fits
 
 namespace {
@@ -553,6 +554,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   u.tol_abs = tol_abs; u.idx = idx; u.coef = coef; u.count = count; u.resnorm = resnorm;
   u.ip = ip; u.path_out = path; u.Lf = Lf; u.yv = yv; u.tol = tol; u.active = active;
   u.root_count = counts; u.N = N; u.leaf_sel = leaf_sel;
+  u.gram = (method == kMethodOMP && K <= 8 && g_update_omp8) ? ensure_gram(const_cast<DictHandle*>(d), st) : nullptr;
   u.m = d->m;
   // stage the support atoms in shared memory when the patch groups fit comfortably
   u.cache_atoms = update_smem_bytes(uc, K, d->ld, true) <= 96 * 1024 ? 1 : 0;
@@ -615,7 +617,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       }
       if (e != cudaSuccess) return e;
     }
-    if ((e = launch_update(uc, u, ublocks, usmem, st)) != cudaSuccess) return e;
+    e = u.gram ? launch_update_omp8(u, ublocks, st) : launch_update(uc, u, ublocks, usmem, st);
+    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }

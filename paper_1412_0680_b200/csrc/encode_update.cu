@@ -292,7 +292,163 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
   count_root(act && gl == 0, a.root_count);
 }
 
+// ------------------------------------------------------------------ OMP update, K <= 8
+// Specialisation for the common small-K case with an atom Gram table: the 8
+// lanes of a patch group own one row each of the inverse Cholesky factor M
+// (and the matching y_j, c_j), every lane holds the whole Gram column, and the
+// column sums of the refit are butterfly all-reductions -- no shared memory,
+// no data-dependent loops, one global round trip for all of the patch state.
+template <int CPL>
+__global__ void __launch_bounds__(128) update_omp8_kernel(UpdateArgs a) {
+  constexpr int G = 8, KM = 8;
+  const int64_t p = (int64_t)blockIdx.x * (128 / G) + threadIdx.x / G;
+  const int gl = threadIdx.x % G;
+  const int K = a.K;
+  const int F = a.ld >> 2;
+  const int KK = K * (K + 1) / 2;
+  using Sl = Slice<G, CPL>;
+  const bool inb = p < a.N;
+  const int64_t pc = inb ? p : 0;
+  // ---- every independent load of the patch, issued together
+  bool act = inb && a.active[pc];
+  const int t = a.count[pc];
+  const int lsel = a.leaf_sel[pc];
+  Sl x;
+  x.load(a.X2 + pc * a.ld2, gl, F);
+  int S[KM];
+#pragma unroll
+  for (int k = 0; k < KM; ++k) S[k] = k < K ? a.idx[pc * K + k] : -1;
+  const bool own = gl < K;
+  const float cj = own ? a.coef[pc * K + gl] : 0.f;
+  const float yj = own ? a.yv[pc * K + gl] : 0.f;
+  float mrow[KM];
+  const float* Mrow = a.Lf + pc * KK + gl * (gl + 1) / 2;
+#pragma unroll
+  for (int k = 0; k < KM; ++k) mrow[k] = (own && k <= gl) ? Mrow[k] : 0.f;
+
+  if (act) {
+    Sl r;
+    int atom = lsel;
+    if (lsel < 0) {  // multi-atom leaf: max |a . r|, ties to the lowest atom index
+      r.load(a.R + p * a.ld, gl, F);
+      const int node = -1 - lsel;
+      const int cb = __ldg(a.child_begin + node), cc = __ldg(a.child_count + node);
+      float bestv = -1.f;
+      atom = __ldg(a.leaf_atom + cb);
+      for (int j = 0; j < cc; ++j) {
+        const int aj = __ldg(a.leaf_atom + cb + j);
+        Sl v;
+        v.load(a.atoms + (int64_t)aj * a.ld, gl, F);
+        const float mv = fabsf(group_sum<G>(v.dot(r)));
+        if (mv > bestv || (mv == bestv && aj < atom)) { bestv = mv; atom = aj; }
+      }
+    }
+    Sl av;
+    av.load(a.atoms + (int64_t)atom * a.ld, gl, F);
+    const float* grow = a.gram + (int64_t)atom * a.m;
+    float g[KM];
+    bool dup = false;
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {
+      const bool in = k < t;
+      g[k] = in ? __ldg(grow + S[k]) : 0.f;
+      dup |= in && S[k] == atom;
+    }
+    const float gtt = __ldg(grow + atom);
+    const float bt = group_sum<G>(av.dot(x));
+    float gmine = 0.f;   // g[gl] without dynamic indexing
+#pragma unroll
+    for (int k = 0; k < KM; ++k) gmine = k == gl ? g[k] : gmine;
+    const bool row_live = gl < t;
+    const float gc = group_sum<G>(row_live ? gmine * cj : 0.f);   // a . (A_S c_prev)
+    const float score = bt - gc;   // a . r for r = x - A_S c_prev (pursuit.py:217 check)
+    if (dup || score == 0.f) {
+      act = false;   // re-selection (or a zero score) ends the loop
+    } else {
+      // w = M g (lane j: row j), then the column sums  sum_j w_j M[j][k]  and  sum_j y_j M[j][k]
+      float wj = 0.f;
+#pragma unroll
+      for (int k = 0; k < KM; ++k) wj = fmaf(mrow[k], g[k], wj);
+      if (!row_live) wj = 0.f;
+      const float wsum = group_sum<G>(wj * wj);
+      const float wy = group_sum<G>(row_live ? wj * yj : 0.f);
+      const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
+      const float inv_d = 1.f / dg;
+      const float yy = (bt - wy) * inv_d;
+      float colw[KM], coly[KM];
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        colw[k] = row_live ? wj * mrow[k] : 0.f;
+        coly[k] = row_live ? yj * mrow[k] : 0.f;
+      }
+#pragma unroll
+      for (int o = G >> 1; o; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < KM; ++k) {
+          colw[k] += __shfl_xor_sync(group_mask<G>(), colw[k], o);
+          coly[k] += __shfl_xor_sync(group_mask<G>(), coly[k], o);
+        }
+      }
+      // new row t of M: (-(1/d) w^T M, 1/d);  c = M^T y with y_t = yy
+      float c[KM];
+      float mt_mine = 0.f, c_mine = 0.f;
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        const float mtk = k < t ? -inv_d * colw[k] : (k == t ? inv_d : 0.f);
+        c[k] = k < t ? fmaf(mtk, yy, coly[k]) : (k == t ? inv_d * yy : 0.f);
+        if (k == gl) { mt_mine = mtk; c_mine = c[k]; }
+      }
+      // residual r = x - A_S c (support rows from L2) - c_t a
+      const float ct = inv_d * yy;
+#pragma unroll
+      for (int i = 0; i < CPL * 4; ++i) r.v[i] = fmaf(-ct, av.v[i], x.v[i]);
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        if (k < t) {
+          Sl sv;
+          sv.load(a.atoms + (int64_t)S[k] * a.ld, gl, F);
+#pragma unroll
+          for (int i = 0; i < CPL * 4; ++i) r.v[i] = fmaf(-c[k], sv.v[i], r.v[i]);
+        }
+      }
+      r.store(a.R + p * a.ld, gl, F);
+      float s2 = 0.f;
+#pragma unroll
+      for (int i = 0; i < CPL * 4; ++i) s2 = fmaf(r.v[i], r.v[i], s2);
+      const float rn = sqrtf(group_sum<G>(s2));
+      if (gl <= t) {
+        a.Lf[p * KK + t * (t + 1) / 2 + gl] = mt_mine;
+        a.coef[p * K + gl] = c_mine;
+      }
+      if (gl == 0) {
+        a.yv[p * K + t] = yy;
+        a.idx[p * K + t] = atom;
+        a.count[p] = t + 1;
+        a.resnorm[p] = rn;
+      }
+      act = (t + 1 < K) && rn > a.tol[p];
+    }
+    if (gl == 0) a.active[p] = act ? 1 : 0;
+  }
+  count_root(act && gl == 0, a.root_count);
+}
+
 }  // namespace
+
+cudaError_t launch_update_omp8(const UpdateArgs& a, int blocks, cudaStream_t st) {
+  if (a.gram == nullptr || a.K > 8 || a.method != kMethodOMP) return cudaErrorNotSupported;
+  const int F = a.ld / 4;
+  const int cpl = (F + 7) / 8;
+  switch (cpl) {
+    case 1: update_omp8_kernel<1><<<blocks, 128, 0, st>>>(a); break;
+    case 2: update_omp8_kernel<2><<<blocks, 128, 0, st>>>(a); break;
+    case 3: update_omp8_kernel<3><<<blocks, 128, 0, st>>>(a); break;
+    case 4: update_omp8_kernel<4><<<blocks, 128, 0, st>>>(a); break;
+    case 5: update_omp8_kernel<5><<<blocks, 128, 0, st>>>(a); break;
+    default: return cudaErrorNotSupported;
+  }
+  return cudaGetLastError();
+}
 
 bool update_config(int ld, int K, UpdateCfg& c) {
   (void)K;

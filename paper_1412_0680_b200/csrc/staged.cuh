@@ -50,13 +50,14 @@ struct UpdateArgs {
   float* resnorm;
   int32_t* ip;
   int32_t* path_out;
-  float* Lf;             // packed Cholesky factor per patch
-  float* yv;             // forward-substituted rhs per patch
+  float* Lf;             // packed inverse Cholesky factor M = L^{-1} per patch
+  float* yv;             // y = M A_S x per patch
   float* tol;
   int* active;
 
   int* root_count;
   const int* leaf_sel;   // written by the last score pass
+  const float* gram;     // optional [m, m] atom Gram matrix (enables the 8-lane OMP kernel)
   int64_t m;
   int cache_atoms;       // stage the support atoms in shared memory
   int64_t N;
@@ -73,6 +74,12 @@ cudaError_t launch_init(const UpdateCfg& c, const UpdateArgs& a, int blocks, cud
 cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, size_t smem,
                           cudaStream_t st);
 size_t update_smem_bytes(const UpdateCfg& c, int K, int ld, bool cache_atoms);
+// OMP update specialised for K <= 8 with a Gram table: one lane per Cholesky row,
+// all solver state in registers.  Returns cudaErrorNotSupported when not applicable.
+cudaError_t launch_update_omp8(const UpdateArgs& a, int blocks, cudaStream_t st);
+// Build the [m, m] Gram matrix of the (padded) dictionary on `st`; returns nullptr if
+// m exceeds kGramMaxAtoms or memory is short.
+const float* ensure_gram(DictHandle* d, cudaStream_t st);
 
 size_t score_smem_bytes(int kchunks, int npad);
 
@@ -84,6 +91,7 @@ __host__ __device__ inline uint32_t table_bytes(int kch, int npad, bool last) {
 }
 
 extern int g_score_ws;
+extern int g_update_omp8;
 bool score_ws_fits(int kchunks, int npad, bool last);
 cudaError_t launch_score_ws(const ScoreArgs& s, int sms, cudaStream_t st);
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
