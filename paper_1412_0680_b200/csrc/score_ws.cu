@@ -130,42 +130,66 @@ __global__ void __launch_bounds__(kWsThreads, 1) score_ws_kernel(ScoreArgs a) {
 
   if (warp < 4) {
     // ============================ producers ============================
+    // Per tile: (1) prepare tile jj+NS-1 -- its item record, patch ids and node
+    // metadata are loaded into registers (loads in flight, nothing waits);
+    // (2) wait for tile jj's rows, split them, publish; (3) launch tile
+    // jj+NS-1's gather + table copy from the prepared registers.  The id
+    // round trip overlaps the split instead of sitting on the critical path.
     const int pt = tid;
-    auto issue = [&](int q) {
+    constexpr int kSlots = F;  // e-slots per thread: e = pt + 128*k
+    int rid[kSlots];
+    int4 pit = make_int4(0, 0, 0, 0);
+    int pcb = 0, pcc = 0;
+    auto prepare = [&](int q) {
+      pit = a.items[i0 + q];
+#pragma unroll
+      for (int k = 0; k < kSlots; ++k) {
+        const int row = (pt + 128 * k) / F;
+        rid[k] = row < pit.z ? a.perm[pit.y + row] : 0;
+      }
+      if (pt == 0) {
+        const int gnode = a.level_base + pit.x;
+        pcb = __ldg(a.child_begin + gnode);
+        pcc = __ldg(a.child_count + gnode);
+      }
+    };
+    auto launch = [&](int q) {
       const int s = q % NS;
-      const int4 it = a.items[i0 + q];
       const uint32_t dst = smem_u32(raw + s * kPlane);
-#pragma unroll 4
-      for (int e = pt; e < kT * F; e += 128) {
+#pragma unroll
+      for (int k = 0; k < kSlots; ++k) {
+        const int e = pt + 128 * k;
         const int row = e / F;
         const int c = e - row * F;
-        const bool ok = row < it.z;
-        const int rid = ok ? a.perm[it.y + row] : 0;
-        if (c == 0 && ok) st_rows[s * kT + row] = rid;
+        const bool ok = row < pit.z;
+        if (c == 0 && ok) st_rows[s * kT + row] = rid[k];
         const uint32_t off = (uint32_t)(c >> 3) * (kT * 128u) + sw128_offset(row, c & 7);
-        cp_async16(dst + off, a.R + (int64_t)rid * a.ld + 4 * c, ok ? 16u : 0u);
+        cp_async16(dst + off, a.R + (int64_t)rid[k] * a.ld + 4 * c, ok ? 16u : 0u);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
       if (pt == 0) {
-        const int gnode = a.level_base + it.x;
         StageMeta m;
-        m.bin = it.x; m.start = it.y; m.rows = it.z;
-        m.cb = __ldg(a.child_begin + gnode);
-        m.cc = __ldg(a.child_count + gnode);
+        m.bin = pit.x; m.start = pit.y; m.rows = pit.z;
+        m.cb = pcb; m.cc = pcc;
         m.pad0 = m.pad1 = m.pad2 = 0;
         st_meta[s] = m;
         mbar_arrive_expect_tx(tab_full + s, tb);
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.table) + (size_t)it.x * tb;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.table) + (size_t)pit.x * tb;
         for (uint32_t off = 0; off < tb; off += 65536u)
           bulk_g2s(btab + s * tb_al + off, src + off, min(65536u, tb - off), tab_full + s);
       }
     };
-    for (int q = 0; q < NS - 1 && q < n; ++q) issue(q);
+    for (int q = 0; q < NS - 1 && q < n; ++q) {
+      prepare(q);
+      launch(q);
+    }
     for (int jj = 0; jj < n; ++jj) {
       const int s = jj % NS;
+      const int q = jj + NS - 1;
+      if (q < n) prepare(q);
       if (jj >= 1) mbar_wait(mma_done, (uint32_t)((jj - 1) & 1));
-      if (jj + NS - 1 < n) issue(jj + NS - 1);
-      cp_async_wait_n(min(NS - 1, n - 1 - jj));
+      // groups committed so far: tiles 0 .. min(n, jj+NS-1)-1
+      cp_async_wait_n(min(NS - 2, n - 1 - jj));
       named_bar(1, 128);  // every producer's copies of tile jj have landed
       const int acc = jj & 1;
       if (jj >= 2) mbar_wait(acc_empty + acc, (uint32_t)(((jj >> 1) - 1) & 1));
@@ -195,6 +219,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) score_ws_kernel(ScoreArgs a) {
       }
       fence_proxy_async_smem();
       mbar_arrive(ab_full);
+      // slot (jj-1) % NS is free (MMA jj-1 done): launch the prepared tile into it
+      if (q < n) {
+        named_bar(1, 128);  // every producer has read st_meta / st_rows of tile jj
+        launch(q);
+      }
     }
   } else if (warp == 8) {
     // ============================ MMA issuer ============================
