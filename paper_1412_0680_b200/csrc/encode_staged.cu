@@ -600,7 +600,9 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
         s.leaf_sel = leaf_sel;
       }
       s.tmem_cols = lv.tmem_cols;
-      if (g_score_ws && score_ws_fits(s.kchunks, lv.npad, l + 1 == L)) {
+      if (g_score_ws == 2 && score_ts_fits(s.kchunks, lv.npad, l + 1 == L)) {
+        e = launch_score_ts(s, sms, st);
+      } else if (g_score_ws == 1 && score_ws_fits(s.kchunks, lv.npad, l + 1 == L)) {
         int cols = 32;
         while (cols < 2 * lv.npad) cols <<= 1;
         s.tmem_cols = cols;

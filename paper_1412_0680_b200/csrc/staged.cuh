@@ -94,6 +94,8 @@ extern int g_score_ws;
 extern int g_update_omp8;
 bool score_ws_fits(int kchunks, int npad, bool last);
 cudaError_t launch_score_ws(const ScoreArgs& s, int sms, cudaStream_t st);
+bool score_ts_fits(int kchunks, int npad, bool last);
+cudaError_t launch_score_ts(const ScoreArgs& s, int sms, cudaStream_t st);
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
 size_t staged_workspace_bytes(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method);
 cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X, int64_t N,

@@ -28,13 +28,16 @@ def P():
     return pkg
 
 
-@pytest.fixture(params=["fused", "staged"])
+@pytest.fixture(params=["fused", "staged", "staged-ws", "staged-ts"])
 def path(request):
-    """Force one encoder implementation (the C ABI 'path' option) for the test."""
+    """Force one encoder implementation (the C ABI 'path' / 'score_kernel' options)."""
     from paper_1412_0680_b200 import _lib
-    _lib.set_option("path", {"fused": _lib.PATH_FUSED, "staged": _lib.PATH_STAGED}[request.param])
-    yield request.param
+    mode = request.param
+    _lib.set_option("path", _lib.PATH_FUSED if mode == "fused" else _lib.PATH_STAGED)
+    _lib.set_option("score_kernel", {"staged-ws": 1, "staged-ts": 2}.get(mode, 0))
+    yield mode
     _lib.set_option("path", _lib.PATH_AUTO)
+    _lib.set_option("score_kernel", 0)
 
 
 def as_np(res):
