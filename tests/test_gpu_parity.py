@@ -34,10 +34,10 @@ def path(request):
     from paper_1412_0680_b200 import _lib
     mode = request.param
     _lib.set_option("path", _lib.PATH_FUSED if mode == "fused" else _lib.PATH_STAGED)
-    _lib.set_option("score_kernel", {"staged-ws": 1, "staged-ts": 2}.get(mode, 0))
+    _lib.set_option("score_kernel", {"staged-ws": 1, "staged": 0}.get(mode, 2))
     yield mode
     _lib.set_option("path", _lib.PATH_AUTO)
-    _lib.set_option("score_kernel", 0)
+    _lib.set_option("score_kernel", 2)
 
 
 def as_np(res):
