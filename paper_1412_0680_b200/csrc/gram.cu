@@ -70,7 +70,8 @@ const float* ensure_gram(DictHandle* d, cudaStream_t st) {
   }
   const dim3 grid((unsigned)((d->m + kGT - 1) / kGT), (unsigned)((d->m + kGT - 1) / kGT));
   gram_kernel<<<grid, 256, 0, st>>>(d->atoms, d->m, d->ld, g);
-  if (cudaGetLastError() != cudaSuccess) {
+  // one-time build: finish it before any stream can read the table
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
     cudaFree(g);
     return nullptr;
   }
