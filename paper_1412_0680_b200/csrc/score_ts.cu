@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a) {
       if (kc > 0) {  // the previous chunk's MMAs must have consumed the A columns
         mbar_wait(&bars[1], mma_phase);
         mma_phase ^= 1u;
+        tc_fence_after();  // order the tcgen05.st below after the MMAs' completion
       }
       tmem_st32(tmem + lane_base + kColA, hi);
       tmem_st32(tmem + lane_base + kColA + 32, lo);

@@ -34,10 +34,36 @@ def path(request):
     from paper_1412_0680_b200 import _lib
     mode = request.param
     _lib.set_option("path", _lib.PATH_FUSED if mode == "fused" else _lib.PATH_STAGED)
-    _lib.set_option("score_kernel", {"staged-ws": 1, "staged": 0}.get(mode, 2))
+    _lib.set_option("score_kernel", {"staged-ws": 1, "staged-ts": 2}.get(mode, 0))
     yield mode
     _lib.set_option("path", _lib.PATH_AUTO)
-    _lib.set_option("score_kernel", 2)
+    _lib.set_option("score_kernel", 0)
+
+
+@pytest.mark.parametrize("score_kernel", [0, 1, 2])
+def test_staged_is_deterministic_and_batch_invariant(score_kernel):
+    """262,144 config-1 patches: two runs and a run in 8192-patch batches must agree
+    bitwise (each patch's arithmetic is independent of bucketing order)."""
+    from paper_1412_0680_b200 import _lib
+    from paper_1412_0680_b200 import workloads as W
+    cfg, wl, flat = config(1)
+    X = torch.as_tensor(W.make_patches(wl, 262144)).cuda()
+    sel = P().TreeSelector(flat, wl.atoms, cfg.alpha)
+    _lib.set_option("path", _lib.PATH_STAGED)
+    _lib.set_option("score_kernel", score_kernel)
+    try:
+        a = P().encode(sel, X, cfg.K, method="omp")
+        b = P().encode(sel, X, cfg.K, method="omp")
+        c = [P().encode(sel, X[s:s + 8192], cfg.K, method="omp") for s in range(0, len(X), 8192)]
+        torch.cuda.synchronize()
+        ci = torch.cat([r.idx for r in c])
+        cc = torch.cat([r.coef for r in c])
+        assert int((a.idx != b.idx).any(1).sum()) == 0
+        assert int((a.idx != ci).any(1).sum()) == 0
+        assert bool(torch.equal(a.coef, cc))
+    finally:
+        _lib.set_option("path", _lib.PATH_AUTO)
+        _lib.set_option("score_kernel", 0)
 
 
 def as_np(res):
