@@ -238,10 +238,6 @@ int stmp_set_option(const char* key, int64_t value) {
     g_path_mode = (int)value;
     return STMP_OK;
   }
-  if (strcmp(key, "ts_variant") == 0) {
-    stmp::g_ts_variant = (int)value;
-    return STMP_OK;
-  }
   if (strcmp(key, "update_kernel") == 0) {
     if (value < 0 || value > 1) return fail(STMP_EINVAL, "update_kernel must be 0 (generic) or 1 (K<=8 Gram-table OMP)");
     stmp::g_update_omp8 = (int)value;

@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
       leaf_cnt = s_leaf_cnt[best];
     }
     if (has_next && tid < nit.z) s_rows[(buf ^ 1) * kTile + tid] = nperm;
+    fence_proxy_async_smem();  // leaf metadata reads before the async-proxy table refill
     __syncthreads();  // s_rows of the next item visible; leaf metadata read
     if (has_next) {
       const bool new_tab = nit.x != loaded_bin;

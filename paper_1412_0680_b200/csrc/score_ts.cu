@@ -18,11 +18,7 @@ namespace stmp {
 
 using namespace sm100;
 
-int g_ts_variant = 0;  // debug bits: 1 gather after MMA wait, 2 one CTA/SM, 4 proxy fence before table refill
-
 namespace {
-
-__device__ int g_ts_variant_dev;
 
 constexpr int kT = 128;
 constexpr int kThreads = 128;   // thread = patch row; warp w owns TMEM lanes 32w..32w+31
@@ -187,8 +183,7 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a) {
       table_pending = false;
     }
     // launch the next tile's gather; it overlaps the MMAs and this tile's epilogue
-    const bool early = (g_ts_variant_dev & 1) == 0;
-    if (has_next && early) {
+    if (has_next) {
       __syncthreads();  // s_rows of the next tile visible
       gather_rows<KCH>(a, s_rows + (buf ^ 1) * kT, nit.z, raw_s, tid);
     }
@@ -196,10 +191,6 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a) {
     mbar_wait(&bars[1], mma_phase);
     mma_phase ^= 1u;
     tc_fence_after();
-    if (has_next && !early) {
-      __syncthreads();
-      gather_rows<KCH>(a, s_rows + (buf ^ 1) * kT, nit.z, raw_s, tid);
-    }
 
     int best = 0;
     float bestv = -1.f;
@@ -223,8 +214,10 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a) {
       leaf_info = s_leaf_info[best];
       leaf_cnt = s_leaf_cnt[best];
     }
-    if (g_ts_variant_dev & 4) fence_proxy_async_smem();
-    __syncthreads();  // leaf metadata read before the table slot is refilled
+    // generic-proxy reads of the table block (leaf metadata) must be ordered
+    // before the async-proxy bulk copy that refills it
+    fence_proxy_async_smem();
+    __syncthreads();
     if (has_next && nit.x != loaded_bin) {
       if (tid == 0) {
         mbar_arrive_expect_tx(&bars[0], tb);
@@ -273,10 +266,7 @@ cudaError_t launch_ts_kch(ScoreArgs s, int sms, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int by_smem = (int)((228 * 1024) / (smem + 1024));
   const int by_tmem = 512 / cols;
-  int per_sm = std::max(1, std::min(4, std::min(by_smem, by_tmem)));
-  if (g_ts_variant & 2) per_sm = 1;
-  e = cudaMemcpyToSymbolAsync(g_ts_variant_dev, &g_ts_variant, sizeof(int), 0, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return e;
+  const int per_sm = std::max(1, std::min(4, std::min(by_smem, by_tmem)));
   score_ts_kernel<KCH><<<sms * per_sm, kThreads, smem, st>>>(s);
   return cudaGetLastError();
 }

@@ -91,7 +91,6 @@ __host__ __device__ inline uint32_t table_bytes(int kch, int npad, bool last) {
 }
 
 extern int g_score_ws;
-extern int g_ts_variant;
 extern int g_update_omp8;
 bool score_ws_fits(int kchunks, int npad, bool last);
 cudaError_t launch_score_ws(const ScoreArgs& s, int sms, cudaStream_t st);
