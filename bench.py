@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--score-kernel", type=int, default=0, choices=[0, 1, 2],
+    ap.add_argument("--score-kernel", type=int, default=2, choices=[0, 1, 2],
                     help="tcgen05 score pass: 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM")
     return ap.parse_args()
 

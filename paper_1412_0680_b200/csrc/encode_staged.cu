@@ -26,7 +26,7 @@ namespace stmp {
 using namespace sm100;
 
 int g_update_omp8 = 1;  // 1: K <= 8 OMP update with the Gram table (encode_update.cu)
-int g_score_ws = 0;  // 0 single-role (default), 1 warp-specialized multi-stage, 2 A operand in TMEM
+int g_score_ws = 2;  // 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM (default)
 
 namespace {
 
