@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -54,6 +55,48 @@ int check_device() {
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
   if (major != 10)
     return fail(STMP_ECUDA, "device compute capability %d.x: this library is built for sm_100a only", major);
+  return STMP_OK;
+}
+
+// Device staging of the host-buffer entry point, one per stream, grown on demand.
+struct HostStage {
+  cudaStream_t st = nullptr;
+  int64_t cap_rows = 0;
+  int cap_n = 0, cap_K = 0;
+  size_t cap_ws = 0;
+  float* dX = nullptr;
+  int32_t* dI = nullptr;
+  float* dC = nullptr;
+  int32_t* dN = nullptr;
+  float* dR = nullptr;
+  int32_t* dP = nullptr;
+  void* dW = nullptr;
+};
+constexpr int kHostStreams = 3;
+std::mutex g_host_mutex;
+HostStage g_host[kHostStreams];
+
+int ensure_stage(HostStage& h, int64_t rows, int n, int K, size_t ws) {
+  if (h.st == nullptr) STMP_CUDA(cudaStreamCreateWithFlags(&h.st, cudaStreamNonBlocking), "stream create");
+  if (rows > h.cap_rows || n > h.cap_n || K > h.cap_K) {
+    cudaStreamSynchronize(h.st);
+    cudaFree(h.dX); cudaFree(h.dI); cudaFree(h.dC); cudaFree(h.dN); cudaFree(h.dR); cudaFree(h.dP);
+    h.cap_rows = std::max(rows, h.cap_rows);
+    h.cap_n = std::max(n, h.cap_n);
+    h.cap_K = std::max(K, h.cap_K);
+    STMP_CUDA(cudaMalloc(&h.dX, h.cap_rows * h.cap_n * sizeof(float)), "staging alloc");
+    STMP_CUDA(cudaMalloc(&h.dI, h.cap_rows * h.cap_K * sizeof(int32_t)), "staging alloc");
+    STMP_CUDA(cudaMalloc(&h.dC, h.cap_rows * h.cap_K * sizeof(float)), "staging alloc");
+    STMP_CUDA(cudaMalloc(&h.dN, h.cap_rows * sizeof(int32_t)), "staging alloc");
+    STMP_CUDA(cudaMalloc(&h.dR, h.cap_rows * sizeof(float)), "staging alloc");
+    STMP_CUDA(cudaMalloc(&h.dP, h.cap_rows * 2 * sizeof(int32_t)), "staging alloc");
+  }
+  if (ws > h.cap_ws) {
+    cudaStreamSynchronize(h.st);
+    cudaFree(h.dW);
+    STMP_CUDA(cudaMalloc(&h.dW, ws), "workspace alloc");
+    h.cap_ws = ws;
+  }
   return STMP_OK;
 }
 
@@ -359,51 +402,37 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
   if (N == 0) return STMP_OK;
   if (X == nullptr || idx == nullptr || coef == nullptr)
     return fail(STMP_EINVAL, "X, idx and coef must be host pointers");
-  if (chunk <= 0) chunk = 65536;
+  if (chunk <= 0) chunk = 1 << 17;
   if (chunk > N) chunk = N;
-  const int NS = 2;
-  cudaStream_t st[NS];
-  float* dX[NS] = {};
-  int32_t* dI[NS] = {};
-  float* dC[NS] = {};
-  int32_t* dN[NS] = {};
-  float* dR[NS] = {};
-  int32_t* dP[NS] = {};
-  void* dW[NS] = {};
+  // Persistent staging: device buffers and streams are kept between calls
+  // (allocating ~1 GB of workspace per call would dominate the host path).
+  std::lock_guard<std::mutex> lock(g_host_mutex);
   const size_t wsz = stmp_encode_workspace(d, t, chunk, K, method);
+  for (int i = 0; i < kHostStreams; ++i)
+    if (int rc = ensure_stage(g_host[i], chunk, d->n, K, wsz)) return rc;
   int rc = STMP_OK;
-  for (int i = 0; i < NS; ++i) {
-    STMP_CUDA(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking), "stream create");
-    STMP_CUDA(cudaMalloc(&dX[i], chunk * d->n * sizeof(float)), "staging alloc");
-    STMP_CUDA(cudaMalloc(&dI[i], chunk * K * sizeof(int32_t)), "staging alloc");
-    STMP_CUDA(cudaMalloc(&dC[i], chunk * K * sizeof(float)), "staging alloc");
-    STMP_CUDA(cudaMalloc(&dN[i], chunk * sizeof(int32_t)), "staging alloc");
-    STMP_CUDA(cudaMalloc(&dR[i], chunk * sizeof(float)), "staging alloc");
-    STMP_CUDA(cudaMalloc(&dP[i], chunk * 2 * sizeof(int32_t)), "staging alloc");
-    if (wsz) STMP_CUDA(cudaMalloc(&dW[i], wsz), "workspace alloc");
-  }
   int64_t ci = 0;
   for (int64_t s0 = 0; s0 < N && rc == STMP_OK; s0 += chunk, ++ci) {
-    const int b = (int)(ci % NS);
+    HostStage& h = g_host[ci % kHostStreams];
     const int64_t rows = std::min(chunk, N - s0);
-    cudaError_t e = cudaMemcpy2DAsync(dX[b], d->n * sizeof(float), X + s0 * ldx, ldx * sizeof(float),
-                                      d->n * sizeof(float), rows, cudaMemcpyHostToDevice, st[b]);
+    cudaError_t e = ldx == d->n
+        ? cudaMemcpyAsync(h.dX, X + s0 * ldx, rows * d->n * sizeof(float), cudaMemcpyHostToDevice, h.st)
+        : cudaMemcpy2DAsync(h.dX, d->n * sizeof(float), X + s0 * ldx, ldx * sizeof(float),
+                            d->n * sizeof(float), rows, cudaMemcpyHostToDevice, h.st);
     if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
-    rc = stmp_encode(d, t, dX[b], rows, d->n, K, method, alpha, tol_abs, dI[b], dC[b], dN[b], dR[b],
-                     nullptr, dP[b], dW[b], wsz, st[b]);
+    rc = stmp_encode(d, t, h.dX, rows, d->n, K, method, alpha, tol_abs, h.dI, h.dC, h.dN, h.dR,
+                     nullptr, h.dP, h.dW, h.cap_ws, h.st);
     if (rc != STMP_OK) break;
-    e = cudaMemcpyAsync(idx + s0 * K, dI[b], rows * K * sizeof(int32_t), cudaMemcpyDeviceToHost, st[b]);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(coef + s0 * K, dC[b], rows * K * sizeof(float), cudaMemcpyDeviceToHost, st[b]);
-    if (e == cudaSuccess && count) e = cudaMemcpyAsync(count + s0, dN[b], rows * sizeof(int32_t), cudaMemcpyDeviceToHost, st[b]);
-    if (e == cudaSuccess && resnorm) e = cudaMemcpyAsync(resnorm + s0, dR[b], rows * sizeof(float), cudaMemcpyDeviceToHost, st[b]);
-    if (e == cudaSuccess && ip) e = cudaMemcpyAsync(ip + 2 * s0, dP[b], rows * 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st[b]);
+    e = cudaMemcpyAsync(idx + s0 * K, h.dI, rows * K * sizeof(int32_t), cudaMemcpyDeviceToHost, h.st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(coef + s0 * K, h.dC, rows * K * sizeof(float), cudaMemcpyDeviceToHost, h.st);
+    if (e == cudaSuccess && count) e = cudaMemcpyAsync(count + s0, h.dN, rows * sizeof(int32_t), cudaMemcpyDeviceToHost, h.st);
+    if (e == cudaSuccess && resnorm) e = cudaMemcpyAsync(resnorm + s0, h.dR, rows * sizeof(float), cudaMemcpyDeviceToHost, h.st);
+    if (e == cudaSuccess && ip) e = cudaMemcpyAsync(ip + 2 * s0, h.dP, rows * 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, h.st);
     if (e != cudaSuccess) rc = cuda_fail(e, "D2H");
   }
-  for (int i = 0; i < NS; ++i) {
-    cudaError_t e = cudaStreamSynchronize(st[i]);
+  for (int i = 0; i < kHostStreams; ++i) {
+    cudaError_t e = cudaStreamSynchronize(g_host[i].st);
     if (e != cudaSuccess && rc == STMP_OK) rc = cuda_fail(e, "encode_host sync");
-    cudaFree(dX[i]); cudaFree(dI[i]); cudaFree(dC[i]); cudaFree(dN[i]); cudaFree(dR[i]); cudaFree(dP[i]); cudaFree(dW[i]);
-    cudaStreamDestroy(st[i]);
   }
   return rc;
 }

@@ -562,9 +562,17 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
 
   const int gpb = 128 / uc.G;
   const int ublocks = (int)((N + gpb - 1) / gpb);
-  // init writes the padded x into R (and into Xpad for OMP, whose update
-  // rebuilds r = x - A_S c every iteration)
-  if ((e = launch_init(uc, u, ublocks, st)) != cudaSuccess) return e;
+  // When the caller's rows are already padded (n == ld, contiguous) they serve
+  // directly as the iteration-0 residual and as the x of the OMP rebuild;
+  // otherwise init writes a padded copy into R (and Xpad for OMP).
+  const bool direct = ldx == d->ld && d->n == d->ld;
+  {
+    UpdateArgs ui = u;
+    if (direct) { ui.R = nullptr; ui.X2 = nullptr; }
+    if ((e = launch_init(uc, ui, ublocks, st)) != cudaSuccess) return e;
+  }
+  if (direct && method == kMethodOMP) u.X2 = X;
+  const float* R0 = direct ? X : R;
 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -589,7 +597,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
         scatter_kernel<<<scatter_blocks, 256, 0, st>>>(N, active, path_ws, L, l, (int)t->level_offsets[l],
                                                       offsets, cursor, perm);
       ScoreArgs s{};
-      s.R = R; s.ld = d->ld; s.perm = perm; s.items = items; s.num_items = num_items;
+      s.R = it == 0 ? R0 : R; s.ld = d->ld; s.perm = perm; s.items = items; s.num_items = num_items;
       s.table = t->staged_tables[l]; s.npad = lv.npad; s.kchunks = d->ld / 32; s.tmem_cols = lv.tmem_cols;
       s.level = l; s.level_base = (int)t->level_offsets[l]; s.child_begin = t->child_begin;
       s.child_count = t->child_count; s.path_ws = path_ws; s.path_out = path; s.count = count;
@@ -620,6 +628,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       }
       if (e != cudaSuccess) return e;
     }
+    u.R_in = it == 0 ? R0 : R;
     e = u.gram ? launch_update_omp8(u, ublocks, st) : launch_update(uc, u, ublocks, usmem, st);
     if (e != cudaSuccess) return e;
   }

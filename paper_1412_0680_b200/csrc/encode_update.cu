@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
         ss = fmaf(x.v[4 * i + k], x.v[4 * i + k], ss);
       }
     }
-    x.store(a.R + p * a.ld, gl, F);
+    if (a.R) x.store(a.R + p * a.ld, gl, F);
     if (a.X2) x.store(const_cast<float*>(a.X2) + p * a.ld2, gl, F);
   }
   ss = group_sum<G>(ss);
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
     for (int i = gl; i < K * (K + 1) / 2; i += G) L_s[i] = Lp[i];
   }
   if (act) {
-    if (!omp || lsel < 0) r.load(a.R + p * a.ld, gl, F);
+    if (!omp || lsel < 0) r.load(a.R_in + p * a.ld, gl, F);
     // leaf choice: single-atom leaves were resolved by the last score pass;
     // otherwise max |a . r| over the node's atoms, ties to the lowest atom index
     int atom = lsel;
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(128) update_omp8_kernel(UpdateArgs a) {
     Sl r;
     int atom = lsel;
     if (lsel < 0) {  // multi-atom leaf: max |a . r|, ties to the lowest atom index
-      r.load(a.R + p * a.ld, gl, F);
+      r.load(a.R_in + p * a.ld, gl, F);
       const int node = -1 - lsel;
       const int cb = __ldg(a.child_begin + node), cc = __ldg(a.child_count + node);
       float bestv = -1.f;

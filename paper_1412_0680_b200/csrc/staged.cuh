@@ -32,7 +32,8 @@ struct UpdateArgs {
   const float* X;        // caller's patches (row stride ldx, n valid columns)
   int64_t ldx;
   int n;
-  float* R;              // residual [N, ld]
+  float* R;              // residual [N, ld] (written)
+  const float* R_in;     // residual read by this pass (x itself on the first iteration)
   int ld;
   const float* X2;       // padded copy of X used by the OMP rebuild (OMP only)
   int ld2;

@@ -24,8 +24,8 @@ def load(path):
 
 def main(path, out_json, patches, method="omp", selector="tree"):
     ls = load(path)
-    half = len(ls) // 2
-    step = ls[half:]           # second encode = the timed step
+    starts = [i for i, l in enumerate(ls) if "init_kernel" in l["name"]]
+    step = ls[starts[-1]:] if starts else ls[len(ls) // 2:]   # last encode = the timed step
     t = sum(l.get("gpu__time_duration.sum", 0) for l in step)
     rd = sum(l.get("dram__bytes_read.sum", 0) for l in step)
     wr = sum(l.get("dram__bytes_write.sum", 0) for l in step)
