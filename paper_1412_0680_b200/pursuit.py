@@ -369,7 +369,7 @@ def encode(selector, X, K: int, method: str = "omp", tol: float | None = None,
 
 
 def encode_host(selector, X: np.ndarray, K: int, method: str = "omp", tol: float | None = None,
-                chunk: int = 1 << 17, out: dict | None = None) -> EncodeResult:
+                chunk: int = 1 << 18, out: dict | None = None) -> EncodeResult:
     """End-to-end encode from host memory (``stmp_encode_host``): chunked H2D,
     encode and D2H overlapped on two streams.  Pass pinned buffers (e.g. torch
     ``pin_memory()`` tensors' numpy views) for full copy bandwidth."""
