@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--score-kernel", type=int, default=2, choices=[0, 1, 2],
                     help="tcgen05 score pass: 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM")
+    ap.add_argument("--update-kernel", type=int, default=1, choices=[0, 1, 2],
+                    help="staged OMP update: 0 generic, 1 Gram-table K<=8, 2 tile + fused root scoring")
     return ap.parse_args()
 
 
@@ -222,6 +224,7 @@ def main():
     build.build()
     from paper_1412_0680_b200 import _lib
     _lib.set_option("score_kernel", args.score_kernel)
+    _lib.set_option("update_kernel", args.update_kernel)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -252,12 +255,14 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
+    lc0 = _lib.kernel_launches()
     e0.record(stream)
     for i in range(args.steps):
         ev[i][0].record(stream)
         step()
         ev[i][1].record(stream)
     e1.record(stream)
+    launches = _lib.kernel_launches() - lc0   # counted by the library at each launch site
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -306,12 +311,10 @@ def main():
     launch_ms = statistics.mean(per_launch_ms)
     staged = (not exhaustive) and N >= 16384 and cfg.n <= 256 and cfg.cid != 2
     if staged:
-        L = len(cfg.branching)
-        launches_per_step = 1 + cfg.K * (3 * L + 1)  # init + per iteration (scan, scatter, score) x L + update
-        kernel_desc = ("staged pipeline per step: init + K x (L x (scan, scatter, score_tc) + update); "
+        kernel_desc = ("staged pipeline per step: init + K x (L x (scan, scatter, score_ts) + update); "
+                       "update_kernel=2 fuses the root level of iterations >= 1 into update_tile; "
                        "achieved is over the whole step")
     else:
-        launches_per_step = 1
         kernel_desc = "encode_fused_kernel (one launch per step)"
     peaks = {}
     pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -362,7 +365,7 @@ def main():
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches,
         "clocks": clocks,
         "roofline_model_patches_per_s": rm["patches_per_s_roof"],
     }

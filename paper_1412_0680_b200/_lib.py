@@ -43,6 +43,7 @@ EXPORTS = {
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     "stmp_stream_sync": (C.c_int, [C.c_void_p]),
     "stmp_set_option": (C.c_int, [C.c_char_p, C.c_int64]),
+    "stmp_kernel_launches": (C.c_int, [C.c_void_p]),
 }
 
 PATH_AUTO, PATH_FUSED, PATH_STAGED = 0, 1, 2
@@ -50,6 +51,13 @@ PATH_AUTO, PATH_FUSED, PATH_STAGED = 0, 1, 2
 
 def set_option(key: str, value: int) -> None:
     check(load().stmp_set_option(key.encode(), int(value)))
+
+
+def kernel_launches() -> int:
+    """Cumulative number of kernels the library has launched in this process."""
+    v = C.c_int64(0)
+    check(load().stmp_kernel_launches(C.byref(v)))
+    return int(v.value)
 
 _lib = None
 

@@ -123,6 +123,12 @@ uint64_t stmp_fnv1a64(const void* data, size_t len, uint64_t h) {
   return h;
 }
 
+int stmp_kernel_launches(int64_t* out) {
+  if (out == nullptr) return fail(STMP_EINVAL, "null output");
+  *out = stmp::launch_counter().load(std::memory_order_relaxed);
+  return STMP_OK;
+}
+
 int stmp_stream_sync(void* stream) {
   STMP_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "cudaStreamSynchronize");
   return STMP_OK;
@@ -282,8 +288,10 @@ int stmp_set_option(const char* key, int64_t value) {
     return STMP_OK;
   }
   if (strcmp(key, "update_kernel") == 0) {
-    if (value < 0 || value > 1) return fail(STMP_EINVAL, "update_kernel must be 0 (generic) or 1 (K<=8 Gram-table OMP)");
-    stmp::g_update_omp8 = (int)value;
+    if (value < 0 || value > 2)
+      return fail(STMP_EINVAL, "update_kernel must be 0 (generic), 1 (K<=8 Gram-table OMP) or 2 (tile + fused root)");
+    stmp::g_update_omp8 = value >= 1 ? 1 : 0;
+    stmp::g_update_tile = value == 2 ? 1 : 0;
     return STMP_OK;
   }
   if (strcmp(key, "score_kernel") == 0) {

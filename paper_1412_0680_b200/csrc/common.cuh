@@ -4,10 +4,18 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
 namespace stmp {
+
+// process-wide count of kernel launches (stmp_kernel_launches)
+inline std::atomic<int64_t>& launch_counter() {
+  static std::atomic<int64_t> c{0};
+  return c;
+}
+inline void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr float kRidge = 1e-8f;     // pkg/src/stmp/pursuit.py:249

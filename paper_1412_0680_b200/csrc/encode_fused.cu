@@ -254,7 +254,7 @@ cudaError_t launch_vpl(const FusedArgs& a, size_t smem, int grid, cudaStream_t s
   auto k = encode_fused_kernel<VPL>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<grid, 256, smem, s>>>(a);
+  k<<<grid, 256, smem, s>>>(a); note_launch();
   return cudaGetLastError();
 }
 

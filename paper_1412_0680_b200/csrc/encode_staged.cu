@@ -25,6 +25,7 @@ namespace stmp {
 
 using namespace sm100;
 
+int g_update_tile = 0;  // 1: tile OMP update fused with the next root scoring (update_tile.cu)
 int g_update_omp8 = 1;  // 1: K <= 8 OMP update with the Gram table (encode_update.cu)
 int g_score_ws = 2;  // 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM (default)
 
@@ -373,7 +374,7 @@ cudaError_t launch_score(const ScoreArgs& s, int sms, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int per_sm = std::max(1, (int)((227 * 1024) / smem));
   const int grid = sms * std::min(per_sm, 2);
-  score_tc_kernel<KCH><<<grid, kScoreThreads, smem, st>>>(s);
+  score_tc_kernel<KCH><<<grid, kScoreThreads, smem, st>>>(s); note_launch();
   return cudaGetLastError();
 }
 
@@ -470,7 +471,7 @@ namespace {
 
 struct WsLayout {
   size_t total = 0;
-  size_t R, Xpad, tol, active, perm, path_ws, leaf_sel, Lf, yv, counts, offsets, tile_off, cursor, items,
+  size_t R, Xpad, tol, active, perm, path_ws, leaf_sel, Lf, yv, S_ws, c_ws, counts, offsets, tile_off, cursor, items,
       num_items;
 };
 
@@ -499,6 +500,8 @@ WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int 
   w.leaf_sel = add((size_t)N * 4);
   w.Lf = add((size_t)N * K * (K + 1) / 2 * 4);
   w.yv = add((size_t)N * K * 4);
+  w.S_ws = add((size_t)N * K * 4);
+  w.c_ws = add((size_t)N * K * 4);
   w.counts = add((size_t)bin_off[L] * 4);
   w.offsets = add((size_t)(maxbins + 1) * 4);
   w.tile_off = add((size_t)(maxbins + 1) * 4);
@@ -535,6 +538,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   int* leaf_sel = (int*)(b + w.leaf_sel);
   float* Lf = (float*)(b + w.Lf);
   float* yv = (float*)(b + w.yv);
+  int* S_ws = (int*)(b + w.S_ws);
+  float* c_ws = (float*)(b + w.c_ws);
   int* counts = (int*)(b + w.counts);
   int* offsets = (int*)(b + w.offsets);
   int* tile_off = (int*)(b + w.tile_off);
@@ -579,13 +584,15 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int scatter_blocks = (int)((N + 255) / 256);
   const size_t usmem = update_smem_bytes(uc, K, d->ld, u.cache_atoms != 0);
+  // tile update: OMP refit + next-iteration root scoring in one kernel
+  const bool tile = g_update_tile && u.gram != nullptr && update_tile_supported(d, t, K, method);
 
   for (int it = 0; it < K; ++it) {
-    for (int l = 0; l < L; ++l) {
+    for (int l = (tile && it > 0) ? 1 : 0; l < L; ++l) {
       const StagedLevel& lv = t->staged_levels[l];
       const int nb = (int)(t->level_offsets[l + 1] - t->level_offsets[l]);
       scan_kernel<<<1, kScanThreads, 0, st>>>(counts + bin_off[l], nb, offsets, items, num_items, tile_off,
-                                               cursor);
+                                               cursor); note_launch();
       if (l == 0)
         scatter_root_kernel<<<scatter_blocks, 256, 0, st>>>(N, active, offsets, cursor, perm);
       else if (nb <= 4096)
@@ -596,6 +603,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       else
         scatter_kernel<<<scatter_blocks, 256, 0, st>>>(N, active, path_ws, L, l, (int)t->level_offsets[l],
                                                       offsets, cursor, perm);
+      note_launch();
       ScoreArgs s{};
       s.R = it == 0 ? R0 : R; s.ld = d->ld; s.perm = perm; s.items = items; s.num_items = num_items;
       s.table = t->staged_tables[l]; s.npad = lv.npad; s.kchunks = d->ld / 32; s.tmem_cols = lv.tmem_cols;
@@ -629,7 +637,25 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       if (e != cudaSuccess) return e;
     }
     u.R_in = it == 0 ? R0 : R;
-    e = u.gram ? launch_update_omp8(u, ublocks, st) : launch_update(uc, u, ublocks, usmem, st);
+    if (tile) {
+      TileArgs ta{};
+      ta.u = u;
+      ta.S_ws = S_ws;
+      ta.c_ws = c_ws;
+      ta.root_table = t->staged_tables[0];
+      ta.root_npad = t->staged_levels[0].npad;
+      ta.root_cc = t->root_children;
+      ta.root_cb = (int)t->level_offsets[1];
+      ta.next_counts = counts + bin_off[1];
+      ta.next_base = (int)t->level_offsets[1];
+      ta.path_ws = path_ws;
+      ta.L = L;
+      ta.iter = it;
+      ta.do_root = it + 1 < K ? 1 : 0;
+      e = launch_update_tile(ta, st);
+    } else {
+      e = u.gram ? launch_update_omp8(u, ublocks, st) : launch_update(uc, u, ublocks, usmem, st);
+    }
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -440,11 +440,11 @@ cudaError_t launch_update_omp8(const UpdateArgs& a, int blocks, cudaStream_t st)
   const int F = a.ld / 4;
   const int cpl = (F + 7) / 8;
   switch (cpl) {
-    case 1: update_omp8_kernel<1><<<blocks, 128, 0, st>>>(a); break;
-    case 2: update_omp8_kernel<2><<<blocks, 128, 0, st>>>(a); break;
-    case 3: update_omp8_kernel<3><<<blocks, 128, 0, st>>>(a); break;
-    case 4: update_omp8_kernel<4><<<blocks, 128, 0, st>>>(a); break;
-    case 5: update_omp8_kernel<5><<<blocks, 128, 0, st>>>(a); break;
+    case 1: update_omp8_kernel<1><<<blocks, 128, 0, st>>>(a); note_launch(); break;
+    case 2: update_omp8_kernel<2><<<blocks, 128, 0, st>>>(a); note_launch(); break;
+    case 3: update_omp8_kernel<3><<<blocks, 128, 0, st>>>(a); note_launch(); break;
+    case 4: update_omp8_kernel<4><<<blocks, 128, 0, st>>>(a); note_launch(); break;
+    case 5: update_omp8_kernel<5><<<blocks, 128, 0, st>>>(a); note_launch(); break;
     default: return cudaErrorNotSupported;
   }
   return cudaGetLastError();
@@ -474,7 +474,7 @@ bool update_config(int ld, int K, UpdateCfg& c) {
 cudaError_t launch_init(const UpdateCfg& c, const UpdateArgs& a, int blocks, cudaStream_t st) {
   switch (c.G * 100 + c.E) {
 #define STMP_INIT_CASE(g, e) \
-  case g * 100 + e: init_kernel<g, e><<<blocks, 128, 0, st>>>(a); break;
+  case g * 100 + e: init_kernel<g, e><<<blocks, 128, 0, st>>>(a); note_launch(); break;
     STMP_UPD_CASES(STMP_INIT_CASE)
 #undef STMP_INIT_CASE
     default: return cudaErrorInvalidValue;
@@ -489,7 +489,7 @@ cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, s
     cudaError_t err = cudaFuncSetAttribute(update_kernel<g, e>,                     \
         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                    \
     if (err != cudaSuccess) return err;                                             \
-    update_kernel<g, e><<<blocks, 128, smem, st>>>(a);                              \
+    update_kernel<g, e><<<blocks, 128, smem, st>>>(a); note_launch();                              \
     break;                                                                          \
   }
     STMP_UPD_CASES(STMP_UPD_CASE)

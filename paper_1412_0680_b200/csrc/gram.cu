@@ -69,7 +69,7 @@ const float* ensure_gram(DictHandle* d, cudaStream_t st) {
     return nullptr;
   }
   const dim3 grid((unsigned)((d->m + kGT - 1) / kGT), (unsigned)((d->m + kGT - 1) / kGT));
-  gram_kernel<<<grid, 256, 0, st>>>(d->atoms, d->m, d->ld, g);
+  gram_kernel<<<grid, 256, 0, st>>>(d->atoms, d->m, d->ld, g); note_launch();
   // one-time build: finish it before any stream can read the table
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
     cudaFree(g);

@@ -267,7 +267,7 @@ cudaError_t launch_ts_kch(ScoreArgs s, int sms, cudaStream_t st) {
   const int by_smem = (int)((228 * 1024) / (smem + 1024));
   const int by_tmem = 512 / cols;
   const int per_sm = std::max(1, std::min(4, std::min(by_smem, by_tmem)));
-  score_ts_kernel<KCH><<<sms * per_sm, kThreads, smem, st>>>(s);
+  score_ts_kernel<KCH><<<sms * per_sm, kThreads, smem, st>>>(s); note_launch();
   return cudaGetLastError();
 }
 

@@ -326,7 +326,7 @@ cudaError_t launch_ws(const ScoreArgs& s, int sms, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(score_ws_kernel<KCH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  score_ws_kernel<KCH, NS><<<sms, kWsThreads, smem, st>>>(s);
+  score_ws_kernel<KCH, NS><<<sms, kWsThreads, smem, st>>>(s); note_launch();
   return cudaGetLastError();
 }
 

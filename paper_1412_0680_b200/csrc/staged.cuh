@@ -64,6 +64,26 @@ struct UpdateArgs {
   int64_t N;
 };
 
+// Tile-based OMP update + next-iteration root scoring (update_tile.cu).  Uses the
+// [entry][patch] state layout: Lf [K(K+1)/2][N], yv [K][N], S_ws [K][N], c_ws [K][N].
+struct TileArgs {
+  UpdateArgs u;
+  int* S_ws;
+  float* c_ws;
+  const float* root_table;  // staged table block of the root (bin 0, level 0)
+  int root_npad, root_cc, root_cb;
+  int* next_counts;         // level-1 bin counters
+  int next_base;
+  int* path_ws;
+  int L;
+  int iter;                 // iteration index (= support size of every active patch)
+  int do_root;              // score the root for the next iteration
+  int tmem_cols;
+};
+bool update_tile_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
+cudaError_t launch_update_tile(const TileArgs& a, cudaStream_t st);
+extern int g_update_tile;
+
 struct UpdateCfg {
   int G = 0;   // lanes per patch
   int E = 0;   // row elements per lane (G * E == ld)

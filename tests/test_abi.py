@@ -98,3 +98,17 @@ def test_argument_validation_maps_to_value_error(lib):
     rc = lib.stmp_encode(None, None, None, 0, 4, 3, 1, 1.0, -1.0, None, None, None, None, None,
                          None, None, 0, None)
     assert rc == _lib.STMP_EINVAL
+
+
+def test_options_and_launch_counter(lib):
+    before = _lib.kernel_launches()
+    assert before >= 0
+    for key, bad in (("path", 3), ("score_kernel", 3), ("update_kernel", 3)):
+        with pytest.raises(ValueError):
+            _lib.set_option(key, bad)
+    with pytest.raises(ValueError):
+        _lib.set_option("no_such_option", 0)
+    _lib.set_option("update_kernel", 1)
+    _lib.set_option("score_kernel", 2)
+    _lib.set_option("path", _lib.PATH_AUTO)
+    assert _lib.kernel_launches() == before   # option changes launch nothing

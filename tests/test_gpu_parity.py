@@ -28,20 +28,32 @@ def P():
     return pkg
 
 
-@pytest.fixture(params=["fused", "staged", "staged-ws", "staged-ts"])
+# (score_kernel, update_kernel) per staged variant; library defaults are (2, 1)
+STAGED_KERNELS = {"staged": (0, 1), "staged-ws": (1, 1), "staged-ts": (2, 1), "staged-tile": (2, 2)}
+
+
+def restore_defaults(_lib):
+    _lib.set_option("path", _lib.PATH_AUTO)
+    _lib.set_option("score_kernel", 2)
+    _lib.set_option("update_kernel", 1)
+
+
+@pytest.fixture(params=["fused", "staged", "staged-ws", "staged-ts", "staged-tile"])
 def path(request):
-    """Force one encoder implementation (the C ABI 'path' / 'score_kernel' options)."""
+    """Force one encoder implementation (the C ABI 'path' / 'score_kernel' /
+    'update_kernel' options)."""
     from paper_1412_0680_b200 import _lib
     mode = request.param
     _lib.set_option("path", _lib.PATH_FUSED if mode == "fused" else _lib.PATH_STAGED)
-    _lib.set_option("score_kernel", {"staged-ws": 1, "staged-ts": 2}.get(mode, 0))
+    sk, uk = STAGED_KERNELS.get(mode, (2, 2))
+    _lib.set_option("score_kernel", sk)
+    _lib.set_option("update_kernel", uk)
     yield mode
-    _lib.set_option("path", _lib.PATH_AUTO)
-    _lib.set_option("score_kernel", 0)
+    restore_defaults(_lib)
 
 
-@pytest.mark.parametrize("score_kernel", [0, 1, 2])
-def test_staged_is_deterministic_and_batch_invariant(score_kernel):
+@pytest.mark.parametrize("kernels", sorted(STAGED_KERNELS.values()))
+def test_staged_is_deterministic_and_batch_invariant(kernels):
     """262,144 config-1 patches: two runs and a run in 8192-patch batches must agree
     bitwise (each patch's arithmetic is independent of bucketing order)."""
     from paper_1412_0680_b200 import _lib
@@ -50,7 +62,8 @@ def test_staged_is_deterministic_and_batch_invariant(score_kernel):
     X = torch.as_tensor(W.make_patches(wl, 262144)).cuda()
     sel = P().TreeSelector(flat, wl.atoms, cfg.alpha)
     _lib.set_option("path", _lib.PATH_STAGED)
-    _lib.set_option("score_kernel", score_kernel)
+    _lib.set_option("score_kernel", kernels[0])
+    _lib.set_option("update_kernel", kernels[1])
     try:
         a = P().encode(sel, X, cfg.K, method="omp")
         b = P().encode(sel, X, cfg.K, method="omp")
@@ -62,8 +75,7 @@ def test_staged_is_deterministic_and_batch_invariant(score_kernel):
         assert int((a.idx != ci).any(1).sum()) == 0
         assert bool(torch.equal(a.coef, cc))
     finally:
-        _lib.set_option("path", _lib.PATH_AUTO)
-        _lib.set_option("score_kernel", 0)
+        restore_defaults(_lib)
 
 
 def as_np(res):

@@ -18,7 +18,8 @@ X = W.make_patches(wl, N)
 sel = P.TreeSelector(flat, wl.atoms, cfg.alpha)
 Xd = torch.as_tensor(X).cuda()
 _lib.set_option("path", 2)
-for upd in (1, 0):
+ref = None
+for upd in (2, 1, 0):
     for sk in (2, 0, 1):
         _lib.set_option("score_kernel", sk)
         _lib.set_option("update_kernel", upd)
@@ -28,4 +29,8 @@ for upd in (1, 0):
         d01 = int((runs[0] != runs[1]).any(1).sum())
         d02 = int((runs[0] != runs[2]).any(1).sum())
         ds = int((runs[0] != small).any(1).sum())
-        print(f"update={upd} score={sk}: run0 vs run1 {d01} rows, run0 vs run2 {d02}, run0 vs 8192-chunks {ds}", flush=True)
+        if ref is None:
+            ref = runs[0]
+        dr = int((runs[0] != ref).any(1).sum())
+        print(f"update={upd} score={sk}: run0 vs run1 {d01} rows, run0 vs run2 {d02}, run0 vs 8192-chunks {ds}, "
+              f"vs update=2/score=2 {dr}", flush=True)
