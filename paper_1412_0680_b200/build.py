@@ -21,6 +21,8 @@ LIB = os.path.join(OUT_DIR, "libstmp_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+# developer hook for kernel-variant sweeps (e.g. "-DSTMP_OMP8_MINB=10"); unset in normal builds
+FLAGS += os.environ.get("STMP_NVCC_DEFS", "").split()
 
 
 def _nvcc() -> str:

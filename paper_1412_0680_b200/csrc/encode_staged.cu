@@ -244,14 +244,29 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
 // ------------------------------------------------------------------ scan (one CTA)
 constexpr int kScanThreads = 1024;
 
+// `stripes` (root level only): kRootStripes partial counts of bin 0, folded
+// into counts[0] and reset here.
 __global__ void __launch_bounds__(kScanThreads) scan_kernel(int* counts, int nbins, int* offsets,
                                                              int4* items, int* num_items,
-                                                             int* tile_off, int* cursor) {
+                                                             int* tile_off, int* cursor, int* stripes) {
   using Scan = cub::BlockScan<int, kScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry[2];
-  if (threadIdx.x == 0) carry[0] = carry[1] = 0;
+  __shared__ int root_total;
+  if (threadIdx.x == 0) carry[0] = carry[1] = root_total = 0;
   __syncthreads();
+  if (stripes != nullptr) {
+    if (threadIdx.x < kRootStripes) {
+      int v = stripes[threadIdx.x];
+      stripes[threadIdx.x] = 0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      if ((threadIdx.x & 31) == 0) atomicAdd(&root_total, v);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) counts[0] += root_total;
+    __syncthreads();
+  }
   for (int b0 = 0; b0 < nbins; b0 += kScanThreads) {
     const int b = b0 + threadIdx.x;
     const int c = b < nbins ? counts[b] : 0;
@@ -502,7 +517,7 @@ WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int 
   w.yv = add((size_t)N * K * 4);
   w.S_ws = add((size_t)N * K * 4);
   w.c_ws = add((size_t)N * K * 4);
-  w.counts = add((size_t)bin_off[L] * 4);
+  w.counts = add((size_t)(bin_off[L] + kRootStripes) * 4);
   w.offsets = add((size_t)(maxbins + 1) * 4);
   w.tile_off = add((size_t)(maxbins + 1) * 4);
   w.cursor = add((size_t)(maxbins + 1) * 4);
@@ -547,7 +562,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   int4* items = (int4*)(b + w.items);
   int* num_items = (int*)(b + w.num_items);
 
-  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)bin_off[L] * 4, st);
+  int* stripes = counts + bin_off[L];
+  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)(bin_off[L] + kRootStripes) * 4, st);
   if (e != cudaSuccess) return e;
 
   UpdateCfg uc;
@@ -559,7 +575,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   u.leaf_atom = t->leaf_atom; u.L = L; u.path_ws = path_ws; u.K = K; u.method = method;
   u.tol_abs = tol_abs; u.idx = idx; u.coef = coef; u.count = count; u.resnorm = resnorm;
   u.ip = ip; u.path_out = path; u.Lf = Lf; u.yv = yv; u.tol = tol; u.active = active;
-  u.root_count = counts; u.N = N; u.leaf_sel = leaf_sel;
+  u.root_count = stripes; u.N = N; u.leaf_sel = leaf_sel;
   u.gram = (method == kMethodOMP && K <= 8 && g_update_omp8) ? ensure_gram(const_cast<DictHandle*>(d), st) : nullptr;
   u.m = d->m;
   // stage the support atoms in shared memory when the patch groups fit comfortably
@@ -592,7 +608,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       const StagedLevel& lv = t->staged_levels[l];
       const int nb = (int)(t->level_offsets[l + 1] - t->level_offsets[l]);
       scan_kernel<<<1, kScanThreads, 0, st>>>(counts + bin_off[l], nb, offsets, items, num_items, tile_off,
-                                               cursor); note_launch();
+                                               cursor, l == 0 ? stripes : nullptr); note_launch();
       if (l == 0)
         scatter_root_kernel<<<scatter_blocks, 256, 0, st>>>(N, active, offsets, cursor, perm);
       else if (nb <= 4096)

@@ -34,12 +34,14 @@ __device__ __forceinline__ float group_sum(float v) {
   return v;
 }
 
-// Count the patches that stay active into the single root bin: one
-// fire-and-forget atomic per warp (called by every lane; `act` true on at
-// most one lane per patch group).  Slots are assigned later by the scatter.
-__device__ __forceinline__ void count_root(bool act, int* counter) {
+// Count the patches that stay active into the root bin: one fire-and-forget
+// atomic per warp (called by every lane; `act` true on at most one lane per
+// patch group), spread over kRootStripes counters so the adds of a whole grid
+// do not serialise on one L2 address.  scan_kernel folds the stripes.
+__device__ __forceinline__ void count_root(bool act, int* stripes) {
   const unsigned m = __ballot_sync(kFull, act);
-  if (m && (int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(counter, __popc(m));
+  if (m && (int)(threadIdx.x & 31) == __ffs(m) - 1)
+    atomicAdd(&stripes[(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) & (kRootStripes - 1)], __popc(m));
 }
 
 // Row slice of this lane: chunks gl + G*i (i < CPL) of F 16-byte chunks.
@@ -298,8 +300,15 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
 // (and the matching y_j, c_j), every lane holds the whole Gram column, and the
 // column sums of the refit are butterfly all-reductions -- no shared memory,
 // no data-dependent loops, one global round trip for all of the patch state.
+#ifndef STMP_PF
+#define STMP_PF 0
+#endif
+constexpr bool kPrefetchSupport = STMP_PF;
+#ifndef STMP_OMP8_MINB
+#define STMP_OMP8_MINB 8
+#endif
 template <int CPL>
-__global__ void __launch_bounds__(128) update_omp8_kernel(UpdateArgs a) {
+__global__ void __launch_bounds__(128, STMP_OMP8_MINB) update_omp8_kernel(UpdateArgs a) {
   constexpr int G = 8, KM = 8;
   const int64_t p = (int64_t)blockIdx.x * (128 / G) + threadIdx.x / G;
   const int gl = threadIdx.x % G;
@@ -341,6 +350,17 @@ __global__ void __launch_bounds__(128) update_omp8_kernel(UpdateArgs a) {
         v.load(a.atoms + (int64_t)aj * a.ld, gl, F);
         const float mv = fabsf(group_sum<G>(v.dot(r)));
         if (mv > bestv || (mv == bestv && aj < atom)) { bestv = mv; atom = aj; }
+      }
+    }
+    // support rows are re-read after the refit: start their L1 fills now
+    if (kPrefetchSupport) {
+      const int nl = a.ld >> 5;   // 128-byte lines per row
+      for (int e = gl; e < t * nl; e += G) {
+        const int k = e / nl;
+        int sk = S[0];
+#pragma unroll
+        for (int kk = 1; kk < KM; ++kk) sk = kk == k ? S[kk] : sk;
+        sm100::prefetch_l1(a.atoms + (int64_t)sk * a.ld + 32 * (e - k * nl));
       }
     }
     Sl av;

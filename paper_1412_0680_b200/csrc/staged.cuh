@@ -5,6 +5,9 @@
 
 namespace stmp {
 
+// striped counters of the root bin (count_root / scan_kernel)
+constexpr int kRootStripes = 128;
+
 struct ScoreArgs {
   const float* R;        // residual rows [N, ld]
   int ld;
@@ -56,7 +59,7 @@ struct UpdateArgs {
   float* tol;
   int* active;
 
-  int* root_count;
+  int* root_count;       // kRootStripes counters of the next root bin
   const int* leaf_sel;   // written by the last score pass
   const float* gram;     // optional [m, m] atom Gram matrix (enables the 8-lane OMP kernel)
   int64_t m;
