@@ -58,6 +58,8 @@ def parse():
                     help="tcgen05 score pass: 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM")
     ap.add_argument("--update-kernel", type=int, default=1, choices=[0, 1, 2],
                     help="staged OMP update: 0 generic, 1 Gram-table K<=8, 2 tile + fused root scoring")
+    ap.add_argument("--pdl", type=int, default=1, choices=[0, 1],
+                    help="programmatic dependent launch between the staged kernels")
     return ap.parse_args()
 
 
@@ -225,6 +227,7 @@ def main():
     from paper_1412_0680_b200 import _lib
     _lib.set_option("score_kernel", args.score_kernel)
     _lib.set_option("update_kernel", args.update_kernel)
+    _lib.set_option("pdl", args.pdl)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:

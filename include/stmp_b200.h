@@ -116,7 +116,8 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
  *   "path": 0 auto (default), 1 fused warp-per-patch kernel, 2 staged tensor-core pipeline;
  *   "staged_min_batch": batch size from which `auto` picks the staged pipeline;
  *   "score_kernel": staged score pass 0 single-role, 1 warp-specialised, 2 TMEM A operand (default);
- *   "update_kernel": staged update 0 generic, 1 Gram-table K<=8 (default), 2 tile + fused root. */
+ *   "update_kernel": staged update 0 generic, 1 Gram-table K<=8 (default), 2 tile + fused root;
+ *   "pdl": 1 (default) launch the staged kernels with programmatic dependent launch, 0 plain. */
 int stmp_set_option(const char* key, int64_t value);
 
 /* Instrumentation: cumulative number of CUDA kernels this library has launched. */

@@ -287,6 +287,11 @@ int stmp_set_option(const char* key, int64_t value) {
     g_path_mode = (int)value;
     return STMP_OK;
   }
+  if (strcmp(key, "pdl") == 0) {
+    if (value < 0 || value > 1) return fail(STMP_EINVAL, "pdl must be 0 or 1");
+    stmp::g_pdl = (int)value;
+    return STMP_OK;
+  }
   if (strcmp(key, "update_kernel") == 0) {
     if (value < 0 || value > 2)
       return fail(STMP_EINVAL, "update_kernel must be 0 (generic), 1 (K<=8 Gram-table OMP) or 2 (tile + fused root)");

@@ -17,6 +17,34 @@ inline std::atomic<int64_t>& launch_counter() {
 }
 inline void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
 
+// Programmatic dependent launch between the kernels of one encode: a kernel
+// launched with `pdl` is set up while its predecessor's last CTAs drain (the
+// trigger is the implicit one at CTA exit -- an early explicit trigger let
+// successor CTAs crowd out the persistent score kernels and measured slower);
+// pdl_enter(), the first statement of every staged kernel, waits for the
+// predecessor's completion and memory flush.  Every kernel waits before it can
+// complete, so a kernel still sees everything written by all earlier kernels.
+extern int g_pdl;
+
+__device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && g_pdl) ? 1 : 0;
+  note_launch();
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr float kRidge = 1e-8f;     // pkg/src/stmp/pursuit.py:249
 constexpr float kRelTol = 1e-6f;    // pkg/src/stmp/pursuit.py:209

@@ -25,6 +25,7 @@ namespace stmp {
 
 using namespace sm100;
 
+int g_pdl = 1;          // programmatic dependent launch between staged kernels
 int g_update_tile = 0;  // 1: tile OMP update fused with the next root scoring (update_tile.cu)
 int g_update_omp8 = 1;  // 1: K <= 8 OMP update with the Gram table (encode_update.cu)
 int g_score_ws = 2;  // 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM (default)
@@ -54,6 +55,7 @@ __device__ __forceinline__ void issue_gather(const ScoreArgs& a, const int* rows
 // ------------------------------------------------------------------ score (tcgen05)
 template <int KCH>
 __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a) {
+  pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* base = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -249,6 +251,7 @@ constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads) scan_kernel(int* counts, int nbins, int* offsets,
                                                              int4* items, int* num_items,
                                                              int* tile_off, int* cursor, int* stripes) {
+  pdl_enter();
   using Scan = cub::BlockScan<int, kScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry[2];
@@ -308,6 +311,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(int* counts, int nbi
 // perm[offsets[bin] + slot] = p, slots claimed with one atomic per (warp, bin).
 __global__ void scatter_kernel(int64_t N, const int* active, const int* path_ws, int L, int level,
                                int level_base, const int* offsets, int* cursor, int* perm) {
+  pdl_enter();
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool act = p < N && active[p];
@@ -330,18 +334,29 @@ constexpr int kScatterPer = 8;
 __global__ void __launch_bounds__(kScatterThreads) scatter_hist_kernel(
     int64_t N, const int* active, const int* path_ws, int L, int level, int level_base, int nbins,
     const int* offsets, int* cursor, int* perm) {
+  pdl_enter();
   extern __shared__ int sh[];  // [nbins] local counts, then [nbins] global bases
   int* base = sh + nbins;
   for (int b = threadIdx.x; b < nbins; b += kScatterThreads) sh[b] = 0;
   __syncthreads();
   int bins[kScatterPer], local[kScatterPer];
   const int64_t p0 = (int64_t)blockIdx.x * kScatterThreads * kScatterPer + threadIdx.x;
+  const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int i = 0; i < kScatterPer; ++i) {
     const int64_t p = p0 + (int64_t)i * kScatterThreads;
     const bool act = p < N && active[p];
     bins[i] = act ? path_ws[p * L + level - 1] - level_base : -1;
-    local[i] = act ? atomicAdd(&sh[bins[i]], 1) : 0;
+  }
+  // one shared-memory atomic per (warp, bin): few bins means many equal keys
+#pragma unroll
+  for (int i = 0; i < kScatterPer; ++i) {
+    const unsigned peers = __match_any_sync(kFull, bins[i]);
+    const int leader = __ffs(peers) - 1;
+    int b = 0;
+    if (lane == leader && bins[i] >= 0) b = atomicAdd(&sh[bins[i]], __popc(peers));
+    b = __shfl_sync(kFull, b, leader);
+    local[i] = b + __popc(peers & ((1u << lane) - 1u));
   }
   __syncthreads();
   for (int b = threadIdx.x; b < nbins; b += kScatterThreads) {
@@ -361,6 +376,7 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_hist_kernel(
 // Root level: a single bin holding every active patch.  One atomic per CTA.
 __global__ void __launch_bounds__(256) scatter_root_kernel(int64_t N, const int* active, const int* offsets,
                                                            int* cursor, int* perm) {
+  pdl_enter();
   __shared__ int warp_off[8];
   __shared__ int base;
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -389,8 +405,7 @@ cudaError_t launch_score(const ScoreArgs& s, int sms, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int per_sm = std::max(1, (int)((227 * 1024) / smem));
   const int grid = sms * std::min(per_sm, 2);
-  score_tc_kernel<KCH><<<grid, kScoreThreads, smem, st>>>(s); note_launch();
-  return cudaGetLastError();
+  return launch_kernel(score_tc_kernel<KCH>, grid, kScoreThreads, smem, st, true, s);
 }
 
 }  // namespace
@@ -607,19 +622,23 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
     for (int l = (tile && it > 0) ? 1 : 0; l < L; ++l) {
       const StagedLevel& lv = t->staged_levels[l];
       const int nb = (int)(t->level_offsets[l + 1] - t->level_offsets[l]);
-      scan_kernel<<<1, kScanThreads, 0, st>>>(counts + bin_off[l], nb, offsets, items, num_items, tile_off,
-                                               cursor, l == 0 ? stripes : nullptr); note_launch();
+      e = launch_kernel(scan_kernel, 1, kScanThreads, 0, st, true, counts + bin_off[l], nb, offsets, items,
+                        num_items, tile_off, cursor, l == 0 ? stripes : nullptr);
+      if (e != cudaSuccess) return e;
       if (l == 0)
-        scatter_root_kernel<<<scatter_blocks, 256, 0, st>>>(N, active, offsets, cursor, perm);
+        e = launch_kernel(scatter_root_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
+                          (const int*)offsets, cursor, perm);
       else if (nb <= 4096)
-        scatter_hist_kernel<<<(int)((N + kScatterThreads * kScatterPer - 1) / (kScatterThreads * kScatterPer)),
-                              kScatterThreads, (size_t)nb * 8, st>>>(N, active, path_ws, L, l,
-                                                                     (int)t->level_offsets[l], nb, offsets,
-                                                                     cursor, perm);
+        e = launch_kernel(scatter_hist_kernel,
+                          (int)((N + kScatterThreads * kScatterPer - 1) / (kScatterThreads * kScatterPer)),
+                          kScatterThreads, (size_t)nb * 8, st, true, N, (const int*)active,
+                          (const int*)path_ws, L, l, (int)t->level_offsets[l], nb, (const int*)offsets, cursor,
+                          perm);
       else
-        scatter_kernel<<<scatter_blocks, 256, 0, st>>>(N, active, path_ws, L, l, (int)t->level_offsets[l],
-                                                      offsets, cursor, perm);
-      note_launch();
+        e = launch_kernel(scatter_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
+                          (const int*)path_ws, L, l, (int)t->level_offsets[l], (const int*)offsets, cursor,
+                          perm);
+      if (e != cudaSuccess) return e;
       ScoreArgs s{};
       s.R = it == 0 ? R0 : R; s.ld = d->ld; s.perm = perm; s.items = items; s.num_items = num_items;
       s.table = t->staged_tables[l]; s.npad = lv.npad; s.kchunks = d->ld / 32; s.tmem_cols = lv.tmem_cols;

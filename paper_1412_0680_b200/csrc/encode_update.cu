@@ -76,6 +76,7 @@ struct Slice {
 // ------------------------------------------------------------------ init
 template <int G, int CPL>
 __global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
+  pdl_enter();
   const int gpb = blockDim.x / G;
   const int64_t p = (int64_t)blockIdx.x * gpb + threadIdx.x / G;
   const int gl = threadIdx.x % G;
@@ -83,17 +84,23 @@ __global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
   const bool inb = p < a.N;
   Slice<G, CPL> x;
   float ss = 0.f;
+  // rows already padded and 16-byte aligned: vector loads
+  const bool vec = a.n == a.ld && (a.ldx & 3) == 0 && ((uintptr_t)a.X & 15) == 0;
   if (inb) {
     const float* xp = a.X + p * a.ldx;
+    if (vec) {
+      x.load(xp, gl, F);
+    } else {
 #pragma unroll
-    for (int i = 0; i < CPL; ++i) {
+      for (int i = 0; i < CPL; ++i)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int d = 4 * (gl + G * i) + k;
-        x.v[4 * i + k] = d < a.n ? __ldg(xp + d) : 0.f;
-        ss = fmaf(x.v[4 * i + k], x.v[4 * i + k], ss);
-      }
+        for (int k = 0; k < 4; ++k) {
+          const int d = 4 * (gl + G * i) + k;
+          x.v[4 * i + k] = d < a.n ? __ldg(xp + d) : 0.f;
+        }
     }
+#pragma unroll
+    for (int i = 0; i < CPL * 4; ++i) ss = fmaf(x.v[i], x.v[i], ss);
     if (a.R) x.store(a.R + p * a.ld, gl, F);
     if (a.X2) x.store(const_cast<float*>(a.X2) + p * a.ld2, gl, F);
   }
@@ -123,6 +130,7 @@ __host__ __device__ inline int upd_scalar_floats(int K) { return (6 * K + K * (K
 
 template <int G, int CPL>
 __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
+  pdl_enter();
   extern __shared__ __align__(16) float upd_smem[];
   const int gpb = blockDim.x / G;
   const int grp = threadIdx.x / G;
@@ -309,6 +317,7 @@ constexpr bool kPrefetchSupport = STMP_PF;
 #endif
 template <int CPL>
 __global__ void __launch_bounds__(128, STMP_OMP8_MINB) update_omp8_kernel(UpdateArgs a) {
+  pdl_enter();
   constexpr int G = 8, KM = 8;
   const int64_t p = (int64_t)blockIdx.x * (128 / G) + threadIdx.x / G;
   const int gl = threadIdx.x % G;
@@ -460,11 +469,11 @@ cudaError_t launch_update_omp8(const UpdateArgs& a, int blocks, cudaStream_t st)
   const int F = a.ld / 4;
   const int cpl = (F + 7) / 8;
   switch (cpl) {
-    case 1: update_omp8_kernel<1><<<blocks, 128, 0, st>>>(a); note_launch(); break;
-    case 2: update_omp8_kernel<2><<<blocks, 128, 0, st>>>(a); note_launch(); break;
-    case 3: update_omp8_kernel<3><<<blocks, 128, 0, st>>>(a); note_launch(); break;
-    case 4: update_omp8_kernel<4><<<blocks, 128, 0, st>>>(a); note_launch(); break;
-    case 5: update_omp8_kernel<5><<<blocks, 128, 0, st>>>(a); note_launch(); break;
+    case 1: return launch_kernel(update_omp8_kernel<1>, blocks, 128, 0, st, true, a);
+    case 2: return launch_kernel(update_omp8_kernel<2>, blocks, 128, 0, st, true, a);
+    case 3: return launch_kernel(update_omp8_kernel<3>, blocks, 128, 0, st, true, a);
+    case 4: return launch_kernel(update_omp8_kernel<4>, blocks, 128, 0, st, true, a);
+    case 5: return launch_kernel(update_omp8_kernel<5>, blocks, 128, 0, st, true, a);
     default: return cudaErrorNotSupported;
   }
   return cudaGetLastError();
@@ -494,7 +503,7 @@ bool update_config(int ld, int K, UpdateCfg& c) {
 cudaError_t launch_init(const UpdateCfg& c, const UpdateArgs& a, int blocks, cudaStream_t st) {
   switch (c.G * 100 + c.E) {
 #define STMP_INIT_CASE(g, e) \
-  case g * 100 + e: init_kernel<g, e><<<blocks, 128, 0, st>>>(a); note_launch(); break;
+  case g * 100 + e: return launch_kernel(init_kernel<g, e>, blocks, 128, 0, st, false, a);
     STMP_UPD_CASES(STMP_INIT_CASE)
 #undef STMP_INIT_CASE
     default: return cudaErrorInvalidValue;
@@ -509,8 +518,7 @@ cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, s
     cudaError_t err = cudaFuncSetAttribute(update_kernel<g, e>,                     \
         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                    \
     if (err != cudaSuccess) return err;                                             \
-    update_kernel<g, e><<<blocks, 128, smem, st>>>(a); note_launch();                              \
-    break;                                                                          \
+    return launch_kernel(update_kernel<g, e>, blocks, 128, smem, st, true, a);     \
   }
     STMP_UPD_CASES(STMP_UPD_CASE)
 #undef STMP_UPD_CASE

@@ -61,6 +61,7 @@ __device__ __forceinline__ void gather_rows(const ScoreArgs& a, const int* rows_
 
 template <int KCH>
 __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a) {
+  pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* base = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -267,8 +268,7 @@ cudaError_t launch_ts_kch(ScoreArgs s, int sms, cudaStream_t st) {
   const int by_smem = (int)((228 * 1024) / (smem + 1024));
   const int by_tmem = 512 / cols;
   const int per_sm = std::max(1, std::min(4, std::min(by_smem, by_tmem)));
-  score_ts_kernel<KCH><<<sms * per_sm, kThreads, smem, st>>>(s); note_launch();
-  return cudaGetLastError();
+  return launch_kernel(score_ts_kernel<KCH>, sms * per_sm, kThreads, smem, st, true, s);
 }
 
 }  // namespace

@@ -77,6 +77,7 @@ __host__ __device__ inline WsLayoutSmem ws_layout(int kch, int npad, bool last, 
 
 template <int KCH, int NS>
 __global__ void __launch_bounds__(kWsThreads, 1) score_ws_kernel(ScoreArgs a) {
+  pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* base = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -326,8 +327,7 @@ cudaError_t launch_ws(const ScoreArgs& s, int sms, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(score_ws_kernel<KCH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  score_ws_kernel<KCH, NS><<<sms, kWsThreads, smem, st>>>(s); note_launch();
-  return cudaGetLastError();
+  return launch_kernel(score_ws_kernel<KCH, NS>, sms, kWsThreads, (size_t)smem, st, true, s);
 }
 
 template <int KCH>

@@ -82,6 +82,7 @@ __device__ __forceinline__ void own_row(const uint8_t* buf, int row, float (&v)[
 
 template <int KCH>
 __global__ void __launch_bounds__(kTT, 2) update_tile_kernel(TileArgs a) {
+  pdl_enter();
   constexpr int LD = 32 * KCH;
   constexpr int F = 8 * KCH;
   extern __shared__ uint8_t smem_raw[];
@@ -392,8 +393,7 @@ cudaError_t launch_tile(TileArgs a, cudaStream_t st) {
                                        (int)Ly.total);
   if (e != cudaSuccess) return e;
   const int blocks = (int)((a.u.N + kTT - 1) / kTT);
-  update_tile_kernel<KCH><<<blocks, kTT, Ly.total, st>>>(a); note_launch();
-  return cudaGetLastError();
+  return launch_kernel(update_tile_kernel<KCH>, blocks, kTT, (size_t)Ly.total, st, true, a);
 }
 
 }  // namespace
