@@ -590,7 +590,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   u.leaf_atom = t->leaf_atom; u.L = L; u.path_ws = path_ws; u.K = K; u.method = method;
   u.tol_abs = tol_abs; u.idx = idx; u.coef = coef; u.count = count; u.resnorm = resnorm;
   u.ip = ip; u.path_out = path; u.Lf = Lf; u.yv = yv; u.tol = tol; u.active = active;
-  u.root_count = stripes; u.N = N; u.leaf_sel = leaf_sel;
+  u.root_count = stripes; u.N = N; u.S_ws = S_ws; u.c_ws = c_ws; u.leaf_sel = leaf_sel;
   u.gram = (method == kMethodOMP && K <= 8 && g_update_omp8) ? ensure_gram(const_cast<DictHandle*>(d), st) : nullptr;
   u.m = d->m;
   // stage the support atoms in shared memory when the patch groups fit comfortably
@@ -689,6 +689,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       ta.do_root = it + 1 < K ? 1 : 0;
       e = launch_update_tile(ta, st);
     } else {
+      u.iter = it;
       e = u.gram ? launch_update_omp8(u, ublocks, st) : launch_update(uc, u, ublocks, usmem, st);
     }
     if (e != cudaSuccess) return e;

@@ -303,47 +303,65 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
 }
 
 // ------------------------------------------------------------------ OMP update, K <= 8
-// Specialisation for the common small-K case with an atom Gram table: the 8
-// lanes of a patch group own one row each of the inverse Cholesky factor M
-// (and the matching y_j, c_j), every lane holds the whole Gram column, and the
-// column sums of the refit are butterfly all-reductions -- no shared memory,
-// no data-dependent loops, one global round trip for all of the patch state.
-#ifndef STMP_PF
-#define STMP_PF 0
-#endif
-constexpr bool kPrefetchSupport = STMP_PF;
+// Lockstep specialisation for the common small-K case with an atom Gram table.
+// In the staged pipeline every patch still active at iteration T holds exactly
+// T atoms, so T is a template parameter: every loop over the support is fully
+// unrolled with no support-size predicates.  The 8 lanes of a patch group own
+// one row each of the inverse Cholesky factor M (and the matching y_j, c_j),
+// every lane holds the Gram column, and the column sums of the refit are
+// butterfly all-reductions.  Solver state is laid out [entry][patch] (S_ws,
+// c_ws, yv, Lf), so one entry of the 4 patches of a warp is one sector; the
+// caller-visible idx / coef rows are written once, when the patch stops.
 #ifndef STMP_OMP8_MINB
 #define STMP_OMP8_MINB 8
 #endif
-template <int CPL>
-__global__ void __launch_bounds__(128, STMP_OMP8_MINB) update_omp8_kernel(UpdateArgs a) {
+#ifndef STMP_OMP8_MINB0
+#define STMP_OMP8_MINB0 12
+#endif
+#ifndef STMP_SUP_SMEM
+#define STMP_SUP_SMEM 1
+#endif
+// support rows through shared memory (cp.async) only while they are few: at
+// larger T the shared-memory footprint costs more L1 than it saves latency
+template <int T>
+constexpr bool sup_smem() { return STMP_SUP_SMEM && T >= 1 && T <= 3; }
+template <int CPL, int T>
+__global__ void __launch_bounds__(128, T == 0 ? STMP_OMP8_MINB0 : STMP_OMP8_MINB) update_omp8_kernel(UpdateArgs a) {
+  constexpr bool kSupSmem = sup_smem<T>();
   pdl_enter();
-  constexpr int G = 8, KM = 8;
+  constexpr int G = 8;
+  const int64_t N = a.N;
   const int64_t p = (int64_t)blockIdx.x * (128 / G) + threadIdx.x / G;
   const int gl = threadIdx.x % G;
   const int K = a.K;
   const int F = a.ld >> 2;
-  const int KK = K * (K + 1) / 2;
   using Sl = Slice<G, CPL>;
-  const bool inb = p < a.N;
+  const bool inb = p < N;
   const int64_t pc = inb ? p : 0;
-  // ---- every independent load of the patch, issued together
-  bool act = inb && a.active[pc];
-  const int t = a.count[pc];
-  const int lsel = a.leaf_sel[pc];
+  // ---- every independent load of the patch, issued together and before the
+  // activity test (volatile loads: the compiler may not sink them into the
+  // branch, which would add a dependent round trip)
+  const int act_in = inb ? sm100::ld_now(a.active + pc) : 0;
+  const int lsel = sm100::ld_now(a.leaf_sel + pc);
   Sl x;
-  x.load(a.X2 + pc * a.ld2, gl, F);
-  int S[KM];
 #pragma unroll
-  for (int k = 0; k < KM; ++k) S[k] = k < K ? a.idx[pc * K + k] : -1;
-  const bool own = gl < K;
-  const float cj = own ? a.coef[pc * K + gl] : 0.f;
-  const float yj = own ? a.yv[pc * K + gl] : 0.f;
-  float mrow[KM];
-  const float* Mrow = a.Lf + pc * KK + gl * (gl + 1) / 2;
+  for (int i = 0; i < CPL; ++i) {
+    const int ch = gl + G * i;
+    const float4 q = ch < F ? sm100::ld_now(reinterpret_cast<const float4*>(a.X2 + pc * a.ld2) + ch)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    x.v[4 * i] = q.x; x.v[4 * i + 1] = q.y; x.v[4 * i + 2] = q.z; x.v[4 * i + 3] = q.w;
+  }
+  int S[T + 1];
 #pragma unroll
-  for (int k = 0; k < KM; ++k) mrow[k] = (own && k <= gl) ? Mrow[k] : 0.f;
-
+  for (int k = 0; k < T; ++k) S[k] = sm100::ld_now(a.S_ws + k * N + pc);
+  const bool row_live = gl < T;
+  const float cj = row_live ? sm100::ld_now(a.c_ws + gl * N + pc) : 0.f;
+  const float yj = row_live ? sm100::ld_now(a.yv + gl * N + pc) : 0.f;
+  float mrow[T + 1];
+  const float* Mrow = a.Lf + (int64_t)(gl * (gl + 1) / 2) * N + pc;
+#pragma unroll
+  for (int k = 0; k < T; ++k) mrow[k] = (row_live && k <= gl) ? sm100::ld_now(Mrow + k * N) : 0.f;
+  bool act = act_in != 0;
   if (act) {
     Sl r;
     int atom = lsel;
@@ -361,103 +379,137 @@ __global__ void __launch_bounds__(128, STMP_OMP8_MINB) update_omp8_kernel(Update
         if (mv > bestv || (mv == bestv && aj < atom)) { bestv = mv; atom = aj; }
       }
     }
-    // support rows are re-read after the refit: start their L1 fills now
-    if (kPrefetchSupport) {
-      const int nl = a.ld >> 5;   // 128-byte lines per row
-      for (int e = gl; e < t * nl; e += G) {
-        const int k = e / nl;
-        int sk = S[0];
+    // support rows, needed after the refit: cp.async into this group's shared
+    // slice now, so their L2 round trip overlaps the new atom's
+    extern __shared__ float4 s_sup[];   // [16 groups][T][F] 16-byte chunks
+    float4* sup = s_sup + (size_t)((threadIdx.x / G) * T) * F;
+    if constexpr (kSupSmem) {
 #pragma unroll
-        for (int kk = 1; kk < KM; ++kk) sk = kk == k ? S[kk] : sk;
-        sm100::prefetch_l1(a.atoms + (int64_t)sk * a.ld + 32 * (e - k * nl));
-      }
+      for (int k = 0; k < T; ++k)
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+          const int ch = gl + G * i;
+          if (ch < F)
+            sm100::cp_async16(sm100::smem_u32(sup + k * F + ch), a.atoms + (int64_t)S[k] * a.ld + 4 * ch, 16u);
+        }
+      asm volatile("cp.async.commit_group;" ::: "memory");
     }
     Sl av;
     av.load(a.atoms + (int64_t)atom * a.ld, gl, F);
     const float* grow = a.gram + (int64_t)atom * a.m;
-    float g[KM];
+    float g[T + 1];
     bool dup = false;
 #pragma unroll
-    for (int k = 0; k < KM; ++k) {
-      const bool in = k < t;
-      g[k] = in ? __ldg(grow + S[k]) : 0.f;
-      dup |= in && S[k] == atom;
+    for (int k = 0; k < T; ++k) {
+      g[k] = __ldg(grow + S[k]);
+      dup |= S[k] == atom;
     }
     const float gtt = __ldg(grow + atom);
     const float bt = group_sum<G>(av.dot(x));
     float gmine = 0.f;   // g[gl] without dynamic indexing
 #pragma unroll
-    for (int k = 0; k < KM; ++k) gmine = k == gl ? g[k] : gmine;
-    const bool row_live = gl < t;
-    const float gc = group_sum<G>(row_live ? gmine * cj : 0.f);   // a . (A_S c_prev)
+    for (int k = 0; k < T; ++k) gmine = k == gl ? g[k] : gmine;
+    const float gc = group_sum<G>(gmine * cj);   // a . (A_S c_prev)
     const float score = bt - gc;   // a . r for r = x - A_S c_prev (pursuit.py:217 check)
-    if (dup || score == 0.f) {
-      act = false;   // re-selection (or a zero score) ends the loop
-    } else {
+    const bool ok = !dup && score != 0.f;   // re-selection or a zero score ends the loop
+    float c[T + 1];
+    bool act_next = false;
+    if (ok) {
       // w = M g (lane j: row j), then the column sums  sum_j w_j M[j][k]  and  sum_j y_j M[j][k]
       float wj = 0.f;
 #pragma unroll
-      for (int k = 0; k < KM; ++k) wj = fmaf(mrow[k], g[k], wj);
-      if (!row_live) wj = 0.f;
+      for (int k = 0; k < T; ++k) wj = fmaf(mrow[k], g[k], wj);
       const float wsum = group_sum<G>(wj * wj);
-      const float wy = group_sum<G>(row_live ? wj * yj : 0.f);
+      const float wy = group_sum<G>(wj * yj);
       const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
       const float inv_d = 1.f / dg;
       const float yy = (bt - wy) * inv_d;
-      float colw[KM], coly[KM];
+      float colw[T + 1], coly[T + 1];
 #pragma unroll
-      for (int k = 0; k < KM; ++k) {
-        colw[k] = row_live ? wj * mrow[k] : 0.f;
-        coly[k] = row_live ? yj * mrow[k] : 0.f;
+      for (int k = 0; k < T; ++k) {
+        colw[k] = wj * mrow[k];
+        coly[k] = yj * mrow[k];
       }
 #pragma unroll
       for (int o = G >> 1; o; o >>= 1) {
 #pragma unroll
-        for (int k = 0; k < KM; ++k) {
+        for (int k = 0; k < T; ++k) {
           colw[k] += __shfl_xor_sync(group_mask<G>(), colw[k], o);
           coly[k] += __shfl_xor_sync(group_mask<G>(), coly[k], o);
         }
       }
-      // new row t of M: (-(1/d) w^T M, 1/d);  c = M^T y with y_t = yy
-      float c[KM];
-      float mt_mine = 0.f, c_mine = 0.f;
+      // new row T of M: (-(1/d) w^T M, 1/d);  c = M^T y with y_T = yy
+      float mt_mine = gl == T ? inv_d : 0.f;
 #pragma unroll
-      for (int k = 0; k < KM; ++k) {
-        const float mtk = k < t ? -inv_d * colw[k] : (k == t ? inv_d : 0.f);
-        c[k] = k < t ? fmaf(mtk, yy, coly[k]) : (k == t ? inv_d * yy : 0.f);
-        if (k == gl) { mt_mine = mtk; c_mine = c[k]; }
+      for (int k = 0; k < T; ++k) {
+        const float mtk = -inv_d * colw[k];
+        c[k] = fmaf(mtk, yy, coly[k]);
+        mt_mine = k == gl ? mtk : mt_mine;
       }
-      // residual r = x - A_S c (support rows from L2) - c_t a
-      const float ct = inv_d * yy;
+      c[T] = inv_d * yy;
+      S[T] = atom;
+      // residual r = x - A_S c (support rows from L2) - c_T a
 #pragma unroll
-      for (int i = 0; i < CPL * 4; ++i) r.v[i] = fmaf(-ct, av.v[i], x.v[i]);
+      for (int i = 0; i < CPL * 4; ++i) r.v[i] = fmaf(-c[T], av.v[i], x.v[i]);
+      if constexpr (kSupSmem) asm volatile("cp.async.wait_all;" ::: "memory");   // own copies only: no barrier
 #pragma unroll
-      for (int k = 0; k < KM; ++k) {
-        if (k < t) {
-          Sl sv;
-          sv.load(a.atoms + (int64_t)S[k] * a.ld, gl, F);
+      for (int k = 0; k < T; ++k)
 #pragma unroll
-          for (int i = 0; i < CPL * 4; ++i) r.v[i] = fmaf(-c[k], sv.v[i], r.v[i]);
+        for (int i = 0; i < CPL; ++i) {
+          const int ch = gl + G * i;
+          if (ch < F) {
+            const float4 q = kSupSmem ? sup[k * F + ch]
+                                      : __ldg(reinterpret_cast<const float4*>(a.atoms + (int64_t)S[k] * a.ld) + ch);
+            r.v[4 * i] = fmaf(-c[k], q.x, r.v[4 * i]);
+            r.v[4 * i + 1] = fmaf(-c[k], q.y, r.v[4 * i + 1]);
+            r.v[4 * i + 2] = fmaf(-c[k], q.z, r.v[4 * i + 2]);
+            r.v[4 * i + 3] = fmaf(-c[k], q.w, r.v[4 * i + 3]);
+          }
         }
-      }
       r.store(a.R + p * a.ld, gl, F);
       float s2 = 0.f;
 #pragma unroll
       for (int i = 0; i < CPL * 4; ++i) s2 = fmaf(r.v[i], r.v[i], s2);
       const float rn = sqrtf(group_sum<G>(s2));
-      if (gl <= t) {
-        a.Lf[p * KK + t * (t + 1) / 2 + gl] = mt_mine;
-        a.coef[p * K + gl] = c_mine;
+      act_next = (T + 1 < K) && rn > a.tol[p];
+      if (act_next) {
+        if (gl <= T) a.Lf[(int64_t)(T * (T + 1) / 2 + gl) * N + p] = mt_mine;
+        float c_mine = c[T];
+#pragma unroll
+        for (int k = 0; k < T; ++k) c_mine = k == gl ? c[k] : c_mine;
+        if (gl <= T) a.c_ws[gl * N + p] = c_mine;
+        if (gl == 0) {
+          a.yv[T * N + p] = yy;
+          a.S_ws[T * N + p] = atom;
+        }
       }
       if (gl == 0) {
-        a.yv[p * K + t] = yy;
-        a.idx[p * K + t] = atom;
-        a.count[p] = t + 1;
+        a.count[p] = T + 1;
         a.resnorm[p] = rn;
       }
-      act = (t + 1 < K) && rn > a.tol[p];
+    } else {
+      if constexpr (kSupSmem) asm volatile("cp.async.wait_all;" ::: "memory");   // no copy may outlive the CTA's smem
+      // the patch stops on its previous support: c_prev is the lane-owned c_j
+#pragma unroll
+      for (int k = 0; k < T; ++k) c[k] = __shfl_sync(group_mask<G>(), cj, (threadIdx.x & ~(G - 1)) + k);
     }
-    if (gl == 0) a.active[p] = act ? 1 : 0;
+    if (!act_next) {
+      // final rows of the caller's idx / coef (T or T + 1 entries; the rest stay -1 / 0 from init)
+      const int n_out = ok ? T + 1 : T;
+      if (gl < n_out) {
+        int s_mine = S[0];
+        float c_mine = c[0];
+#pragma unroll
+        for (int k = 1; k <= T; ++k) {
+          s_mine = k == gl ? S[k] : s_mine;
+          c_mine = k == gl ? c[k] : c_mine;
+        }
+        a.idx[p * K + gl] = s_mine;
+        a.coef[p * K + gl] = c_mine;
+      }
+    }
+    if (gl == 0) a.active[p] = act_next ? 1 : 0;
+    act = act_next;
   }
   count_root(act && gl == 0, a.root_count);
 }
@@ -465,18 +517,27 @@ __global__ void __launch_bounds__(128, STMP_OMP8_MINB) update_omp8_kernel(Update
 }  // namespace
 
 cudaError_t launch_update_omp8(const UpdateArgs& a, int blocks, cudaStream_t st) {
-  if (a.gram == nullptr || a.K > 8 || a.method != kMethodOMP) return cudaErrorNotSupported;
-  const int F = a.ld / 4;
-  const int cpl = (F + 7) / 8;
-  switch (cpl) {
-    case 1: return launch_kernel(update_omp8_kernel<1>, blocks, 128, 0, st, true, a);
-    case 2: return launch_kernel(update_omp8_kernel<2>, blocks, 128, 0, st, true, a);
-    case 3: return launch_kernel(update_omp8_kernel<3>, blocks, 128, 0, st, true, a);
-    case 4: return launch_kernel(update_omp8_kernel<4>, blocks, 128, 0, st, true, a);
-    case 5: return launch_kernel(update_omp8_kernel<5>, blocks, 128, 0, st, true, a);
+  if (a.gram == nullptr || a.K > 8 || a.method != kMethodOMP || a.S_ws == nullptr) return cudaErrorNotSupported;
+  const int cpl = (a.ld / 4 + 7) / 8;
+  switch (cpl * 16 + a.iter) {
+#define STMP_OMP8_CASE(cp, t) \
+  case cp * 16 + t: {                                                                              \
+    const size_t smem = sup_smem<t>() ? (size_t)16 * t * (a.ld / 4) * 16 : 0;                      \
+    if (smem > 48 * 1024) {                                                                        \
+      cudaError_t err = cudaFuncSetAttribute(update_omp8_kernel<cp, t>,                            \
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (err != cudaSuccess) return err;                                                          \
+    }                                                                                              \
+    return launch_kernel(update_omp8_kernel<cp, t>, blocks, 128, smem, st, true, a);              \
+  }
+#define STMP_OMP8_ITERS(cp)                                                                        \
+  STMP_OMP8_CASE(cp, 0) STMP_OMP8_CASE(cp, 1) STMP_OMP8_CASE(cp, 2) STMP_OMP8_CASE(cp, 3)         \
+  STMP_OMP8_CASE(cp, 4) STMP_OMP8_CASE(cp, 5) STMP_OMP8_CASE(cp, 6) STMP_OMP8_CASE(cp, 7)
+    STMP_OMP8_ITERS(1) STMP_OMP8_ITERS(2) STMP_OMP8_ITERS(3) STMP_OMP8_ITERS(4) STMP_OMP8_ITERS(5)
+#undef STMP_OMP8_ITERS
+#undef STMP_OMP8_CASE
     default: return cudaErrorNotSupported;
   }
-  return cudaGetLastError();
 }
 
 bool update_config(int ld, int K, UpdateCfg& c) {

@@ -65,6 +65,10 @@ struct UpdateArgs {
   int64_t m;
   int cache_atoms;       // stage the support atoms in shared memory
   int64_t N;
+  // lockstep OMP kernels (update_omp8 / update_tile): state laid out [entry][patch]
+  int* S_ws;             // support atoms [K][N]
+  float* c_ws;           // coefficients [K][N]
+  int iter;              // iteration index = support size of every active patch
 };
 
 // Tile-based OMP update + next-iteration root scoring (update_tile.cu).  Uses the
@@ -99,7 +103,8 @@ cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, s
                           cudaStream_t st);
 size_t update_smem_bytes(const UpdateCfg& c, int K, int ld, bool cache_atoms);
 // OMP update specialised for K <= 8 with a Gram table: one lane per Cholesky row,
-// all solver state in registers.  Returns cudaErrorNotSupported when not applicable.
+// all solver state in registers, support size a.iter fixed at compile time,
+// state in the [entry][patch] layout.  Returns cudaErrorNotSupported when not applicable.
 cudaError_t launch_update_omp8(const UpdateArgs& a, int blocks, cudaStream_t st);
 // Build the [m, m] Gram matrix of the (padded) dictionary on `st`; returns nullptr if
 // m exceeds kGramMaxAtoms or memory is short.
