@@ -92,7 +92,7 @@ void stmp_tree_free(stmp_tree* t);
  *   count[N] int32 atoms selected, resnorm[N] f32 final ||r||,
  *   path[N*K*L] int32 BFS node id kept at each level (optional),
  *   ip[N*2] int32 {inner products, centroid inner products} per patch
- *   (ScoreCounter, pkg/src/stmp/dictionary.py:40-65) (optional).
+ *   (ScoreCounter, pkg/src/stmp/dictionary.py:40-65) (optional; 8-byte aligned).
  * Replaces `matching_pursuit` (pursuit.py:194-221) driven by the batch loop
  * of `_code_patches` (pkg/src/stmp/pipelines.py:180-217).
  * Workspace: stmp_encode_workspace() bytes of device memory, caller-owned.   */

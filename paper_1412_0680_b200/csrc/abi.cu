@@ -356,6 +356,8 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
   if (N == 0) return STMP_OK;
   if (X == nullptr || idx == nullptr || coef == nullptr)
     return fail(STMP_EINVAL, "X, idx and coef must be device pointers");
+  if (reinterpret_cast<uintptr_t>(ip) % 8 != 0)
+    return fail(STMP_EINVAL, "ip must be 8-byte aligned (its two counters are updated as one 64-bit word)");
   if (use_staged(d, t, N, K, method)) {
     const size_t need = stmp::staged_workspace_bytes(d, t, N, K, method);
     if (workspace == nullptr || workspace_bytes < need)

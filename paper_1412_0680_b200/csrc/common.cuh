@@ -46,6 +46,13 @@ inline cudaError_t launch_kernel(void (*k)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 constexpr unsigned kFull = 0xffffffffu;
+
+// ScoreCounter update of one patch: both int32 counters {all, centroid} in one
+// 64-bit add (the low word never carries: counts stay far below 2^32).
+__device__ __forceinline__ void add_ip(int32_t* ip, int64_t p, int all, int cent) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(ip + 2 * p),
+            ((unsigned long long)(unsigned)cent << 32) | (unsigned)all);
+}
 constexpr float kRidge = 1e-8f;     // pkg/src/stmp/pursuit.py:249
 constexpr float kRelTol = 1e-6f;    // pkg/src/stmp/pursuit.py:209
 

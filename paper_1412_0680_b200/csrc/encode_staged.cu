@@ -222,8 +222,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
       if (a.next_counts) atomicAdd(&s_hist[best], 1);
       if (last) a.leaf_sel[p] = leaf_info;
       if (a.ip) {  // ScoreCounter: cc centroids at this level (+ the leaf atoms), fire-and-forget
-        atomicAdd(&a.ip[2 * (int64_t)p], cc + leaf_cnt);
-        atomicAdd(&a.ip[2 * (int64_t)p + 1], cc);
+        add_ip(a.ip, p, cc + leaf_cnt, cc);
       }
     }
     if (a.next_counts) {
@@ -591,7 +590,10 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   u.tol_abs = tol_abs; u.idx = idx; u.coef = coef; u.count = count; u.resnorm = resnorm;
   u.ip = ip; u.path_out = path; u.Lf = Lf; u.yv = yv; u.tol = tol; u.active = active;
   u.root_count = stripes; u.N = N; u.S_ws = S_ws; u.c_ws = c_ws; u.leaf_sel = leaf_sel;
-  u.gram = (method == kMethodOMP && K <= 8 && g_update_omp8) ? ensure_gram(const_cast<DictHandle*>(d), st) : nullptr;
+  // lockstep Gram-table OMP update (update_omp8_kernel): K <= 8, rows of <= 5 chunks per lane
+  u.gram = (method == kMethodOMP && K <= 8 && d->ld <= 160 && g_update_omp8)
+               ? ensure_gram(const_cast<DictHandle*>(d), st)
+               : nullptr;
   u.m = d->m;
   // stage the support atoms in shared memory when the patch groups fit comfortably
   u.cache_atoms = update_smem_bytes(uc, K, d->ld, true) <= 96 * 1024 ? 1 : 0;

@@ -235,8 +235,7 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a) {
       if (a.next_counts) atomicAdd(&s_hist[best], 1);
       if (last) a.leaf_sel[p] = leaf_info;
       if (a.ip) {
-        atomicAdd(&a.ip[2 * (int64_t)p], cc + leaf_cnt);
-        atomicAdd(&a.ip[2 * (int64_t)p + 1], cc);
+        add_ip(a.ip, p, cc + leaf_cnt, cc);
       }
     }
     if (a.next_counts) {

@@ -297,8 +297,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) score_ws_kernel(ScoreArgs a) {
         if (a.next_counts) atomicAdd(&s_hist[best], 1);
         if (last) a.leaf_sel[p] = leaf_info;
         if (a.ip) {  // ScoreCounter: cc centroids at this level (+ the leaf atoms)
-          atomicAdd(&a.ip[2 * (int64_t)p], m.cc + leaf_cnt);
-          atomicAdd(&a.ip[2 * (int64_t)p + 1], m.cc);
+          add_ip(a.ip, p, m.cc + leaf_cnt, m.cc);
         }
       }
       // the tile's bookkeeping has been consumed: release the slot

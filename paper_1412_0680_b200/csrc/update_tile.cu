@@ -367,8 +367,7 @@ __global__ void __launch_bounds__(kTT, 2) update_tile_kernel(TileArgs a) {
       if (a.u.path_out) a.u.path_out[(p * K + (t + 1)) * a.L] = child;
       atomicAdd(&s_hist[best], 1);
       if (a.u.ip) {  // ScoreCounter: the root's children for the next selection
-        atomicAdd(&a.u.ip[2 * p], cc);
-        atomicAdd(&a.u.ip[2 * p + 1], cc);
+        add_ip(a.u.ip, p, cc, cc);
       }
     }
     __syncthreads();
