@@ -117,7 +117,8 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
  *   "staged_min_batch": batch size from which `auto` picks the staged pipeline;
  *   "score_kernel": staged score pass 0 single-role, 1 warp-specialised, 2 TMEM A operand (default);
  *   "update_kernel": staged update 0 generic, 1 Gram-table K<=8 (default), 2 tile + fused root;
- *   "pdl": 1 (default) launch the staged kernels with programmatic dependent launch, 0 plain. */
+ *   "pdl": 1 (default) launch the staged kernels with programmatic dependent launch, 0 plain;
+ *   "score_tma": 1 gather the score pass's rows with TMA tile::gather4, 0 per-thread cp.async (default). */
 int stmp_set_option(const char* key, int64_t value);
 
 /* Instrumentation: cumulative number of CUDA kernels this library has launched. */

@@ -287,6 +287,11 @@ int stmp_set_option(const char* key, int64_t value) {
     g_path_mode = (int)value;
     return STMP_OK;
   }
+  if (strcmp(key, "score_tma") == 0) {
+    if (value < 0 || value > 1) return fail(STMP_EINVAL, "score_tma must be 0 or 1");
+    stmp::g_score_tma = (int)value;
+    return STMP_OK;
+  }
   if (strcmp(key, "pdl") == 0) {
     if (value < 0 || value > 1) return fail(STMP_EINVAL, "pdl must be 0 or 1");
     stmp::g_pdl = (int)value;

@@ -642,7 +642,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
                           perm);
       if (e != cudaSuccess) return e;
       ScoreArgs s{};
-      s.R = it == 0 ? R0 : R; s.ld = d->ld; s.perm = perm; s.items = items; s.num_items = num_items;
+      s.R = it == 0 ? R0 : R; s.ld = d->ld; s.nrows = N; s.perm = perm; s.items = items; s.num_items = num_items;
       s.table = t->staged_tables[l]; s.npad = lv.npad; s.kchunks = d->ld / 32; s.tmem_cols = lv.tmem_cols;
       s.level = l; s.level_base = (int)t->level_offsets[l]; s.child_begin = t->child_begin;
       s.child_count = t->child_count; s.path_ws = path_ws; s.path_out = path; s.count = count;

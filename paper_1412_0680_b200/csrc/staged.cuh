@@ -11,6 +11,7 @@ constexpr int kRootStripes = 128;
 struct ScoreArgs {
   const float* R;        // residual rows [N, ld]
   int ld;
+  int64_t nrows;         // N (extent of R for the row tensor map)
   const int* perm;       // patch ids grouped by bin
   const int4* items;     // {bin, start in perm, rows, 0}
   const int* num_items;
@@ -120,6 +121,7 @@ __host__ __device__ inline uint32_t table_bytes(int kch, int npad, bool last) {
 }
 
 extern int g_score_ws;
+extern int g_score_tma;   // score_ts: tensor-map gathers (1) or per-thread cp.async (0)
 extern int g_update_omp8;
 bool score_ws_fits(int kchunks, int npad, bool last);
 cudaError_t launch_score_ws(const ScoreArgs& s, int sms, cudaStream_t st);
