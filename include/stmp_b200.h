@@ -115,7 +115,8 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
 /* Process-wide tuning knobs (no reference counterpart):
  *   "path": 0 auto (default), 1 fused warp-per-patch kernel, 2 staged tensor-core pipeline;
  *   "staged_min_batch": batch size from which `auto` picks the staged pipeline;
- *   "score_kernel": staged score pass 0 single-role, 1 warp-specialised, 2 TMEM A operand (default);
+ *   "score_kernel": staged score pass 0 single-role, 1 warp-specialised, 2 TMEM A operand (default),
+ *                   3 streamed table (always used for nodes whose table exceeds shared memory);
  *   "update_kernel": staged update 0 generic, 1 Gram-table K<=8 (default), 2 tile + fused root;
  *   "pdl": 1 (default) launch the staged kernels with programmatic dependent launch, 0 plain;
  *   "score_tma": 1 gather the score pass's rows with TMA tile::gather4, 0 per-thread cp.async (default). */

@@ -305,8 +305,9 @@ int stmp_set_option(const char* key, int64_t value) {
     return STMP_OK;
   }
   if (strcmp(key, "score_kernel") == 0) {
-    if (value < 0 || value > 2)
-      return fail(STMP_EINVAL, "score_kernel must be 0 (single-role), 1 (warp-specialized) or 2 (A in TMEM)");
+    if (value < 0 || value > 3)
+      return fail(STMP_EINVAL,
+                  "score_kernel must be 0 (single-role), 1 (warp-specialized), 2 (A in TMEM) or 3 (streamed table)");
     stmp::g_score_ws = (int)value;
     return STMP_OK;
   }

@@ -28,7 +28,7 @@ using namespace sm100;
 int g_pdl = 1;          // programmatic dependent launch between staged kernels
 int g_update_tile = 0;  // 1: tile OMP update fused with the next root scoring (update_tile.cu)
 int g_update_omp8 = 1;  // 1: K <= 8 OMP update with the Gram table (encode_update.cu)
-int g_score_ws = 2;  // 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM (default)
+int g_score_ws = 2;  // 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM (default), 3 streamed table
 
 namespace {
 
@@ -423,6 +423,40 @@ bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int metho
   return true;
 }
 
+// Per-node score tables on the device: for every node of one level, its
+// children's centroid rows split into tf32 hi / lo, laid out [kchunk][hi|lo]
+// [npad rows x 128 B] SW128 (the UMMA K-major B operand), then for the last
+// level npad leaf records {single leaf atom or -1 - leaf node} and npad leaf
+// atom counts (pursuit.py:155-162).  One CTA per node; the block is pre-zeroed.
+__global__ void __launch_bounds__(256) table_kernel(const float* __restrict__ cent, int ld, const int* child_begin,
+                                                    const int* child_count, const int* leaf_atom, int64_t level_base,
+                                                    int kch, int npad, int last, float* __restrict__ out) {
+  const int64_t v = level_base + blockIdx.x;
+  float* blk = out + (size_t)blockIdx.x * (table_bytes(kch, npad, last != 0) / 4);
+  const int cb = child_begin[v], cc = child_count[v];
+  const int width = 32 * kch;
+  for (int e = threadIdx.x; e < cc * width; e += blockDim.x) {
+    const int j = e / width, col = e - j * width;
+    const float val = cent[(int64_t)(cb + j) * ld + col];
+    const float hi = sm100::tf32_hi(val);
+    const int kc = col >> 5, q = col & 31;
+    const uint32_t off = sm100::sw128_offset((uint32_t)j, (uint32_t)(q >> 2)) / 4 + (q & 3);
+    float* plane = blk + (size_t)kc * 2 * npad * 32;
+    plane[off] = hi;
+    plane[(size_t)npad * 32 + off] = val - hi;
+  }
+  if (last) {
+    int32_t* info = reinterpret_cast<int32_t*>(blk + (size_t)kch * 2 * npad * 32);
+    int32_t* cnt = info + npad;
+    for (int j = threadIdx.x; j < cc; j += blockDim.x) {
+      const int child = cb + j;
+      const int lc = child_count[child];
+      info[j] = lc == 1 ? leaf_atom[child_begin[child]] : -1 - child;
+      cnt[j] = lc;
+    }
+  }
+}
+
 bool build_staged_tables(TreeHandle* t, const int32_t* child_begin, const int32_t* child_count,
                          const float* centroids, const int32_t* leaf_atom, cudaStream_t st,
                          std::string* err) {
@@ -439,45 +473,25 @@ bool build_staged_tables(TreeHandle* t, const int32_t* child_begin, const int32_
     int cols = 32;
     while (cols < levels[l].npad) cols <<= 1;
     levels[l].tmem_cols = cols;
-    if (score_smem_bytes(kch, levels[l].npad) > 227 * 1024) return false;
+    // whole-table kernels need the node table in shared memory; the streamed one does not
+    if (score_smem_bytes(kch, levels[l].npad) > 227 * 1024 && !score_st_fits(kch, levels[l].npad, l == L - 1))
+      return false;
   }
   std::vector<float*> tables(L, nullptr);
+  (void)child_begin; (void)centroids; (void)leaf_atom;
   for (int l = 0; l < L; ++l) {
     const int npad = levels[l].npad;
     const bool last = l == L - 1;
     const int64_t nodes = t->level_offsets[l + 1] - t->level_offsets[l];
-    const size_t per_node = table_bytes(kch, npad, last) / 4;  // 4-byte words
-    std::vector<float> host(per_node * nodes, 0.f);
-    for (int64_t i = 0; i < nodes; ++i) {
-      const int64_t v = t->level_offsets[l] + i;
-      const int cb = child_begin[v], cc = child_count[v];
-      float* blk = host.data() + per_node * i;
-      for (int j = 0; j < cc; ++j) {
-        const float* row = centroids + (int64_t)(cb + j) * t->n;
-        for (int col = 0; col < t->n; ++col) {
-          const float val = row[col];
-          const float hi = sm100::tf32_hi(val);
-          const float lo = val - hi;
-          const int kc = col / 32, e = col % 32;
-          const uint32_t off = sm100::sw128_offset(j, e / 4) / 4 + (e % 4);
-          float* plane = blk + (size_t)kc * 2 * npad * 32;
-          plane[off] = hi;
-          plane[npad * 32 + off] = lo;
-        }
-      }
-      if (last) {  // leaf metadata of each child (a depth-L node): pursuit.py:155-162
-        int32_t* info = reinterpret_cast<int32_t*>(blk + (size_t)kch * 2 * npad * 32);
-        int32_t* cnt = info + npad;
-        for (int j = 0; j < cc; ++j) {
-          const int child = cb + j;
-          const int lc = child_count[child];
-          info[j] = lc == 1 ? leaf_atom[child_begin[child]] : -1 - child;
-          cnt[j] = lc;
-        }
-      }
+    const size_t bytes = (size_t)table_bytes(kch, npad, last) * nodes;
+    cudaError_t e = cudaMalloc(&tables[l], bytes);
+    if (e == cudaSuccess) e = cudaMemsetAsync(tables[l], 0, bytes, st);
+    if (e == cudaSuccess) {
+      table_kernel<<<(unsigned)nodes, 256, 0, st>>>(t->cent, t->ld, t->child_begin, t->child_count, t->leaf_atom,
+                                                    t->level_offsets[l], kch, npad, last ? 1 : 0, tables[l]);
+      note_launch();
+      e = cudaGetLastError();
     }
-    cudaError_t e = cudaMalloc(&tables[l], host.size() * 4);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(tables[l], host.data(), host.size() * 4, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
       for (float* p : tables) cudaFree(p);
@@ -654,7 +668,10 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
         s.leaf_sel = leaf_sel;
       }
       s.tmem_cols = lv.tmem_cols;
-      if (g_score_ws == 2 && score_ts_fits(s.kchunks, lv.npad, l + 1 == L)) {
+      const bool whole = score_smem_bytes(s.kchunks, lv.npad) <= 227 * 1024;
+      if (g_score_ws == 3 || !whole) {
+        e = launch_score_st(s, sms, st);
+      } else if (g_score_ws == 2 && score_ts_fits(s.kchunks, lv.npad, l + 1 == L)) {
         e = launch_score_ts(s, sms, st);
       } else if (g_score_ws == 1 && score_ws_fits(s.kchunks, lv.npad, l + 1 == L)) {
         int cols = 32;

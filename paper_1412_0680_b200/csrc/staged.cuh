@@ -126,6 +126,9 @@ extern int g_update_omp8;
 bool score_ws_fits(int kchunks, int npad, bool last);
 cudaError_t launch_score_ws(const ScoreArgs& s, int sms, cudaStream_t st);
 bool score_ts_fits(int kchunks, int npad, bool last);
+// streamed-table score pass (score_st.cu): any K, npad <= 256
+bool score_st_fits(int kchunks, int npad, bool last);
+cudaError_t launch_score_st(const ScoreArgs& s, int sms, cudaStream_t st);
 cudaError_t launch_score_ts(const ScoreArgs& s, int sms, cudaStream_t st);
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
 size_t staged_workspace_bytes(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method);

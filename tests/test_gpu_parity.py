@@ -29,7 +29,8 @@ def P():
 
 
 # (score_kernel, update_kernel) per staged variant; library defaults are (2, 1)
-STAGED_KERNELS = {"staged": (0, 1), "staged-ws": (1, 1), "staged-ts": (2, 1), "staged-tile": (2, 2)}
+STAGED_KERNELS = {"staged": (0, 1), "staged-ws": (1, 1), "staged-ts": (2, 1), "staged-tile": (2, 2),
+                  "staged-st": (3, 1)}
 
 
 def restore_defaults(_lib):
@@ -38,7 +39,7 @@ def restore_defaults(_lib):
     _lib.set_option("update_kernel", 1)
 
 
-@pytest.fixture(params=["fused", "staged", "staged-ws", "staged-ts", "staged-tile"])
+@pytest.fixture(params=["fused", "staged", "staged-ws", "staged-ts", "staged-tile", "staged-st"])
 def path(request):
     """Force one encoder implementation (the C ABI 'path' / 'score_kernel' /
     'update_kernel' options)."""
