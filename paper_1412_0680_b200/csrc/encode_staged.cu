@@ -604,10 +604,10 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   u.tol_abs = tol_abs; u.idx = idx; u.coef = coef; u.count = count; u.resnorm = resnorm;
   u.ip = ip; u.path_out = path; u.Lf = Lf; u.yv = yv; u.tol = tol; u.active = active;
   u.root_count = stripes; u.N = N; u.S_ws = S_ws; u.c_ws = c_ws; u.leaf_sel = leaf_sel;
-  // lockstep Gram-table OMP update (update_omp8_kernel): K <= 8, rows of <= 5 chunks per lane
-  u.gram = (method == kMethodOMP && K <= 8 && d->ld <= 160 && g_update_omp8)
-               ? ensure_gram(const_cast<DictHandle*>(d), st)
-               : nullptr;
+  // lockstep OMP update (update_omp8_kernel): K <= 8, rows of <= 5 chunks per lane; the
+  // atom Gram table when the dictionary is small enough, dot products otherwise
+  const bool lockstep = method == kMethodOMP && K <= 8 && d->ld <= 160 && g_update_omp8;
+  u.gram = lockstep ? ensure_gram(const_cast<DictHandle*>(d), st) : nullptr;
   u.m = d->m;
   // stage the support atoms in shared memory when the patch groups fit comfortably
   u.cache_atoms = update_smem_bytes(uc, K, d->ld, true) <= 96 * 1024 ? 1 : 0;
@@ -709,7 +709,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       e = launch_update_tile(ta, st);
     } else {
       u.iter = it;
-      e = u.gram ? launch_update_omp8(u, ublocks, st) : launch_update(uc, u, ublocks, usmem, st);
+      e = lockstep ? launch_update_omp8(u, ublocks, st) : launch_update(uc, u, ublocks, usmem, st);
     }
     if (e != cudaSuccess) return e;
   }

@@ -323,11 +323,14 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
 #endif
 // support rows through shared memory (cp.async) only while they are few: at
 // larger T the shared-memory footprint costs more L1 than it saves latency
-template <int T>
-constexpr bool sup_smem() { return STMP_SUP_SMEM && T >= 1 && T <= 3; }
-template <int CPL, int T>
+template <int T, bool GRAM>
+constexpr bool sup_smem() { return STMP_SUP_SMEM && GRAM && T >= 1 && T <= 3; }
+// GRAM = false (dictionaries too large for a Gram table): the Gram column is
+// T group dot products against the support rows, which the residual rebuild
+// reads again (from L1 / L2).
+template <int CPL, int T, bool GRAM>
 __global__ void __launch_bounds__(128, T == 0 ? STMP_OMP8_MINB0 : STMP_OMP8_MINB) update_omp8_kernel(UpdateArgs a) {
-  constexpr bool kSupSmem = sup_smem<T>();
+  constexpr bool kSupSmem = sup_smem<T, GRAM>();
   pdl_enter();
   constexpr int G = 8;
   const int64_t N = a.N;
@@ -396,15 +399,27 @@ __global__ void __launch_bounds__(128, T == 0 ? STMP_OMP8_MINB0 : STMP_OMP8_MINB
     }
     Sl av;
     av.load(a.atoms + (int64_t)atom * a.ld, gl, F);
-    const float* grow = a.gram + (int64_t)atom * a.m;
     float g[T + 1];
     bool dup = false;
+    float gtt;
+    if constexpr (GRAM) {
+      const float* grow = a.gram + (int64_t)atom * a.m;
 #pragma unroll
-    for (int k = 0; k < T; ++k) {
-      g[k] = __ldg(grow + S[k]);
-      dup |= S[k] == atom;
+      for (int k = 0; k < T; ++k) {
+        g[k] = __ldg(grow + S[k]);
+        dup |= S[k] == atom;
+      }
+      gtt = __ldg(grow + atom);
+    } else {
+#pragma unroll
+      for (int k = 0; k < T; ++k) {
+        Sl sv;
+        sv.load(a.atoms + (int64_t)S[k] * a.ld, gl, F);
+        g[k] = group_sum<G>(sv.dot(av));
+        dup |= S[k] == atom;
+      }
+      gtt = group_sum<G>(av.dot(av));
     }
-    const float gtt = __ldg(grow + atom);
     const float bt = group_sum<G>(av.dot(x));
     float gmine = 0.f;   // g[gl] without dynamic indexing
 #pragma unroll
@@ -517,23 +532,25 @@ __global__ void __launch_bounds__(128, T == 0 ? STMP_OMP8_MINB0 : STMP_OMP8_MINB
 }  // namespace
 
 cudaError_t launch_update_omp8(const UpdateArgs& a, int blocks, cudaStream_t st) {
-  if (a.gram == nullptr || a.K > 8 || a.method != kMethodOMP || a.S_ws == nullptr) return cudaErrorNotSupported;
+  if (a.K > 8 || a.method != kMethodOMP || a.S_ws == nullptr) return cudaErrorNotSupported;
   const int cpl = (a.ld / 4 + 7) / 8;
-  switch (cpl * 16 + a.iter) {
-#define STMP_OMP8_CASE(cp, t) \
-  case cp * 16 + t: {                                                                              \
-    const size_t smem = sup_smem<t>() ? (size_t)16 * t * (a.ld / 4) * 16 : 0;                      \
-    if (smem > 48 * 1024) {                                                                        \
-      cudaError_t err = cudaFuncSetAttribute(update_omp8_kernel<cp, t>,                            \
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-      if (err != cudaSuccess) return err;                                                          \
-    }                                                                                              \
-    return launch_kernel(update_omp8_kernel<cp, t>, blocks, 128, smem, st, true, a);              \
+  const int gram = a.gram != nullptr ? 1 : 0;
+  switch ((cpl * 16 + a.iter) * 2 + gram) {
+#define STMP_OMP8_CASE(cp, t, gr)                                                                      \
+  case (cp * 16 + t) * 2 + gr: {                                                                     \
+    const size_t smem = sup_smem<t, gr != 0>() ? (size_t)16 * t * (a.ld / 4) * 16 : 0;              \
+    if (smem > 48 * 1024) {                                                                          \
+      cudaError_t err = cudaFuncSetAttribute(update_omp8_kernel<cp, t, gr != 0>,                     \
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+      if (err != cudaSuccess) return err;                                                            \
+    }                                                                                                \
+    return launch_kernel(update_omp8_kernel<cp, t, gr != 0>, blocks, 128, smem, st, true, a);       \
   }
-#define STMP_OMP8_ITERS(cp)                                                                        \
-  STMP_OMP8_CASE(cp, 0) STMP_OMP8_CASE(cp, 1) STMP_OMP8_CASE(cp, 2) STMP_OMP8_CASE(cp, 3)         \
-  STMP_OMP8_CASE(cp, 4) STMP_OMP8_CASE(cp, 5) STMP_OMP8_CASE(cp, 6) STMP_OMP8_CASE(cp, 7)
-    STMP_OMP8_ITERS(1) STMP_OMP8_ITERS(2) STMP_OMP8_ITERS(3) STMP_OMP8_ITERS(4) STMP_OMP8_ITERS(5)
+#define STMP_OMP8_ITERS(cp, gr)                                                                        \
+  STMP_OMP8_CASE(cp, 0, gr) STMP_OMP8_CASE(cp, 1, gr) STMP_OMP8_CASE(cp, 2, gr) STMP_OMP8_CASE(cp, 3, gr) \
+  STMP_OMP8_CASE(cp, 4, gr) STMP_OMP8_CASE(cp, 5, gr) STMP_OMP8_CASE(cp, 6, gr) STMP_OMP8_CASE(cp, 7, gr)
+    STMP_OMP8_ITERS(1, 1) STMP_OMP8_ITERS(2, 1) STMP_OMP8_ITERS(3, 1) STMP_OMP8_ITERS(4, 1) STMP_OMP8_ITERS(5, 1)
+    STMP_OMP8_ITERS(1, 0) STMP_OMP8_ITERS(2, 0) STMP_OMP8_ITERS(3, 0) STMP_OMP8_ITERS(4, 0) STMP_OMP8_ITERS(5, 0)
 #undef STMP_OMP8_ITERS
 #undef STMP_OMP8_CASE
     default: return cudaErrorNotSupported;
