@@ -25,6 +25,7 @@ namespace {
 thread_local std::string g_err;
 int g_path_mode = 0;          // 0 auto, 1 fused warp-per-patch, 2 staged tensor-core
 int64_t g_staged_min = 16384; // auto: staged path from this batch size on
+int64_t g_exact_min = 512;    // auto: tensor-core exhaustive scan from this batch size on
 
 int fail(int code, const char* fmt, ...) {
   char buf[1024];
@@ -174,6 +175,7 @@ void stmp_dict_free(stmp_dict* d) {
   if (d == nullptr) return;
   cudaFree(d->atoms);
   cudaFree(d->gram);
+  cudaFree(d->xtable);
   delete d;
 }
 
@@ -274,9 +276,10 @@ void stmp_tree_free(stmp_tree* t) {
 }
 
 static bool use_staged(const stmp_dict* d, const stmp_tree* t, int64_t N, int32_t K, int32_t method) {
-  if (g_path_mode == 1 || d == nullptr || t == nullptr) return false;
+  if (g_path_mode == 1 || d == nullptr) return false;
   if (!stmp::staged_supported(d, t, K, method)) return false;
-  return g_path_mode == 2 || N >= g_staged_min;
+  // exhaustive selection: the tensor-core scan wins as soon as one tile fills an SM
+  return g_path_mode == 2 || N >= (t == nullptr ? g_exact_min : g_staged_min);
 }
 
 int stmp_set_option(const char* key, int64_t value) {

@@ -65,6 +65,8 @@ struct DictHandle {
   uint64_t fingerprint = 0;
   float* gram = nullptr;   // optional [m, m] f32 atom Gram matrix (built lazily, small m only)
   bool gram_tried = false;
+  float* xtable = nullptr; // tf32 hi/lo atom blocks for the exhaustive scan (built lazily)
+  bool xtable_tried = false;
 };
 
 // Gram table policy: m^2 floats must stay below this (c0: 64 MB, c1: 1 GB).

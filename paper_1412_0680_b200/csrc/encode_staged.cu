@@ -415,9 +415,10 @@ size_t score_smem_bytes(int kchunks, int npad) {
 }
 
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method) {
-  if (t == nullptr || (method != kMethodMP && method != kMethodOMP)) return false;
+  if (method != kMethodMP && method != kMethodOMP) return false;
   UpdateCfg uc;
   if (!update_config(d->ld, K, uc)) return false;
+  if (t == nullptr) return d->m < (1ll << 31) && K <= 64;   // exhaustive: exact_scan.cu
   if (t->staged_tables.empty()) return false;
   if (K > 64) return false;
   return true;
@@ -520,11 +521,13 @@ struct WsLayout {
 
 WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method,
                 std::vector<int64_t>* bin_off_out, int64_t* maxbins_out) {
-  const int L = t->levels;
+  // exhaustive selection (t == nullptr): one pseudo level holding the single root bin
+  const int L = t ? t->levels : 0;
+  const int LB = t ? L : 1;
   int64_t maxbins = 1;
-  std::vector<int64_t> bin_off(L + 1, 0);
-  for (int l = 0; l < L; ++l) {
-    const int64_t b = t->level_offsets[l + 1] - t->level_offsets[l];
+  std::vector<int64_t> bin_off(LB + 1, 0);
+  for (int l = 0; l < LB; ++l) {
+    const int64_t b = t ? t->level_offsets[l + 1] - t->level_offsets[l] : 1;
     maxbins = std::max(maxbins, b);
     bin_off[l + 1] = bin_off[l] + b;
   }
@@ -545,7 +548,7 @@ WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int 
   w.yv = add((size_t)N * K * 4);
   w.S_ws = add((size_t)N * K * 4);
   w.c_ws = add((size_t)N * K * 4);
-  w.counts = add((size_t)(bin_off[L] + kRootStripes) * 4);
+  w.counts = add((size_t)(bin_off[LB] + kRootStripes) * 4);
   w.offsets = add((size_t)(maxbins + 1) * 4);
   w.tile_off = add((size_t)(maxbins + 1) * 4);
   w.cursor = add((size_t)(maxbins + 1) * 4);
@@ -570,7 +573,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   int64_t maxbins = 1;
   const WsLayout w = layout(d, t, N, K, method, &bin_off, &maxbins);
   if (ws == nullptr || ws_bytes < w.total) return cudaErrorInvalidValue;
-  const int L = t->levels;
+  const int L = t ? t->levels : 0;
+  const int LB = t ? L : 1;   // bin levels (exhaustive: the root bin only)
   uint8_t* b = static_cast<uint8_t*>(ws);
   float* R = (float*)(b + w.R);
   float* Xpad = method == kMethodOMP ? (float*)(b + w.Xpad) : nullptr;
@@ -590,8 +594,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   int4* items = (int4*)(b + w.items);
   int* num_items = (int*)(b + w.num_items);
 
-  int* stripes = counts + bin_off[L];
-  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)(bin_off[L] + kRootStripes) * 4, st);
+  int* stripes = counts + bin_off[LB];
+  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)(bin_off[LB] + kRootStripes) * 4, st);
   if (e != cudaSuccess) return e;
 
   UpdateCfg uc;
@@ -599,8 +603,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   UpdateArgs u{};
   u.X = X; u.ldx = ldx; u.n = d->n; u.R = R; u.ld = d->ld;
   u.X2 = Xpad; u.ld2 = d->ld;  // OMP rebuilds r from this padded copy of x
-  u.atoms = d->atoms; u.child_begin = t->child_begin; u.child_count = t->child_count;
-  u.leaf_atom = t->leaf_atom; u.L = L; u.path_ws = path_ws; u.K = K; u.method = method;
+  u.atoms = d->atoms; u.child_begin = t ? t->child_begin : nullptr; u.child_count = t ? t->child_count : nullptr;
+  u.leaf_atom = t ? t->leaf_atom : nullptr; u.L = L; u.path_ws = path_ws; u.K = K; u.method = method;
   u.tol_abs = tol_abs; u.idx = idx; u.coef = coef; u.count = count; u.resnorm = resnorm;
   u.ip = ip; u.path_out = path; u.Lf = Lf; u.yv = yv; u.tol = tol; u.active = active;
   u.root_count = stripes; u.N = N; u.S_ws = S_ws; u.c_ws = c_ws; u.leaf_sel = leaf_sel;
@@ -632,9 +636,26 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   const int scatter_blocks = (int)((N + 255) / 256);
   const size_t usmem = update_smem_bytes(uc, K, d->ld, u.cache_atoms != 0);
   // tile update: OMP refit + next-iteration root scoring in one kernel
-  const bool tile = g_update_tile && u.gram != nullptr && update_tile_supported(d, t, K, method);
+  const bool tile = t && g_update_tile && u.gram != nullptr && update_tile_supported(d, t, K, method);
+  const float* xtable = t ? nullptr : ensure_xtable(const_cast<DictHandle*>(d), st);
+  if (!t && xtable == nullptr) return cudaErrorMemoryAllocation;
 
   for (int it = 0; it < K; ++it) {
+    if (!t) {
+      // exhaustive selection: compact the active patches, then one tensor-core scan
+      e = launch_kernel(scan_kernel, 1, kScanThreads, 0, st, true, counts, 1, offsets, items, num_items, tile_off,
+                        cursor, stripes);
+      if (e == cudaSuccess)
+        e = launch_kernel(scatter_root_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
+                          (const int*)offsets, cursor, perm);
+      if (e != cudaSuccess) return e;
+      ScoreArgs s{};
+      s.R = it == 0 ? R0 : R; s.ld = d->ld; s.nrows = N; s.perm = perm; s.items = items; s.num_items = num_items;
+      s.table = xtable; s.npad = xtable_block_width(d->ld); s.kchunks = d->ld / 32;
+      s.nblocks = (int)((d->m + s.npad - 1) / s.npad); s.m_atoms = (int)d->m;
+      s.leaf_sel = leaf_sel; s.ip = ip; s.K = K; s.L = 0;
+      if ((e = launch_exact_scan(s, sms, st)) != cudaSuccess) return e;
+    }
     for (int l = (tile && it > 0) ? 1 : 0; l < L; ++l) {
       const StagedLevel& lv = t->staged_levels[l];
       const int nb = (int)(t->level_offsets[l + 1] - t->level_offsets[l]);

@@ -1,0 +1,317 @@
+// Exhaustive selection on the tensor cores: argmax_i |a_i . r| over the whole
+// dictionary for 128-patch tiles, i.e. a GEMM R [N, n] x A^T [n, m] whose
+// epilogue keeps only a running per-row (max |score|, lowest atom index).
+//
+// The dictionary is laid out once (lazily, per handle) as tf32 hi / lo atom
+// blocks of BW = 128 or 256 atoms: [block][kchunk][hi|lo][BW rows x 128 B]
+// SW128 -- the UMMA K-major B operand, one bulk copy per (block, chunk).  The
+// kernel has the warp-specialised shape of score_st_kernel: a producer warp
+// streams the block chunks through a ring of NB slots, an MMA warp issues the
+// 3xTF32 tcgen05.mma (M = 128 patches, N = BW atoms, A from TMEM), and four
+// stager warps gather the tile's rows chunk by chunk (re-staged for every atom
+// block: the A tile is re-read from L2 / HBM, which costs less than a third of
+// the MMA time even at n = 1600), split them into tf32 hi / lo in TMEM, and
+// after each block fold the accumulator into the running argmax.  With BW =
+// 128 two accumulators alternate, so the fold of block j overlaps the MMAs of
+// block j + 1; BW = 256 (long rows, where a block's MMAs take tens of
+// microseconds) uses one.
+// Semantics: exact_select, pkg/src/stmp/pursuit.py:102-109 (np.argmax of |A r|:
+// the first maximum, i.e. the lowest atom index; counter += m).
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "sm100.cuh"
+#include "staged.cuh"
+
+namespace stmp {
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kT = 128;
+constexpr int kStagers = 128;
+constexpr int kThreads = kStagers + 64;
+constexpr uint32_t kSlot = kT * 128u;
+constexpr uint32_t kColAcc = 128;   // TMEM: A buffers [0,64) and [64,128), accumulators from 128
+
+struct XsLayout {
+  uint32_t land, btab, bars, slot, total;
+};
+
+__host__ __device__ inline XsLayout xs_layout(int bw, int na, int nb) {
+  XsLayout L{};
+  uint32_t o = 0;
+  L.land = o; o += (uint32_t)na * kSlot;
+  L.btab = o; o += (uint32_t)nb * (uint32_t)bw * 256u;
+  L.bars = o; o = L.bars + (uint32_t)(2 * nb + 8) * 8;
+  L.slot = o; o += 16;
+  L.total = o + 1024;
+  return L;
+}
+
+template <int NA, int NB>
+__global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, int nacc) {
+  pdl_enter();
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* base = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const int bw = a.npad;           // atoms per block
+  const int kch = a.kchunks;
+  const int nblk = a.nblocks;
+  const int m = a.m_atoms;
+  const XsLayout Ly = xs_layout(bw, NA, NB);
+  const uint32_t bslot = (uint32_t)bw * 256u;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + Ly.bars);
+  uint64_t* done = full + NB;
+  uint64_t* astaged = done + NB;
+  uint64_t* aempty = astaged + 2;
+  uint64_t* accfull = aempty + 2;
+  uint64_t* accempty = accfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + Ly.slot);
+
+  if (warp == 0) tmem_alloc(tmem_slot, a.tmem_cols);
+  if (tid == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&done[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&astaged[b], kStagers);
+      mbar_init(&aempty[b], 1);
+      mbar_init(&accfull[b], 1);
+      mbar_init(&accempty[b], kStagers);
+    }
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int num_items = *a.num_items;
+  const int per = (num_items + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * per;
+  const int i1 = min(num_items, i0 + per);
+  const int per_item = nblk * kch;
+  const int total = i1 > i0 ? (i1 - i0) * per_item : 0;
+
+  if (warp == 5) {
+    // ------------------------------------------------ dictionary block producer
+    if (lane == 0) {
+      for (int g = 0; g < total; ++g) {
+        const int bc = g % per_item;   // block * kch + chunk
+        const int s = g % NB;
+        if (g >= NB) mbar_wait(&done[s], (uint32_t)(g / NB - 1) & 1u);
+        mbar_arrive_expect_tx(&full[s], bslot);
+        bulk_g2s(base + Ly.btab + s * bslot, reinterpret_cast<const uint8_t*>(a.table) + (size_t)bc * bslot, bslot,
+                 &full[s]);
+      }
+    }
+  } else if (warp == 4) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_tf32(kT, bw);
+      const uint32_t b_s = smem_u32(base + Ly.btab);
+      for (int g = 0; g < total; ++g) {
+        const int bs = g / kch, c = g - bs * kch;   // bs: block sequence number of this CTA
+        const int ab = g & 1, s = g % NB;
+        const int acc = nacc == 2 ? (bs & 1) : 0;
+        const uint32_t dcol = tmem + kColAcc + (uint32_t)acc * (uint32_t)bw;
+        if (c == 0 && bs >= nacc) mbar_wait(&accempty[acc], (uint32_t)(bs / nacc - 1) & 1u);
+        mbar_wait(&astaged[ab], (uint32_t)(g >> 1) & 1u);
+        mbar_wait(&full[s], (uint32_t)(g / NB) & 1u);
+        tc_fence_after();
+        const uint32_t bh = b_s + s * bslot;
+        const uint32_t bl = bh + (uint32_t)bw * 128u;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint32_t ah = tmem + (uint32_t)ab * 64u + ks * 8;
+          const uint32_t al = ah + 32;
+          const uint32_t o = ks * 32u;
+          mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bh + o), idesc, (c | ks) ? 1u : 0u);
+          mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bl + o), idesc, 1u);
+          mma_tf32_ts(dcol, al, sw128_kmajor_desc(bh + o), idesc, 1u);
+        }
+        mma_commit(&done[s]);
+        mma_commit(&aempty[ab]);
+        if (c == kch - 1) mma_commit(&accfull[acc]);
+      }
+    }
+  } else {
+    // ------------------------------------------------ stagers + running argmax (warps 0-3)
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t land_s = smem_u32(base + Ly.land);
+    int r_item = -1, r_row = -1;
+    auto row_of = [&](int item) {
+      if (item != r_item) {
+        r_item = item;
+        const int4 it = a.items[item];
+        r_row = tid < it.z ? a.perm[it.y + tid] : -1;
+      }
+      return r_row;
+    };
+    // chunk g (of the tile's rows) -> landing slot g % NA; lanes 8q..8q+7 copy
+    // the 128-byte chunk of one row, four whole lines per instruction
+    auto issue_a = [&](int g) {
+      if (g < total) {
+        const int c = g % kch;
+        const int rmine = row_of(i0 + g / per_item);
+        const uint32_t dst = land_s + (uint32_t)(g % NA) * kSlot;
+        const int q = lane >> 3, j = lane & 7;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rl = 4 * i + q;
+          const int r = __shfl_sync(kFull, rmine, rl);
+          const float* src = a.R + (r >= 0 ? (int64_t)r * a.ld + 32 * c + 4 * j : 0);
+          cp_async16(dst + sw128_offset((uint32_t)(warp * 32 + rl), (uint32_t)j), src, r >= 0 ? 16u : 0u);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int g = 0; g < NA; ++g) issue_a(g);
+    int cur_p = -1;
+    bool valid = false;
+    int best = 0;
+    float bestv = -1.f;
+    for (int g = 0; g < total; ++g) {
+      const int item = i0 + g / per_item, rem = g % per_item;
+      const int blk = rem / kch, c = rem - blk * kch;
+      const int bs = g / kch, ab = g & 1;
+      if (rem == 0) {
+        const int4 it = a.items[item];
+        valid = tid < it.z;
+        cur_p = valid ? a.perm[it.y + tid] : -1;
+        best = 0;
+        bestv = -1.f;
+      }
+      asm volatile("cp.async.wait_group %0;" ::"n"(NA - 1) : "memory");
+      __syncwarp();
+      float hi[32], lo[32];
+      const uint8_t* slot = base + Ly.land + (uint32_t)(g % NA) * kSlot;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 v = *reinterpret_cast<const float4*>(slot + sw128_offset(tid, j));
+        const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          hi[4 * j + q] = tf32_hi(x[q]);
+          lo[4 * j + q] = x[q] - hi[4 * j + q];
+        }
+      }
+      __syncwarp();
+      issue_a(g + NA);
+      if (g >= 2) {
+        mbar_wait(&aempty[ab], (uint32_t)((g >> 1) - 1) & 1u);
+        tc_fence_after();
+      }
+      tmem_st32(tmem + lane_base + (uint32_t)ab * 64u, hi);
+      tmem_st32(tmem + lane_base + (uint32_t)ab * 64u + 32, lo);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&astaged[ab]);
+      if (c != kch - 1) continue;
+
+      // ---- fold this block's scores into the running argmax
+      const int acc = nacc == 2 ? (bs & 1) : 0;
+      mbar_wait(&accfull[acc], (uint32_t)(bs / nacc) & 1u);
+      tc_fence_after();
+      const int a0 = blk * bw;
+      const int cnt = min(bw, m - a0);
+      for (int col0 = 0; col0 < bw; col0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + lane_base + kColAcc + (uint32_t)acc * (uint32_t)bw + (uint32_t)col0, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float mv = fabsf(v[j]);
+          if (col0 + j < cnt && mv > bestv) {
+            bestv = mv;
+            best = a0 + col0 + j;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&accempty[acc]);
+      if (blk == nblk - 1 && valid) {
+        a.leaf_sel[cur_p] = best;
+        if (a.ip) add_ip(a.ip, cur_p, m, 0);   // exact_select: counter += m (pursuit.py:106)
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tmem, a.tmem_cols);
+}
+
+// Dictionary -> [block][kchunk][hi|lo][bw rows x 128 B] SW128 (rows past m zero).
+__global__ void __launch_bounds__(256) xtable_kernel(const float* __restrict__ atoms, int64_t m, int ld, int bw,
+                                                     float* __restrict__ out) {
+  const int kch = ld / 32;
+  const int blk = blockIdx.x / kch, kc = blockIdx.x - blk * kch;
+  float* plane = out + ((size_t)blockIdx.x) * bw * 64;
+  for (int e = threadIdx.x; e < bw * 32; e += blockDim.x) {
+    const int j = e >> 5, q = e & 31;
+    const int64_t atom = (int64_t)blk * bw + j;
+    const float val = atom < m ? atoms[atom * ld + kc * 32 + q] : 0.f;
+    const float hi = tf32_hi(val);
+    const uint32_t off = sw128_offset((uint32_t)j, (uint32_t)(q >> 2)) / 4 + (q & 3);
+    plane[off] = hi;
+    plane[(size_t)bw * 32 + off] = val - hi;
+  }
+}
+
+std::mutex g_xtable_mu;
+
+template <int NA, int NB>
+cudaError_t launch_xs(ScoreArgs s, int sms, cudaStream_t st) {
+  const uint32_t smem = xs_layout(s.npad, NA, NB).total;
+  const int nacc = s.npad <= 128 ? 2 : 1;
+  int cols = 32;
+  while (cols < (int)kColAcc + nacc * s.npad) cols <<= 1;
+  s.tmem_cols = cols;
+  cudaError_t e = cudaFuncSetAttribute(exact_scan_kernel<NA, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_kernel(exact_scan_kernel<NA, NB>, sms, kThreads, (size_t)smem, st, true, s, nacc);
+}
+
+}  // namespace
+
+int xtable_block_width(int ld) { return ld / 32 <= 4 ? 128 : 256; }
+
+const float* ensure_xtable(DictHandle* d, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g_xtable_mu);
+  if (d->xtable != nullptr || d->xtable_tried) return d->xtable;
+  d->xtable_tried = true;
+  const int bw = xtable_block_width(d->ld);
+  const int64_t nblk = (d->m + bw - 1) / bw;
+  float* tab = nullptr;
+  if (cudaMalloc(&tab, (size_t)nblk * bw * d->ld * 8) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  xtable_kernel<<<(unsigned)(nblk * (d->ld / 32)), 256, 0, st>>>(d->atoms, d->m, d->ld, bw, tab);
+  note_launch();
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+    cudaFree(tab);
+    return nullptr;
+  }
+  d->xtable = tab;
+  return tab;
+}
+
+cudaError_t launch_exact_scan(const ScoreArgs& s, int sms, cudaStream_t st) {
+  // 128-atom blocks: 16 KB + 16 KB per chunk slot pair; 256-atom blocks: 64 KB slots
+  if (s.npad == 128) return launch_xs<4, 3>(s, sms, st);
+  if (s.npad == 256) return launch_xs<4, 2>(s, sms, st);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace stmp

@@ -30,6 +30,8 @@ struct ScoreArgs {
   int32_t* ip;           // optional per-patch {inner products, centroid inner products}
   int* leaf_sel;         // last level: the single leaf atom, or -1-node for multi-atom leaves
   const int* leaf_atom;
+  int nblocks;           // exhaustive scan: atom blocks of npad atoms
+  int m_atoms;           // exhaustive scan: dictionary size
 };
 
 struct UpdateArgs {
@@ -126,6 +128,11 @@ extern int g_update_omp8;
 bool score_ws_fits(int kchunks, int npad, bool last);
 cudaError_t launch_score_ws(const ScoreArgs& s, int sms, cudaStream_t st);
 bool score_ts_fits(int kchunks, int npad, bool last);
+// exhaustive selection (exact_scan.cu): dictionary blocks of xtable_block_width(ld)
+// atoms; a.table = ensure_xtable(d), a.npad = block width, a.leaf_sel = best atom
+int xtable_block_width(int ld);
+const float* ensure_xtable(DictHandle* d, cudaStream_t st);
+cudaError_t launch_exact_scan(const ScoreArgs& s, int sms, cudaStream_t st);
 // streamed-table score pass (score_st.cu): any K, npad <= 256
 bool score_st_fits(int kchunks, int npad, bool last);
 cudaError_t launch_score_st(const ScoreArgs& s, int sms, cudaStream_t st);

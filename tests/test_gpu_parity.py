@@ -303,8 +303,9 @@ def test_config0_golden_prefix():
         assert rep.ok, f"{tag}: {rep.summary()}"
 
 
-@pytest.mark.parametrize("cid,rows", [(1, 256), (4, 8)])
-def test_config_exhaustive_parity(cid, rows):
+@pytest.mark.parametrize("path", ["fused", "staged"], indirect=True)
+@pytest.mark.parametrize("cid,rows", [(1, 256), (1, 1000), (4, 8), (4, 300)])
+def test_config_exhaustive_parity(cid, rows, path):
     from paper_1412_0680_b200 import workloads as W
     cfg, wl, flat = config(cid)
     X = W.make_patches(wl, rows)
