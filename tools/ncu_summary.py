@@ -34,7 +34,9 @@ def main(path):
     d = dict(zip(h, v))
     print(f"kernel: {name}")
     print("\n".join(out))
-    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum",
+              "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+              "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"):
         i = h.index(k) if k in h else None
         if i is not None:
             print(f"  {k:<44} {v[i]:>14} {u[i]}")
