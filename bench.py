@@ -60,6 +60,10 @@ def parse():
                     help="staged OMP update: 0 generic, 1 Gram-table K<=8, 2 tile + fused root scoring")
     ap.add_argument("--pdl", type=int, default=1, choices=[0, 1],
                     help="programmatic dependent launch between the staged kernels")
+    ap.add_argument("--path", type=int, default=0, choices=[0, 1, 2],
+                    help="encoder: 0 auto, 1 fused warp-per-patch, 2 staged tensor-core pipeline")
+    ap.add_argument("--graphs", type=int, default=1, choices=[0, 1],
+                    help="replay repeated staged encodes as CUDA graphs")
     return ap.parse_args()
 
 
@@ -228,6 +232,8 @@ def main():
     _lib.set_option("score_kernel", args.score_kernel)
     _lib.set_option("update_kernel", args.update_kernel)
     _lib.set_option("pdl", args.pdl)
+    _lib.set_option("graphs", args.graphs)
+    _lib.set_option("path", args.path)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -240,10 +246,14 @@ def main():
     X_host = W.make_patches(wl, N, start=chunk_start)
     sel = P.ExactSelector(wl.atoms) if exhaustive else P.TreeSelector(flat, wl.atoms, cfg.alpha)
     Xd = torch.as_tensor(X_host).cuda()
-    stream = torch.cuda.current_stream()
+    # a dedicated stream: the library replays repeated encodes on it as CUDA graphs
+    # (the legacy default stream cannot be captured)
+    stream = torch.cuda.Stream()
+    torch.cuda.synchronize()
 
     def step():
-        return P.encode(sel, Xd, cfg.K, method=args.method)
+        with torch.cuda.stream(stream):
+            return P.encode(sel, Xd, cfg.K, method=args.method)
 
     for _ in range(args.warmup):
         step()

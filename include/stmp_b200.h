@@ -119,7 +119,8 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
  *                   3 streamed table (always used for nodes whose table exceeds shared memory);
  *   "update_kernel": staged update 0 generic, 1 Gram-table K<=8 (default), 2 tile + fused root;
  *   "pdl": 1 (default) launch the staged kernels with programmatic dependent launch, 0 plain;
- *   "score_tma": 1 gather the score pass's rows with TMA tile::gather4, 0 per-thread cp.async (default). */
+ *   "score_tma": 1 gather the score pass's rows with TMA tile::gather4, 0 per-thread cp.async (default);
+ *   "graphs": 1 (default) replay repeated staged encodes (same buffers, sizes, stream) as CUDA graphs. */
 int stmp_set_option(const char* key, int64_t value);
 
 /* Instrumentation: cumulative number of CUDA kernels this library has launched. */

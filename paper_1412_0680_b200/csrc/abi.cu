@@ -26,6 +26,27 @@ thread_local std::string g_err;
 int g_path_mode = 0;          // 0 auto, 1 fused warp-per-patch, 2 staged tensor-core
 int64_t g_staged_min = 16384; // auto: staged path from this batch size on
 int64_t g_exact_min = 512;    // auto: tensor-core exhaustive scan from this batch size on
+int g_graphs = 1;             // replay repeated staged encodes as CUDA graphs
+
+// CUDA-graph cache of staged encodes.  A call whose every argument (handles,
+// buffers, sizes, stream) and kernel option matches a previous one is replayed
+// from an instantiated graph: the second occurrence is captured, later ones
+// only launch.  Removes the ~60 host launches per encode from the critical path
+// of small batches and of the chunked host-buffer path.
+struct GraphKey {
+  const void* p[14];
+  int64_t v[12];
+};
+struct GraphEntry {
+  GraphKey key;
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;
+  bool seen = false;
+  uint64_t stamp = 0;
+};
+std::mutex g_graph_mu;
+GraphEntry g_graph_cache[8];
+uint64_t g_graph_clock = 0;
 
 int fail(int code, const char* fmt, ...) {
   char buf[1024];
@@ -295,6 +316,11 @@ int stmp_set_option(const char* key, int64_t value) {
     stmp::g_score_tma = (int)value;
     return STMP_OK;
   }
+  if (strcmp(key, "graphs") == 0) {
+    if (value < 0 || value > 1) return fail(STMP_EINVAL, "graphs must be 0 or 1");
+    g_graphs = (int)value;
+    return STMP_OK;
+  }
   if (strcmp(key, "pdl") == 0) {
     if (value < 0 || value > 1) return fail(STMP_EINVAL, "pdl must be 0 or 1");
     stmp::g_pdl = (int)value;
@@ -372,9 +398,74 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
     if (workspace == nullptr || workspace_bytes < need)
       return fail(STMP_EINVAL, "workspace of %zu bytes is below the required %zu (stmp_encode_workspace)",
                   workspace_bytes, need);
-    cudaError_t e = stmp::run_staged(d, t, X, N, ldx, K, method, tol_abs < 0 ? -1.f : (float)tol_abs, idx,
-                                     coef, count, resnorm, path, ip, workspace, workspace_bytes,
-                                     static_cast<cudaStream_t>(stream));
+    const float tol = tol_abs < 0 ? -1.f : (float)tol_abs;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto run = [&] {
+      return stmp::run_staged(d, t, X, N, ldx, K, method, tol, idx, coef, count, resnorm, path, ip, workspace,
+                              workspace_bytes, st);
+    };
+    // the legacy default stream cannot be captured
+    if (!g_graphs || st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread) {
+      cudaError_t e = run();
+      if (e != cudaSuccess) return cuda_fail(e, "staged encode");
+      return STMP_OK;
+    }
+    GraphKey k;
+    memset(&k, 0, sizeof(k));
+    const void* ps[14] = {d, t, X, idx, coef, count, resnorm, path, ip, workspace, stream, nullptr, nullptr, nullptr};
+    for (int i = 0; i < 14; ++i) k.p[i] = ps[i];
+    const int64_t vs[12] = {N, ldx, K, method, (int64_t)workspace_bytes, (int64_t)(tol * 1e9f), stmp::g_score_ws,
+                            stmp::g_update_omp8, stmp::g_update_tile, stmp::g_pdl, stmp::g_score_tma, 0};
+    memcpy(k.v, vs, sizeof(vs));
+    memcpy(&k.v[11], &tol, sizeof(float));
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    GraphEntry* hit = nullptr;
+    GraphEntry* lru = &g_graph_cache[0];
+    for (GraphEntry& ge : g_graph_cache) {
+      if (ge.seen && memcmp(&ge.key, &k, sizeof(k)) == 0) hit = &ge;
+      if (ge.stamp < lru->stamp) lru = &ge;
+    }
+    if (hit && hit->exec) {
+      hit->stamp = ++g_graph_clock;
+      stmp::launch_counter().fetch_add(hit->launches, std::memory_order_relaxed);
+      cudaError_t e = cudaGraphLaunch(hit->exec, st);
+      if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+      return STMP_OK;
+    }
+    if (hit) {   // second occurrence: capture, instantiate, launch
+      const int64_t before = stmp::launch_counter().load();
+      cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+      cudaGraph_t g = nullptr;
+      if (e == cudaSuccess) {
+        cudaError_t er = run();
+        e = cudaStreamEndCapture(st, &g);
+        if (e == cudaSuccess) e = er;
+      }
+      cudaGraphExec_t exec = nullptr;
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, g, 0);
+      if (g) cudaGraphDestroy(g);
+      if (e == cudaSuccess) {
+        hit->exec = exec;
+        hit->launches = stmp::launch_counter().load() - before;
+        hit->stamp = ++g_graph_clock;
+        e = cudaGraphLaunch(exec, st);
+        if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+        return STMP_OK;
+      }
+      // capture unsupported here: forget the entry and run eagerly
+      cudaGetLastError();
+      stmp::launch_counter().store(before);
+      hit->seen = false;
+      e = run();
+      if (e != cudaSuccess) return cuda_fail(e, "staged encode");
+      return STMP_OK;
+    }
+    if (lru->exec) cudaGraphExecDestroy(lru->exec);
+    lru->exec = nullptr;
+    lru->key = k;
+    lru->seen = true;
+    lru->stamp = ++g_graph_clock;
+    cudaError_t e = run();
     if (e != cudaSuccess) return cuda_fail(e, "staged encode");
     return STMP_OK;
   }

@@ -326,10 +326,11 @@ __global__ void scatter_kernel(int64_t N, const int* active, const int* path_ws,
 }
 
 // Levels with few bins: block-local histogram in shared memory, one global
-// atomic per (block, bin); each block covers kScatterPer patches.
+// atomic per (block, bin); each block covers kScatterThreads * PER patches (PER
+// shrinks with the batch so small batches still spread over the SMs).
 constexpr int kScatterThreads = 512;
-constexpr int kScatterPer = 8;
 
+template <int kScatterPer>
 __global__ void __launch_bounds__(kScatterThreads) scatter_hist_kernel(
     int64_t N, const int* active, const int* path_ws, int L, int level, int level_base, int nbins,
     const int* offsets, int* cursor, int* perm) {
@@ -665,12 +666,13 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       if (l == 0)
         e = launch_kernel(scatter_root_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
                           (const int*)offsets, cursor, perm);
-      else if (nb <= 4096)
-        e = launch_kernel(scatter_hist_kernel,
-                          (int)((N + kScatterThreads * kScatterPer - 1) / (kScatterThreads * kScatterPer)),
-                          kScatterThreads, (size_t)nb * 8, st, true, N, (const int*)active,
-                          (const int*)path_ws, L, l, (int)t->level_offsets[l], nb, (const int*)offsets, cursor,
-                          perm);
+      else if (nb <= 4096) {
+        const int per = N >= (int64_t)sms * kScatterThreads * 8 ? 8 : N >= (int64_t)sms * kScatterThreads * 2 ? 2 : 1;
+        const int grid = (int)((N + kScatterThreads * per - 1) / (kScatterThreads * per));
+        auto k = per == 8 ? scatter_hist_kernel<8> : per == 2 ? scatter_hist_kernel<2> : scatter_hist_kernel<1>;
+        e = launch_kernel(k, grid, kScatterThreads, (size_t)nb * 8, st, true, N, (const int*)active,
+                          (const int*)path_ws, L, l, (int)t->level_offsets[l], nb, (const int*)offsets, cursor, perm);
+      }
       else
         e = launch_kernel(scatter_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
                           (const int*)path_ws, L, l, (int)t->level_offsets[l], (const int*)offsets, cursor,
