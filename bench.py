@@ -322,11 +322,11 @@ def main():
 
     value = world * N * args.steps / (total_ms / 1e3)
     launch_ms = statistics.mean(per_launch_ms)
-    staged = (not exhaustive) and N >= 16384 and cfg.n <= 256 and cfg.cid != 2
-    if staged:
-        kernel_desc = ("staged pipeline per step: init + K x (L x (scan, scatter, score_ts) + update); "
-                       "update_kernel=2 fuses the root level of iterations >= 1 into update_tile; "
-                       "achieved is over the whole step")
+    per_step = launches / max(1, args.steps)
+    if per_step > 1:
+        score = "exact_scan (tensor-core GEMM + argmax)" if exhaustive else "score_ts / score_st (tcgen05 3xTF32)"
+        kernel_desc = (f"staged pipeline, {per_step:.0f} launches per step: init + K x (levels x (scan, scatter, "
+                       f"{score}) + update); achieved is over the whole step")
     else:
         kernel_desc = "encode_fused_kernel (one launch per step)"
     peaks = {}
