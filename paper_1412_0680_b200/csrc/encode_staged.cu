@@ -27,7 +27,7 @@ using namespace sm100;
 
 int g_pdl = 1;          // programmatic dependent launch between staged kernels
 int g_update_tile = 0;  // 1: tile OMP update fused with the next root scoring (update_tile.cu)
-int g_update_omp8 = 1;  // 1: K <= 8 OMP update with the Gram table (encode_update.cu)
+int g_update_omp8 = 1;  // 1: lockstep OMP update (update_omp8_kernel, encode_update.cu)
 int g_score_ws = 2;  // 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM (default), 3 streamed table
 
 namespace {
@@ -609,9 +609,9 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   u.tol_abs = tol_abs; u.idx = idx; u.coef = coef; u.count = count; u.resnorm = resnorm;
   u.ip = ip; u.path_out = path; u.Lf = Lf; u.yv = yv; u.tol = tol; u.active = active;
   u.root_count = stripes; u.N = N; u.S_ws = S_ws; u.c_ws = c_ws; u.leaf_sel = leaf_sel;
-  // lockstep OMP update (update_omp8_kernel): K <= 8, rows of <= 5 chunks per lane; the
+  // lockstep OMP update (update_omp8_kernel): K <= 8 with rows of <= 160 floats or K <= 16 with <= 128; the
   // atom Gram table when the dictionary is small enough, dot products otherwise
-  const bool lockstep = method == kMethodOMP && K <= 8 && d->ld <= 160 && g_update_omp8;
+  const bool lockstep = method == kMethodOMP && lockstep_lanes(d->ld, K) != 0 && g_update_omp8;
   u.gram = lockstep ? ensure_gram(const_cast<DictHandle*>(d), st) : nullptr;
   u.m = d->m;
   // stage the support atoms in shared memory when the patch groups fit comfortably
@@ -732,7 +732,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       e = launch_update_tile(ta, st);
     } else {
       u.iter = it;
-      e = lockstep ? launch_update_omp8(u, ublocks, st) : launch_update(uc, u, ublocks, usmem, st);
+      e = lockstep ? launch_update_omp8(u, st) : launch_update(uc, u, ublocks, usmem, st);
     }
     if (e != cudaSuccess) return e;
   }

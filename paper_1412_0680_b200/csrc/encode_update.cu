@@ -328,11 +328,12 @@ constexpr bool sup_smem() { return STMP_SUP_SMEM && GRAM && T >= 1 && T <= 3; }
 // GRAM = false (dictionaries too large for a Gram table): the Gram column is
 // T group dot products against the support rows, which the residual rebuild
 // reads again (from L1 / L2).
-template <int CPL, int T, bool GRAM>
-__global__ void __launch_bounds__(128, T == 0 ? STMP_OMP8_MINB0 : STMP_OMP8_MINB) update_omp8_kernel(UpdateArgs a) {
+// G = 16 lanes per patch (rows of <= 128 floats) lifts the support limit to 16.
+template <int G, int CPL, int T, bool GRAM>
+__global__ void __launch_bounds__(128, G == 8 ? (T == 0 ? STMP_OMP8_MINB0 : STMP_OMP8_MINB) : 6)
+    update_omp8_kernel(UpdateArgs a) {
   constexpr bool kSupSmem = sup_smem<T, GRAM>();
   pdl_enter();
-  constexpr int G = 8;
   const int64_t N = a.N;
   const int64_t p = (int64_t)blockIdx.x * (128 / G) + threadIdx.x / G;
   const int gl = threadIdx.x % G;
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(128, T == 0 ? STMP_OMP8_MINB0 : STMP_OMP8_MINB
     }
     // support rows, needed after the refit: cp.async into this group's shared
     // slice now, so their L2 round trip overlaps the new atom's
-    extern __shared__ float4 s_sup[];   // [16 groups][T][F] 16-byte chunks
+    extern __shared__ float4 s_sup[];   // [128 / G groups][T][F] 16-byte chunks
     float4* sup = s_sup + (size_t)((threadIdx.x / G) * T) * F;
     if constexpr (kSupSmem) {
 #pragma unroll
@@ -531,26 +532,42 @@ __global__ void __launch_bounds__(128, T == 0 ? STMP_OMP8_MINB0 : STMP_OMP8_MINB
 
 }  // namespace
 
-cudaError_t launch_update_omp8(const UpdateArgs& a, int blocks, cudaStream_t st) {
-  if (a.K > 8 || a.method != kMethodOMP || a.S_ws == nullptr) return cudaErrorNotSupported;
-  const int cpl = (a.ld / 4 + 7) / 8;
+int lockstep_lanes(int ld, int K) {
+  if (K <= 8 && ld <= 160) return 8;
+  if (K <= 16 && ld <= 128) return 16;
+  return 0;
+}
+
+cudaError_t launch_update_omp8(const UpdateArgs& a, cudaStream_t st) {
+  const int G = lockstep_lanes(a.ld, a.K);
+  if (G == 0 || a.method != kMethodOMP || a.S_ws == nullptr) return cudaErrorNotSupported;
+  const int blocks = (int)((a.N + (128 / G) - 1) / (128 / G));
+  const int cpl = (a.ld / 4 + G - 1) / G;
   const int gram = a.gram != nullptr ? 1 : 0;
-  switch ((cpl * 16 + a.iter) * 2 + gram) {
-#define STMP_OMP8_CASE(cp, t, gr)                                                                      \
-  case (cp * 16 + t) * 2 + gr: {                                                                     \
-    const size_t smem = sup_smem<t, gr != 0>() ? (size_t)16 * t * (a.ld / 4) * 16 : 0;              \
+  switch (((G * 8 + cpl) * 16 + a.iter) * 2 + gram) {
+#define STMP_OMP8_CASE(g, cp, t, gr)                                                                   \
+  case ((g * 8 + cp) * 16 + t) * 2 + gr: {                                                           \
+    const size_t smem = sup_smem<t, gr != 0>() ? (size_t)(128 / g) * t * (a.ld / 4) * 16 : 0;       \
     if (smem > 48 * 1024) {                                                                          \
-      cudaError_t err = cudaFuncSetAttribute(update_omp8_kernel<cp, t, gr != 0>,                     \
+      cudaError_t err = cudaFuncSetAttribute(update_omp8_kernel<g, cp, t, gr != 0>,                  \
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
       if (err != cudaSuccess) return err;                                                            \
     }                                                                                                \
-    return launch_kernel(update_omp8_kernel<cp, t, gr != 0>, blocks, 128, smem, st, true, a);       \
+    return launch_kernel(update_omp8_kernel<g, cp, t, gr != 0>, blocks, 128, smem, st, true, a);    \
   }
-#define STMP_OMP8_ITERS(cp, gr)                                                                        \
-  STMP_OMP8_CASE(cp, 0, gr) STMP_OMP8_CASE(cp, 1, gr) STMP_OMP8_CASE(cp, 2, gr) STMP_OMP8_CASE(cp, 3, gr) \
-  STMP_OMP8_CASE(cp, 4, gr) STMP_OMP8_CASE(cp, 5, gr) STMP_OMP8_CASE(cp, 6, gr) STMP_OMP8_CASE(cp, 7, gr)
-    STMP_OMP8_ITERS(1, 1) STMP_OMP8_ITERS(2, 1) STMP_OMP8_ITERS(3, 1) STMP_OMP8_ITERS(4, 1) STMP_OMP8_ITERS(5, 1)
-    STMP_OMP8_ITERS(1, 0) STMP_OMP8_ITERS(2, 0) STMP_OMP8_ITERS(3, 0) STMP_OMP8_ITERS(4, 0) STMP_OMP8_ITERS(5, 0)
+#define STMP_OMP8_ITERS(g, cp, gr)                                                                      \
+  STMP_OMP8_CASE(g, cp, 0, gr) STMP_OMP8_CASE(g, cp, 1, gr) STMP_OMP8_CASE(g, cp, 2, gr)               \
+  STMP_OMP8_CASE(g, cp, 3, gr) STMP_OMP8_CASE(g, cp, 4, gr) STMP_OMP8_CASE(g, cp, 5, gr)               \
+  STMP_OMP8_CASE(g, cp, 6, gr) STMP_OMP8_CASE(g, cp, 7, gr)
+#define STMP_OMP16_ITERS(cp, gr)                                                                        \
+  STMP_OMP8_ITERS(16, cp, gr) STMP_OMP8_CASE(16, cp, 8, gr) STMP_OMP8_CASE(16, cp, 9, gr)              \
+  STMP_OMP8_CASE(16, cp, 10, gr) STMP_OMP8_CASE(16, cp, 11, gr) STMP_OMP8_CASE(16, cp, 12, gr)         \
+  STMP_OMP8_CASE(16, cp, 13, gr) STMP_OMP8_CASE(16, cp, 14, gr) STMP_OMP8_CASE(16, cp, 15, gr)
+    STMP_OMP8_ITERS(8, 1, 1) STMP_OMP8_ITERS(8, 2, 1) STMP_OMP8_ITERS(8, 3, 1) STMP_OMP8_ITERS(8, 4, 1)
+    STMP_OMP8_ITERS(8, 5, 1) STMP_OMP8_ITERS(8, 1, 0) STMP_OMP8_ITERS(8, 2, 0) STMP_OMP8_ITERS(8, 3, 0)
+    STMP_OMP8_ITERS(8, 4, 0) STMP_OMP8_ITERS(8, 5, 0)
+    STMP_OMP16_ITERS(1, 1) STMP_OMP16_ITERS(2, 1) STMP_OMP16_ITERS(1, 0) STMP_OMP16_ITERS(2, 0)
+#undef STMP_OMP16_ITERS
 #undef STMP_OMP8_ITERS
 #undef STMP_OMP8_CASE
     default: return cudaErrorNotSupported;

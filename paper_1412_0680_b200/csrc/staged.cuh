@@ -108,7 +108,9 @@ size_t update_smem_bytes(const UpdateCfg& c, int K, int ld, bool cache_atoms);
 // OMP update specialised for K <= 8 with a Gram table: one lane per Cholesky row,
 // all solver state in registers, support size a.iter fixed at compile time,
 // state in the [entry][patch] layout.  Returns cudaErrorNotSupported when not applicable.
-cudaError_t launch_update_omp8(const UpdateArgs& a, int blocks, cudaStream_t st);
+cudaError_t launch_update_omp8(const UpdateArgs& a, cudaStream_t st);
+// lanes per patch of the lockstep OMP update for this shape (8 or 16), 0 if unsupported
+int lockstep_lanes(int ld, int K);
 // Build the [m, m] Gram matrix of the (padded) dictionary on `st`; returns nullptr if
 // m exceeds kGramMaxAtoms or memory is short.
 const float* ensure_gram(DictHandle* d, cudaStream_t st);
