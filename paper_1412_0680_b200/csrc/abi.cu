@@ -35,7 +35,7 @@ int g_graphs = 1;             // replay repeated staged encodes as CUDA graphs
 // of small batches and of the chunked host-buffer path.
 struct GraphKey {
   const void* p[14];
-  int64_t v[12];
+  int64_t v[13];
 };
 struct GraphEntry {
   GraphKey key;
@@ -316,6 +316,11 @@ int stmp_set_option(const char* key, int64_t value) {
     stmp::g_score_tma = (int)value;
     return STMP_OK;
   }
+  if (strcmp(key, "root_direct") == 0) {
+    if (value < 0 || value > 1) return fail(STMP_EINVAL, "root_direct must be 0 or 1");
+    stmp::g_root_direct = (int)value;
+    return STMP_OK;
+  }
   if (strcmp(key, "graphs") == 0) {
     if (value < 0 || value > 1) return fail(STMP_EINVAL, "graphs must be 0 or 1");
     g_graphs = (int)value;
@@ -414,8 +419,8 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
     memset(&k, 0, sizeof(k));
     const void* ps[14] = {d, t, X, idx, coef, count, resnorm, path, ip, workspace, stream, nullptr, nullptr, nullptr};
     for (int i = 0; i < 14; ++i) k.p[i] = ps[i];
-    const int64_t vs[12] = {N, ldx, K, method, (int64_t)workspace_bytes, (int64_t)(tol * 1e9f), stmp::g_score_ws,
-                            stmp::g_update_omp8, stmp::g_update_tile, stmp::g_pdl, stmp::g_score_tma, 0};
+    const int64_t vs[13] = {N, ldx, K, method, (int64_t)workspace_bytes, stmp::g_root_direct, stmp::g_score_ws,
+                            stmp::g_update_omp8, stmp::g_update_tile, stmp::g_pdl, stmp::g_score_tma, 0, 0};
     memcpy(k.v, vs, sizeof(vs));
     memcpy(&k.v[11], &tol, sizeof(float));
     std::lock_guard<std::mutex> lock(g_graph_mu);

@@ -26,6 +26,7 @@ namespace stmp {
 using namespace sm100;
 
 int g_pdl = 1;          // programmatic dependent launch between staged kernels
+int g_root_direct = 1;  // root pass over the batch in patch order (no scan / scatter at level 0)
 int g_update_tile = 0;  // 1: tile OMP update fused with the next root scoring (update_tile.cu)
 int g_update_omp8 = 1;  // 1: lockstep OMP update (update_omp8_kernel, encode_update.cu)
 int g_score_ws = 2;  // 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM (default), 3 streamed table
@@ -244,6 +245,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a)
 
 // ------------------------------------------------------------------ scan (one CTA)
 constexpr int kScanThreads = 1024;
+constexpr int kScanSmemBins = 3072;   // 36 KB of dynamic shared memory (+ static CUB storage < 48 KB)
+inline size_t scan_smem(int nbins) { return nbins <= kScanSmemBins ? (size_t)12 * nbins : 0; }
 
 // `stripes` (root level only): kRootStripes partial counts of bin 0, folded
 // into counts[0] and reset here.
@@ -255,6 +258,13 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(int* counts, int nbi
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry[2];
   __shared__ int root_total;
+  // bins' tile offsets / row offsets / counts, kept in shared memory for the item
+  // search when they fit (dynamic size 12 * nbins, else 0)
+  extern __shared__ int s_bins[];
+  const bool in_smem = nbins <= kScanSmemBins;
+  int* s_toff = s_bins;
+  int* s_off = s_bins + nbins;
+  int* s_cnt = s_bins + 2 * nbins;
   if (threadIdx.x == 0) carry[0] = carry[1] = root_total = 0;
   __syncthreads();
   if (stripes != nullptr) {
@@ -281,6 +291,11 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(int* counts, int nbi
       offsets[b] = carry[0] + pre_c;
       tile_off[b] = carry[1] + pre_t;
       cursor[b] = 0;
+      if (in_smem) {
+        s_off[b] = carry[0] + pre_c;
+        s_toff[b] = carry[1] + pre_t;
+        s_cnt[b] = c;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -290,16 +305,19 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(int* counts, int nbi
     __syncthreads();
   }
   const int total_tiles = carry[1];
+  const int* toff = in_smem ? s_toff : tile_off;
+  const int* offs = in_smem ? s_off : offsets;
+  const int* cnts = in_smem ? s_cnt : counts;
   // one item per tile: binary-search the bin owning tile i
   for (int i = threadIdx.x; i < total_tiles; i += kScanThreads) {
     int lo = 0, hi = nbins - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (tile_off[mid] <= i) lo = mid; else hi = mid - 1;
+      if (toff[mid] <= i) lo = mid; else hi = mid - 1;
     }
-    const int k = i - tile_off[lo];
-    const int c = counts[lo];
-    items[i] = make_int4(lo, offsets[lo] + k * kTile, min(kTile, c - k * kTile), 0);
+    const int k = i - toff[lo];
+    const int c = cnts[lo];
+    items[i] = make_int4(lo, offs[lo] + k * kTile, min(kTile, c - k * kTile), 0);
   }
   __syncthreads();
   for (int b = threadIdx.x; b < nbins; b += kScanThreads) counts[b] = 0;
@@ -638,20 +656,30 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   const size_t usmem = update_smem_bytes(uc, K, d->ld, u.cache_atoms != 0);
   // tile update: OMP refit + next-iteration root scoring in one kernel
   const bool tile = t && g_update_tile && u.gram != nullptr && update_tile_supported(d, t, K, method);
+  // the root bin holds every active patch: its pass can walk the batch in patch
+  // order (inactive rows skipped) instead of compacting them (score_ts / score_st /
+  // exact_scan only)
+  const bool root_direct = g_root_direct && !tile && (!t || g_score_ws >= 2 ||
+                                                      score_smem_bytes(d->ld / 32, t->staged_levels[0].npad) >
+                                                          227 * 1024);
+  if (root_direct) u.root_count = nullptr;
   const float* xtable = t ? nullptr : ensure_xtable(const_cast<DictHandle*>(d), st);
   if (!t && xtable == nullptr) return cudaErrorMemoryAllocation;
 
   for (int it = 0; it < K; ++it) {
     if (!t) {
-      // exhaustive selection: compact the active patches, then one tensor-core scan
-      e = launch_kernel(scan_kernel, 1, kScanThreads, 0, st, true, counts, 1, offsets, items, num_items, tile_off,
-                        cursor, stripes);
-      if (e == cudaSuccess)
-        e = launch_kernel(scatter_root_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
-                          (const int*)offsets, cursor, perm);
-      if (e != cudaSuccess) return e;
+      // exhaustive selection: (compact the active patches, then) one tensor-core scan
+      if (!root_direct) {
+        e = launch_kernel(scan_kernel, 1, kScanThreads, scan_smem(1), st, true, counts, 1, offsets, items,
+                          num_items, tile_off, cursor, stripes);
+        if (e == cudaSuccess)
+          e = launch_kernel(scatter_root_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
+                            (const int*)offsets, cursor, perm);
+        if (e != cudaSuccess) return e;
+      }
       ScoreArgs s{};
-      s.R = it == 0 ? R0 : R; s.ld = d->ld; s.nrows = N; s.perm = perm; s.items = items; s.num_items = num_items;
+      s.R = it == 0 ? R0 : R; s.ld = d->ld; s.nrows = N; s.perm = root_direct ? nullptr : perm; s.items = items;
+      s.num_items = num_items; s.active = active;
       s.table = xtable; s.npad = xtable_block_width(d->ld); s.kchunks = d->ld / 32;
       s.nblocks = (int)((d->m + s.npad - 1) / s.npad); s.m_atoms = (int)d->m;
       s.leaf_sel = leaf_sel; s.ip = ip; s.K = K; s.L = 0;
@@ -660,8 +688,10 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
     for (int l = (tile && it > 0) ? 1 : 0; l < L; ++l) {
       const StagedLevel& lv = t->staged_levels[l];
       const int nb = (int)(t->level_offsets[l + 1] - t->level_offsets[l]);
-      e = launch_kernel(scan_kernel, 1, kScanThreads, 0, st, true, counts + bin_off[l], nb, offsets, items,
-                        num_items, tile_off, cursor, l == 0 ? stripes : nullptr);
+      const bool direct_pass = l == 0 && root_direct;
+      if (!direct_pass) {
+      e = launch_kernel(scan_kernel, 1, kScanThreads, scan_smem(nb), st, true, counts + bin_off[l], nb, offsets,
+                        items, num_items, tile_off, cursor, l == 0 ? stripes : nullptr);
       if (e != cudaSuccess) return e;
       if (l == 0)
         e = launch_kernel(scatter_root_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
@@ -678,8 +708,10 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
                           (const int*)path_ws, L, l, (int)t->level_offsets[l], (const int*)offsets, cursor,
                           perm);
       if (e != cudaSuccess) return e;
+      }
       ScoreArgs s{};
-      s.R = it == 0 ? R0 : R; s.ld = d->ld; s.nrows = N; s.perm = perm; s.items = items; s.num_items = num_items;
+      s.R = it == 0 ? R0 : R; s.ld = d->ld; s.nrows = N; s.perm = direct_pass ? nullptr : perm; s.items = items;
+      s.num_items = num_items; s.active = active;
       s.table = t->staged_tables[l]; s.npad = lv.npad; s.kchunks = d->ld / 32; s.tmem_cols = lv.tmem_cols;
       s.level = l; s.level_base = (int)t->level_offsets[l]; s.child_begin = t->child_begin;
       s.child_count = t->child_count; s.path_ws = path_ws; s.path_out = path; s.count = count;

@@ -39,6 +39,7 @@ __device__ __forceinline__ float group_sum(float v) {
 // patch group), spread over kRootStripes counters so the adds of a whole grid
 // do not serialise on one L2 address.  scan_kernel folds the stripes.
 __device__ __forceinline__ void count_root(bool act, int* stripes) {
+  if (stripes == nullptr) return;   // root pass runs over the batch in patch order
   const unsigned m = __ballot_sync(kFull, act);
   if (m && (int)(threadIdx.x & 31) == __ffs(m) - 1)
     atomicAdd(&stripes[(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) & (kRootStripes - 1)], __popc(m));

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int num_items = *a.num_items;
+  const int num_items = item_count(a);
   const int per = (num_items + gridDim.x - 1) / gridDim.x;
   const int i0 = blockIdx.x * per;
   const int i1 = min(num_items, i0 + per);
@@ -150,8 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
     auto row_of = [&](int item) {
       if (item != r_item) {
         r_item = item;
-        const int4 it = a.items[item];
-        r_row = tid < it.z ? a.perm[it.y + tid] : -1;
+        const int4 it = item_at(a, item);
+        r_row = tid < it.z ? row_at(a, it, tid) : -1;
       }
       return r_row;
     };
@@ -183,9 +183,9 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
       const int blk = rem / kch, c = rem - blk * kch;
       const int bs = g / kch, ab = g & 1;
       if (rem == 0) {
-        const int4 it = a.items[item];
-        valid = tid < it.z;
-        cur_p = valid ? a.perm[it.y + tid] : -1;
+        const int4 it = item_at(a, item);
+        cur_p = tid < it.z ? row_at(a, it, tid) : -1;
+        valid = cur_p >= 0;
         best = 0;
         bestv = -1.f;
       }

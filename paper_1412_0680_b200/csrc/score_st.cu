@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int num_items = *a.num_items;
+  const int num_items = item_count(a);
   const int per = (num_items + gridDim.x - 1) / gridDim.x;
   const int i0 = blockIdx.x * per;
   const int i1 = min(num_items, i0 + per);
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       for (int g = 0; g < total; ++g) {
         const int seq = g / kch, c = g - seq * kch;
         if (c == 0) {
-          bin = a.items[i0 + seq].x;
+          bin = item_at(a, i0 + seq).x;
           if (last) {
             const int b = seq & 1;
             if (seq >= 2) mbar_wait(&leafempty[b], (uint32_t)((seq >> 1) - 1) & 1u);
@@ -183,8 +183,8 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
     auto row_of = [&](int item) {
       if (item != r_item) {
         r_item = item;
-        const int4 it = a.items[item];
-        r_row = tid < it.z ? a.perm[it.y + tid] : -1;
+        const int4 it = item_at(a, item);
+        r_row = tid < it.z ? row_at(a, it, tid) : -1;
       }
       return r_row;
     };
@@ -213,10 +213,10 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       const int seq = g / kch, c = g - seq * kch;
       const int ab = g & 1;
       if (c == 0) {
-        const int4 it = a.items[i0 + seq];
+        const int4 it = item_at(a, i0 + seq);
         cur_bin = it.x;
         cur_rows = it.z;
-        cur_p = tid < it.z ? a.perm[it.y + tid] : -1;
+        cur_p = tid < it.z ? row_at(a, it, tid) : -1;
       }
       asm volatile("cp.async.wait_group %0;" ::"n"(NA - 1) : "memory");
       __syncwarp();   // the warp's rows were copied by all of its lanes
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       }
       tc_fence_before();
       mbar_arrive(&accempty[acc]);
-      const bool valid = tid < cur_rows;
+      const bool valid = tid < cur_rows && cur_p >= 0;
       const int p = cur_p;
       int leaf_info = 0, leaf_cnt = 0;
       if (last) {

@@ -56,8 +56,9 @@ __device__ __forceinline__ void gather_rows(const ScoreArgs& a, const int* rows_
     const int row = e / F;
     const int c = e - row * F;
     const uint32_t off = (uint32_t)(c >> 3) * (kT * 128u) + sw128_offset(row, c & 7);
-    const bool ok = row < rows;
-    cp_async16(raw_s + off, a.R + (ok ? (int64_t)rows_ids[row] * a.ld + 4 * c : 0), ok ? 16u : 0u);
+    const int rid = row < rows ? rows_ids[row] : -1;
+    const bool ok = rid >= 0;
+    cp_async16(raw_s + off, a.R + (ok ? (int64_t)rid * a.ld + 4 * c : 0), ok ? 16u : 0u);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
   const uint32_t tmem = *tmem_slot;
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
 
-  const int num_items = *a.num_items;
+  const int num_items = item_count(a);
   const int per = (num_items + gridDim.x - 1) / gridDim.x;
   const int i0 = blockIdx.x * per;
   const int i1 = min(num_items, i0 + per);
@@ -133,9 +134,9 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
   int loaded_bin = -1;
   bool table_pending = false;
 
-  int4 it = i0 < i1 ? a.items[i0] : make_int4(0, 0, 0, 0);
+  int4 it = i0 < i1 ? item_at(a, i0) : make_int4(0, 0, 0, 0);
   if (i0 < i1) {
-    if (tid < it.z) s_rows[tid] = a.perm[it.y + tid];
+    if (tid < it.z) s_rows[tid] = row_at(a, it, tid);
     if (tid == 0) {
       mbar_arrive_expect_tx(&bars[0], tb);
       const uint8_t* src = reinterpret_cast<const uint8_t*>(a.table) + (size_t)it.x * tb;
@@ -157,8 +158,8 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
     const int cc = __ldg(a.child_count + gnode);
     // the next tile's record and patch ids, consumed once this tile is in TMEM
     const bool has_next = item + 1 < i1;
-    const int4 nit = has_next ? a.items[item + 1] : make_int4(0, 0, 0, 0);
-    const int nperm = (has_next && tid < nit.z) ? a.perm[nit.y + tid] : 0;
+    const int4 nit = has_next ? item_at(a, item + 1) : make_int4(0, 0, 0, 0);
+    const int nperm = (has_next && tid < nit.z) ? row_at(a, nit, tid) : 0;
 
     if constexpr (TMA) {
       mbar_wait(&bars[2], g_phase);
@@ -242,8 +243,8 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
         }
       }
     }
-    const bool valid = row < rows;
-    const int p = valid ? rows_ids[row] : 0;
+    const int p = row < rows ? rows_ids[row] : -1;
+    const bool valid = p >= 0;
     const int child = cb + best;
     int leaf_info = 0, leaf_cnt = 0;
     if (last && valid) {

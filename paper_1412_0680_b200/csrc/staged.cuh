@@ -32,7 +32,25 @@ struct ScoreArgs {
   const int* leaf_atom;
   int nblocks;           // exhaustive scan: atom blocks of npad atoms
   int m_atoms;           // exhaustive scan: dictionary size
+  const int* active;     // root pass in patch order (perm == nullptr): skip inactive rows
 };
+
+// Work items of a score pass: (bin, first slot in perm, rows) from the scan, or
+// -- the root pass over the whole batch in patch order, perm == nullptr -- the
+// i-th 128-patch tile of the batch, whose inactive rows carry row id -1.
+__device__ __forceinline__ int item_count(const ScoreArgs& a) {
+  return a.perm ? *a.num_items : (int)((a.nrows + 127) / 128);
+}
+__device__ __forceinline__ int4 item_at(const ScoreArgs& a, int i) {
+  if (a.perm) return a.items[i];
+  return make_int4(0, i * 128, (int)min((int64_t)128, a.nrows - (int64_t)i * 128), 0);
+}
+// patch of row r (< it.z) of item `it`, -1 for a skipped row
+__device__ __forceinline__ int row_at(const ScoreArgs& a, int4 it, int r) {
+  if (a.perm) return a.perm[it.y + r];
+  const int p = it.y + r;
+  return a.active[p] ? p : -1;
+}
 
 struct UpdateArgs {
   const float* X;        // caller's patches (row stride ldx, n valid columns)
@@ -127,6 +145,7 @@ __host__ __device__ inline uint32_t table_bytes(int kch, int npad, bool last) {
 extern int g_score_ws;
 extern int g_score_tma;   // score_ts: tensor-map gathers (1) or per-thread cp.async (0)
 extern int g_update_omp8;
+extern int g_root_direct;
 bool score_ws_fits(int kchunks, int npad, bool last);
 cudaError_t launch_score_ws(const ScoreArgs& s, int sms, cudaStream_t st);
 bool score_ts_fits(int kchunks, int npad, bool last);
