@@ -345,6 +345,11 @@ int stmp_set_option(const char* key, int64_t value) {
     stmp::g_score_ws = (int)value;
     return STMP_OK;
   }
+  if (strcmp(key, "gram") == 0) {
+    if (value < 0 || value > 1) return fail(STMP_EINVAL, "gram must be 0 or 1");
+    stmp::g_gram = (int)value;
+    return STMP_OK;
+  }
   if (strcmp(key, "staged_min_batch") == 0) {
     if (value < 1) return fail(STMP_EINVAL, "staged_min_batch must be positive");
     g_staged_min = value;
@@ -420,7 +425,7 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
     const void* ps[14] = {d, t, X, idx, coef, count, resnorm, path, ip, workspace, stream, nullptr, nullptr, nullptr};
     for (int i = 0; i < 14; ++i) k.p[i] = ps[i];
     const int64_t vs[13] = {N, ldx, K, method, (int64_t)workspace_bytes, stmp::g_root_direct, stmp::g_score_ws,
-                            stmp::g_update_omp8, stmp::g_update_tile, stmp::g_pdl, stmp::g_score_tma, 0, 0};
+                            stmp::g_update_omp8, stmp::g_update_tile, stmp::g_pdl, stmp::g_score_tma, 0, stmp::g_gram};
     memcpy(k.v, vs, sizeof(vs));
     memcpy(&k.v[11], &tol, sizeof(float));
     std::lock_guard<std::mutex> lock(g_graph_mu);

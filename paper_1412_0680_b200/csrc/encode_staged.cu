@@ -29,6 +29,7 @@ int g_pdl = 1;          // programmatic dependent launch between staged kernels
 int g_root_direct = 1;  // root pass over the batch in patch order (no scan / scatter at level 0)
 int g_update_tile = 0;  // 1: tile OMP update fused with the next root scoring (update_tile.cu)
 int g_update_omp8 = 1;  // 1: lockstep OMP update (update_omp8_kernel, encode_update.cu)
+int g_gram = 0;         // 1: atom Gram table for the lockstep update (m <= kGramMaxAtoms); off: measured slower than the support-row dots (c1 update 2.09 vs 1.83 ms)
 int g_score_ws = 2;  // 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM (default), 3 streamed table
 
 namespace {
@@ -630,7 +631,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   // lockstep OMP update (update_omp8_kernel): K <= 8 with rows of <= 160 floats or K <= 16 with <= 128; the
   // atom Gram table when the dictionary is small enough, dot products otherwise
   const bool lockstep = method == kMethodOMP && lockstep_lanes(d->ld, K) != 0 && g_update_omp8;
-  u.gram = lockstep ? ensure_gram(const_cast<DictHandle*>(d), st) : nullptr;
+  u.gram = lockstep && g_gram ? ensure_gram(const_cast<DictHandle*>(d), st) : nullptr;
   u.m = d->m;
   // stage the support atoms in shared memory when the patch groups fit comfortably
   u.cache_atoms = update_smem_bytes(uc, K, d->ld, true) <= 96 * 1024 ? 1 : 0;

@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
 #define STMP_OMP8_MINB 8
 #endif
 #ifndef STMP_OMP8_MINB0
-#define STMP_OMP8_MINB0 12
+#define STMP_OMP8_MINB0 10
 #endif
 #ifndef STMP_SUP_SMEM
 #define STMP_SUP_SMEM 1
@@ -330,10 +330,50 @@ constexpr bool sup_smem() { return STMP_SUP_SMEM && GRAM && T >= 1 && T <= 3; }
 // T group dot products against the support rows, which the residual rebuild
 // reads again (from L1 / L2).
 // G = 16 lanes per patch (rows of <= 128 floats) lifts the support limit to 16.
+//
+// The solve runs warp-uniformly: a warp whose patches are all inactive returns,
+// otherwise every lane executes the refit (results of inactive patches are
+// never stored), so every shuffle is a plain full-warp SHFL with no divergence
+// handling.  The reductions are shaped to the refit's data flow:
+//   * the T + 2 dot products (g_k, a.a, a.x) are one reduce-scatter over the
+//     group (lane k receives value k) followed by broadcasts of g;
+//   * w_j = sum_k M[j][k] g_k is lane-local (lane j owns row j of M);
+//   * the column sums sum_j w_j M[j][k] of the new row are one reduce-scatter
+//     (lane k receives column k, which is exactly the entry it stores);
+//   * c_new = c_prev + m_T y_T reuses the stored c_prev (c_prev = M^T y over
+//     the previous rows), so no M^T y sweep is needed.
+template <int G>
+__device__ __forceinline__ float gsum_full(float v) {
+#pragma unroll
+  for (int o = G >> 1; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Reduce-scatter over the G lanes of a group (all 32 lanes call): on return
+// lane gl holds the group sum of p[gl].
+template <int G>
+__device__ __forceinline__ float group_reduce_scatter(float (&p)[G], int gl) {
+#pragma unroll
+  for (int o = G >> 1; o >= 1; o >>= 1) {
+    const bool upper = (gl & o) != 0;
+#pragma unroll
+    for (int j = 0; j < o; ++j) {
+      const float send = upper ? p[j] : p[j + o];
+      const float keep = upper ? p[j + o] : p[j];
+      p[j] = keep + __shfl_xor_sync(kFull, send, o);
+    }
+  }
+  return p[0];
+}
+
+template <int G>
+__device__ __forceinline__ float group_bcast(float v, int k) { return __shfl_sync(kFull, v, k, G); }
+
 template <int G, int CPL, int T, bool GRAM>
-__global__ void __launch_bounds__(128, G == 8 ? (T == 0 ? STMP_OMP8_MINB0 : STMP_OMP8_MINB) : 6)
+__global__ void __launch_bounds__(128, G == 8 ? (CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : STMP_OMP8_MINB) : 5) : 6)
     update_omp8_kernel(UpdateArgs a) {
   constexpr bool kSupSmem = sup_smem<T, GRAM>();
+  static_assert(T < G, "lockstep support index must fit the patch group");
   pdl_enter();
   const int64_t N = a.N;
   const int64_t p = (int64_t)blockIdx.x * (128 / G) + threadIdx.x / G;
@@ -366,135 +406,148 @@ __global__ void __launch_bounds__(128, G == 8 ? (T == 0 ? STMP_OMP8_MINB0 : STMP
   const float* Mrow = a.Lf + (int64_t)(gl * (gl + 1) / 2) * N + pc;
 #pragma unroll
   for (int k = 0; k < T; ++k) mrow[k] = (row_live && k <= gl) ? sm100::ld_now(Mrow + k * N) : 0.f;
-  bool act = act_in != 0;
-  if (act) {
+  const bool act = act_in != 0;
+  if (!__any_sync(kFull, act)) return;   // warp-uniform: nothing to do, nothing to count
+  // inactive patches run along on valid (atom 0) addresses; nothing of theirs is stored
+#pragma unroll
+  for (int k = 0; k < T; ++k) S[k] = act ? S[k] : 0;
+  int atom = act && lsel >= 0 ? lsel : 0;
+  const bool multi = act && lsel < 0;
+  if (__any_sync(kFull, multi)) {  // multi-atom leaf: max |a . r|, ties to the lowest atom index
     Sl r;
-    int atom = lsel;
-    if (lsel < 0) {  // multi-atom leaf: max |a . r|, ties to the lowest atom index
-      r.load(a.R_in + p * a.ld, gl, F);
-      const int node = -1 - lsel;
-      const int cb = __ldg(a.child_begin + node), cc = __ldg(a.child_count + node);
-      float bestv = -1.f;
-      atom = __ldg(a.leaf_atom + cb);
-      for (int j = 0; j < cc; ++j) {
-        const int aj = __ldg(a.leaf_atom + cb + j);
-        Sl v;
-        v.load(a.atoms + (int64_t)aj * a.ld, gl, F);
-        const float mv = fabsf(group_sum<G>(v.dot(r)));
-        if (mv > bestv || (mv == bestv && aj < atom)) { bestv = mv; atom = aj; }
-      }
+    r.load(a.R_in + pc * a.ld, gl, F);
+    const int node = multi ? -1 - lsel : 0;
+    const int cb = multi ? __ldg(a.child_begin + node) : 0;
+    const int cc = multi ? __ldg(a.child_count + node) : 0;
+    int ccmax = cc;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ccmax = max(ccmax, __shfl_xor_sync(kFull, ccmax, o));
+    float bestv = -1.f;
+    if (multi) atom = __ldg(a.leaf_atom + cb);
+    for (int j = 0; j < ccmax; ++j) {
+      const bool in = j < cc;
+      const int aj = in ? __ldg(a.leaf_atom + cb + j) : 0;
+      Sl v;
+      v.load(a.atoms + (int64_t)aj * a.ld, gl, F);
+      const float mv = fabsf(gsum_full<G>(v.dot(r)));
+      if (in && (mv > bestv || (mv == bestv && aj < atom))) { bestv = mv; atom = aj; }
     }
-    // support rows, needed after the refit: cp.async into this group's shared
-    // slice now, so their L2 round trip overlaps the new atom's
-    extern __shared__ float4 s_sup[];   // [128 / G groups][T][F] 16-byte chunks
-    float4* sup = s_sup + (size_t)((threadIdx.x / G) * T) * F;
-    if constexpr (kSupSmem) {
+  }
+  // support rows, needed after the refit: cp.async into this group's shared
+  // slice now, so their L2 round trip overlaps the new atom's
+  extern __shared__ float4 s_sup[];   // [128 / G groups][T][F] 16-byte chunks
+  float4* sup = s_sup + (size_t)((threadIdx.x / G) * T) * F;
+  if constexpr (kSupSmem) {
 #pragma unroll
-      for (int k = 0; k < T; ++k)
+    for (int k = 0; k < T; ++k)
 #pragma unroll
-        for (int i = 0; i < CPL; ++i) {
-          const int ch = gl + G * i;
-          if (ch < F)
-            sm100::cp_async16(sm100::smem_u32(sup + k * F + ch), a.atoms + (int64_t)S[k] * a.ld + 4 * ch, 16u);
+      for (int i = 0; i < CPL; ++i) {
+        const int ch = gl + G * i;
+        if (ch < F)
+          sm100::cp_async16(sm100::smem_u32(sup + k * F + ch), a.atoms + (int64_t)S[k] * a.ld + 4 * ch, 16u);
+      }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  Sl av;
+  av.load(a.atoms + (int64_t)atom * a.ld, gl, F);
+  float g[T + 1];
+  bool dup = false;
+#pragma unroll
+  for (int k = 0; k < T; ++k) dup |= S[k] == atom;
+  float gtt, bt;
+  if constexpr (GRAM) {
+    const float* grow = a.gram + (int64_t)atom * a.m;
+#pragma unroll
+    for (int k = 0; k < T; ++k) g[k] = __ldg(grow + S[k]);
+    gtt = __ldg(grow + atom);
+    bt = gsum_full<G>(av.dot(x));
+  } else {
+    // value k < T: a . a_{S_k};  T: a . a;  T + 1: a . x (if it fits the group)
+    float pv[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k) pv[k] = 0.f;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      Sl sv;
+      sv.load(a.atoms + (int64_t)S[k] * a.ld, gl, F);
+      pv[k] = sv.dot(av);
+    }
+    pv[T] = av.dot(av);
+    constexpr bool kBtInRs = T + 1 < G;
+    float bt_part = av.dot(x);
+    if constexpr (kBtInRs) pv[T + 1] = bt_part;
+    const float mine = group_reduce_scatter<G>(pv, gl);
+#pragma unroll
+    for (int k = 0; k < T; ++k) g[k] = group_bcast<G>(mine, k);
+    gtt = group_bcast<G>(mine, T);
+    if constexpr (kBtInRs) bt = group_bcast<G>(mine, T + 1);
+    else bt = gsum_full<G>(bt_part);
+  }
+  // a . (A_S c_prev), lane k holding c_prev_k:  the a . r of pursuit.py:217
+  float gmine = 0.f;   // g[gl] without dynamic indexing
+#pragma unroll
+  for (int k = 0; k < T; ++k) gmine = k == gl ? g[k] : gmine;
+  // w = M g (lane j: row j); one butterfly for a.(A_S c_prev), w.w, w.y
+  float wj = 0.f;
+#pragma unroll
+  for (int k = 0; k < T; ++k) wj = fmaf(mrow[k], g[k], wj);
+  float gc = gmine * cj, wsum = wj * wj, wy = wj * yj;
+#pragma unroll
+  for (int o = G >> 1; o; o >>= 1) {
+    gc += __shfl_xor_sync(kFull, gc, o);
+    wsum += __shfl_xor_sync(kFull, wsum, o);
+    wy += __shfl_xor_sync(kFull, wy, o);
+  }
+  const float score = bt - gc;   // a . r for r = x - A_S c_prev (pursuit.py:217 check)
+  const bool ok = act && !dup && score != 0.f;   // re-selection or a zero score ends the loop
+  const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
+  const float inv_d = 1.f / dg;
+  const float yy = (bt - wy) * inv_d;
+  // column sums colw_k = sum_j w_j M[j][k]: lane k receives its own column
+  float pc_[G];
+#pragma unroll
+  for (int k = 0; k < G; ++k) pc_[k] = k < T ? wj * mrow[k < T ? k : 0] : 0.f;
+  const float colw = group_reduce_scatter<G>(pc_, gl);
+  // new row T of M: (-(1/d) w^T M, 1/d);  c_new = c_prev + m_T y_T
+  const float mt_mine = gl < T ? -inv_d * colw : (gl == T ? inv_d : 0.f);
+  const float c_new = gl < T ? fmaf(mt_mine, yy, cj) : (gl == T ? inv_d * yy : 0.f);
+  S[T] = atom;
+  bool act_next = false;
+  float c[T + 1];
+#pragma unroll
+  for (int k = 0; k <= T; ++k) c[k] = group_bcast<G>(ok ? c_new : cj, k);
+  if (__any_sync(kFull, ok)) {
+    // residual r = x - A_S c (support rows from L1 / L2 / shared memory) - c_T a
+    Sl r;
+#pragma unroll
+    for (int i = 0; i < CPL * 4; ++i) r.v[i] = fmaf(-c[T], av.v[i], x.v[i]);
+    if constexpr (kSupSmem) asm volatile("cp.async.wait_all;" ::: "memory");   // own copies only: no barrier
+#pragma unroll
+    for (int k = 0; k < T; ++k)
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) {
+        const int ch = gl + G * i;
+        if (ch < F) {
+          const float4 q = kSupSmem ? sup[k * F + ch]
+                                    : __ldg(reinterpret_cast<const float4*>(a.atoms + (int64_t)S[k] * a.ld) + ch);
+          r.v[4 * i] = fmaf(-c[k], q.x, r.v[4 * i]);
+          r.v[4 * i + 1] = fmaf(-c[k], q.y, r.v[4 * i + 1]);
+          r.v[4 * i + 2] = fmaf(-c[k], q.z, r.v[4 * i + 2]);
+          r.v[4 * i + 3] = fmaf(-c[k], q.w, r.v[4 * i + 3]);
         }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-    Sl av;
-    av.load(a.atoms + (int64_t)atom * a.ld, gl, F);
-    float g[T + 1];
-    bool dup = false;
-    float gtt;
-    if constexpr (GRAM) {
-      const float* grow = a.gram + (int64_t)atom * a.m;
-#pragma unroll
-      for (int k = 0; k < T; ++k) {
-        g[k] = __ldg(grow + S[k]);
-        dup |= S[k] == atom;
       }
-      gtt = __ldg(grow + atom);
-    } else {
+    float s2 = 0.f;
 #pragma unroll
-      for (int k = 0; k < T; ++k) {
-        Sl sv;
-        sv.load(a.atoms + (int64_t)S[k] * a.ld, gl, F);
-        g[k] = group_sum<G>(sv.dot(av));
-        dup |= S[k] == atom;
-      }
-      gtt = group_sum<G>(av.dot(av));
-    }
-    const float bt = group_sum<G>(av.dot(x));
-    float gmine = 0.f;   // g[gl] without dynamic indexing
-#pragma unroll
-    for (int k = 0; k < T; ++k) gmine = k == gl ? g[k] : gmine;
-    const float gc = group_sum<G>(gmine * cj);   // a . (A_S c_prev)
-    const float score = bt - gc;   // a . r for r = x - A_S c_prev (pursuit.py:217 check)
-    const bool ok = !dup && score != 0.f;   // re-selection or a zero score ends the loop
-    float c[T + 1];
-    bool act_next = false;
+    for (int i = 0; i < CPL * 4; ++i) s2 = fmaf(r.v[i], r.v[i], s2);
+    const float rn = sqrtf(gsum_full<G>(s2));
     if (ok) {
-      // w = M g (lane j: row j), then the column sums  sum_j w_j M[j][k]  and  sum_j y_j M[j][k]
-      float wj = 0.f;
-#pragma unroll
-      for (int k = 0; k < T; ++k) wj = fmaf(mrow[k], g[k], wj);
-      const float wsum = group_sum<G>(wj * wj);
-      const float wy = group_sum<G>(wj * yj);
-      const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
-      const float inv_d = 1.f / dg;
-      const float yy = (bt - wy) * inv_d;
-      float colw[T + 1], coly[T + 1];
-#pragma unroll
-      for (int k = 0; k < T; ++k) {
-        colw[k] = wj * mrow[k];
-        coly[k] = yj * mrow[k];
-      }
-#pragma unroll
-      for (int o = G >> 1; o; o >>= 1) {
-#pragma unroll
-        for (int k = 0; k < T; ++k) {
-          colw[k] += __shfl_xor_sync(group_mask<G>(), colw[k], o);
-          coly[k] += __shfl_xor_sync(group_mask<G>(), coly[k], o);
-        }
-      }
-      // new row T of M: (-(1/d) w^T M, 1/d);  c = M^T y with y_T = yy
-      float mt_mine = gl == T ? inv_d : 0.f;
-#pragma unroll
-      for (int k = 0; k < T; ++k) {
-        const float mtk = -inv_d * colw[k];
-        c[k] = fmaf(mtk, yy, coly[k]);
-        mt_mine = k == gl ? mtk : mt_mine;
-      }
-      c[T] = inv_d * yy;
-      S[T] = atom;
-      // residual r = x - A_S c (support rows from L2) - c_T a
-#pragma unroll
-      for (int i = 0; i < CPL * 4; ++i) r.v[i] = fmaf(-c[T], av.v[i], x.v[i]);
-      if constexpr (kSupSmem) asm volatile("cp.async.wait_all;" ::: "memory");   // own copies only: no barrier
-#pragma unroll
-      for (int k = 0; k < T; ++k)
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) {
-          const int ch = gl + G * i;
-          if (ch < F) {
-            const float4 q = kSupSmem ? sup[k * F + ch]
-                                      : __ldg(reinterpret_cast<const float4*>(a.atoms + (int64_t)S[k] * a.ld) + ch);
-            r.v[4 * i] = fmaf(-c[k], q.x, r.v[4 * i]);
-            r.v[4 * i + 1] = fmaf(-c[k], q.y, r.v[4 * i + 1]);
-            r.v[4 * i + 2] = fmaf(-c[k], q.z, r.v[4 * i + 2]);
-            r.v[4 * i + 3] = fmaf(-c[k], q.w, r.v[4 * i + 3]);
-          }
-        }
       r.store(a.R + p * a.ld, gl, F);
-      float s2 = 0.f;
-#pragma unroll
-      for (int i = 0; i < CPL * 4; ++i) s2 = fmaf(r.v[i], r.v[i], s2);
-      const float rn = sqrtf(group_sum<G>(s2));
       act_next = (T + 1 < K) && rn > a.tol[p];
       if (act_next) {
-        if (gl <= T) a.Lf[(int64_t)(T * (T + 1) / 2 + gl) * N + p] = mt_mine;
-        float c_mine = c[T];
-#pragma unroll
-        for (int k = 0; k < T; ++k) c_mine = k == gl ? c[k] : c_mine;
-        if (gl <= T) a.c_ws[gl * N + p] = c_mine;
+        if (gl <= T) {
+          a.Lf[(int64_t)(T * (T + 1) / 2 + gl) * N + p] = mt_mine;
+          a.c_ws[gl * N + p] = c_new;
+        }
         if (gl == 0) {
           a.yv[T * N + p] = yy;
           a.S_ws[T * N + p] = atom;
@@ -504,31 +557,23 @@ __global__ void __launch_bounds__(128, G == 8 ? (T == 0 ? STMP_OMP8_MINB0 : STMP
         a.count[p] = T + 1;
         a.resnorm[p] = rn;
       }
-    } else {
-      if constexpr (kSupSmem) asm volatile("cp.async.wait_all;" ::: "memory");   // no copy may outlive the CTA's smem
-      // the patch stops on its previous support: c_prev is the lane-owned c_j
-#pragma unroll
-      for (int k = 0; k < T; ++k) c[k] = __shfl_sync(group_mask<G>(), cj, (threadIdx.x & ~(G - 1)) + k);
     }
-    if (!act_next) {
-      // final rows of the caller's idx / coef (T or T + 1 entries; the rest stay -1 / 0 from init)
-      const int n_out = ok ? T + 1 : T;
-      if (gl < n_out) {
-        int s_mine = S[0];
-        float c_mine = c[0];
-#pragma unroll
-        for (int k = 1; k <= T; ++k) {
-          s_mine = k == gl ? S[k] : s_mine;
-          c_mine = k == gl ? c[k] : c_mine;
-        }
-        a.idx[p * K + gl] = s_mine;
-        a.coef[p * K + gl] = c_mine;
-      }
-    }
-    if (gl == 0) a.active[p] = act_next ? 1 : 0;
-    act = act_next;
+  } else if constexpr (kSupSmem) {
+    asm volatile("cp.async.wait_all;" ::: "memory");   // no copy may outlive the CTA's smem
   }
-  count_root(act && gl == 0, a.root_count);
+  if (act && !act_next) {
+    // final rows of the caller's idx / coef (T or T + 1 entries; the rest stay -1 / 0 from init)
+    const int n_out = ok ? T + 1 : T;
+    if (gl < n_out) {
+      int s_mine = S[0];
+#pragma unroll
+      for (int k = 1; k <= T; ++k) s_mine = k == gl ? S[k] : s_mine;
+      a.idx[p * K + gl] = s_mine;
+      a.coef[p * K + gl] = ok ? c_new : cj;
+    }
+  }
+  if (act && gl == 0) a.active[p] = act_next ? 1 : 0;
+  count_root(act_next && gl == 0, a.root_count);
 }
 
 }  // namespace

@@ -145,6 +145,7 @@ __host__ __device__ inline uint32_t table_bytes(int kch, int npad, bool last) {
 extern int g_score_ws;
 extern int g_score_tma;   // score_ts: tensor-map gathers (1) or per-thread cp.async (0)
 extern int g_update_omp8;
+extern int g_gram;
 extern int g_root_direct;
 bool score_ws_fits(int kchunks, int npad, bool last);
 cudaError_t launch_score_ws(const ScoreArgs& s, int sms, cudaStream_t st);

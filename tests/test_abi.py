@@ -103,7 +103,7 @@ def test_argument_validation_maps_to_value_error(lib):
 def test_options_and_launch_counter(lib):
     before = _lib.kernel_launches()
     assert before >= 0
-    for key, bad in (("path", 3), ("score_kernel", 4), ("update_kernel", 3)):
+    for key, bad in (("path", 3), ("score_kernel", 4), ("update_kernel", 3), ("gram", 2)):
         with pytest.raises(ValueError):
             _lib.set_option(key, bad)
     with pytest.raises(ValueError):

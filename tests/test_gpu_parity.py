@@ -30,16 +30,17 @@ def P():
 
 # (score_kernel, update_kernel) per staged variant; library defaults are (2, 1)
 STAGED_KERNELS = {"staged": (0, 1), "staged-ws": (1, 1), "staged-ts": (2, 1), "staged-tile": (2, 2),
-                  "staged-st": (3, 1)}
+                  "staged-st": (3, 1), "staged-gram": (2, 1)}
 
 
 def restore_defaults(_lib):
     _lib.set_option("path", _lib.PATH_AUTO)
     _lib.set_option("score_kernel", 2)
     _lib.set_option("update_kernel", 1)
+    _lib.set_option("gram", 0)
 
 
-@pytest.fixture(params=["fused", "staged", "staged-ws", "staged-ts", "staged-tile", "staged-st"])
+@pytest.fixture(params=["fused", "staged", "staged-ws", "staged-ts", "staged-tile", "staged-st", "staged-gram"])
 def path(request):
     """Force one encoder implementation (the C ABI 'path' / 'score_kernel' /
     'update_kernel' options)."""
@@ -49,11 +50,12 @@ def path(request):
     sk, uk = STAGED_KERNELS.get(mode, (2, 2))
     _lib.set_option("score_kernel", sk)
     _lib.set_option("update_kernel", uk)
+    _lib.set_option("gram", 1 if mode == "staged-gram" else 0)   # lockstep update with the atom Gram table
     yield mode
     restore_defaults(_lib)
 
 
-@pytest.mark.parametrize("kernels", sorted(STAGED_KERNELS.values()))
+@pytest.mark.parametrize("kernels", sorted(set(STAGED_KERNELS.values())))
 def test_staged_is_deterministic_and_batch_invariant(kernels):
     """262,144 config-1 patches: two runs and a run in 8192-patch batches must agree
     bitwise (each patch's arithmetic is independent of bucketing order)."""
