@@ -344,52 +344,104 @@ __global__ void scatter_kernel(int64_t N, const int* active, const int* path_ws,
   }
 }
 
-// Levels with few bins: block-local histogram in shared memory, one global
-// atomic per (block, bin); each block covers kScatterThreads * PER patches (PER
-// shrinks with the batch so small batches still spread over the SMs).
 constexpr int kScatterThreads = 512;
 
+// Scan fused into the scatter (levels >= 1 with few bins): every CTA scans the
+// level's bin counts (written by the previous level's score pass) in shared
+// memory, so no separate one-CTA scan launch sits between the two passes.  The
+// CTAs also write the score pass's work items (one per 128-patch tile, bins in
+// order) and zero the counters of the other iteration parity, which were last
+// read one iteration ago and are produced again by the next iteration's score
+// passes.  All loads of a patch are issued together (no active -> path chain).
+constexpr int kScanRun = 8;   // bins per thread in the block scan: nbins <= 512 * 8
 template <int kScatterPer>
-__global__ void __launch_bounds__(kScatterThreads) scatter_hist_kernel(
+__global__ void __launch_bounds__(kScatterThreads) scatter_scan_kernel(
     int64_t N, const int* active, const int* path_ws, int L, int level, int level_base, int nbins,
-    const int* offsets, int* cursor, int* perm) {
+    const int* counts, int* cursor, int* zero_counts, int* zero_cursor, int* perm, int4* items,
+    int* num_items) {
   pdl_enter();
-  extern __shared__ int sh[];  // [nbins] local counts, then [nbins] global bases
-  int* base = sh + nbins;
-  for (int b = threadIdx.x; b < nbins; b += kScatterThreads) sh[b] = 0;
-  __syncthreads();
+  using Scan = cub::BlockScan<int, kScatterThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_total_tiles;
+  extern __shared__ int sh[];  // [nbins] local counts | base | bin offsets | tile offsets
+  int* s_loc = sh;
+  int* s_base = sh + nbins;
+  int* s_off = sh + 2 * nbins;
+  int* s_toff = sh + 3 * nbins;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int64_t p0 = (int64_t)blockIdx.x * kScatterThreads * kScatterPer + tid;
   int bins[kScatterPer], local[kScatterPer];
-  const int64_t p0 = (int64_t)blockIdx.x * kScatterThreads * kScatterPer + threadIdx.x;
-  const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int i = 0; i < kScatterPer; ++i) {
     const int64_t p = p0 + (int64_t)i * kScatterThreads;
-    const bool act = p < N && active[p];
-    bins[i] = act ? path_ws[p * L + level - 1] - level_base : -1;
+    const bool in = p < N;
+    const int act = in ? __ldg(active + p) : 0;
+    const int pv = in ? __ldg(path_ws + p * L + level - 1) : level_base;
+    bins[i] = act ? pv - level_base : -1;
   }
-  // one shared-memory atomic per (warp, bin): few bins means many equal keys
+  const int b0 = tid * kScanRun;
+  int cv[kScanRun];
+  int csum = 0, tsum = 0;
+#pragma unroll
+  for (int j = 0; j < kScanRun; ++j) {
+    cv[j] = b0 + j < nbins ? __ldg(counts + b0 + j) : 0;
+    csum += cv[j];
+    tsum += (cv[j] + kTile - 1) / kTile;
+  }
+  for (int b = blockIdx.x * kScatterThreads + tid; b < nbins; b += gridDim.x * kScatterThreads) {
+    zero_counts[b] = 0;
+    zero_cursor[b] = 0;
+  }
+  for (int b = tid; b < nbins; b += kScatterThreads) s_loc[b] = 0;
+  int cpre, tpre, ttot;
+  Scan(tmp).ExclusiveSum(csum, cpre);
+  __syncthreads();
+  Scan(tmp).ExclusiveSum(tsum, tpre, ttot);
+#pragma unroll
+  for (int j = 0; j < kScanRun; ++j) {
+    if (b0 + j < nbins) {
+      s_off[b0 + j] = cpre;
+      s_toff[b0 + j] = tpre;
+    }
+    cpre += cv[j];
+    tpre += (cv[j] + kTile - 1) / kTile;
+  }
+  if (tid == 0) s_total_tiles = ttot;
+  __syncthreads();
+  // one shared-memory atomic per (warp, bin)
 #pragma unroll
   for (int i = 0; i < kScatterPer; ++i) {
     const unsigned peers = __match_any_sync(kFull, bins[i]);
     const int leader = __ffs(peers) - 1;
     int b = 0;
-    if (lane == leader && bins[i] >= 0) b = atomicAdd(&sh[bins[i]], __popc(peers));
+    if (lane == leader && bins[i] >= 0) b = atomicAdd(&s_loc[bins[i]], __popc(peers));
     b = __shfl_sync(kFull, b, leader);
     local[i] = b + __popc(peers & ((1u << lane) - 1u));
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < nbins; b += kScatterThreads) {
-    const int c = sh[b];
-    base[b] = c ? atomicAdd(&cursor[b], c) : 0;
+  for (int b = tid; b < nbins; b += kScatterThreads) {
+    const int c = s_loc[b];
+    s_base[b] = c ? s_off[b] + atomicAdd(&cursor[b], c) : 0;
   }
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kScatterPer; ++i) {
-    if (bins[i] >= 0) {
-      const int64_t p = p0 + (int64_t)i * kScatterThreads;
-      perm[offsets[bins[i]] + base[bins[i]] + local[i]] = (int)p;
-    }
+    if (bins[i] >= 0) perm[s_base[bins[i]] + local[i]] = (int)(p0 + (int64_t)i * kScatterThreads);
   }
+  // work items of the score pass: tile i -> (bin, first slot, rows)
+  const int total = s_total_tiles;
+  for (int i = blockIdx.x * kScatterThreads + tid; i < total; i += gridDim.x * kScatterThreads) {
+    int lo = 0, hi = nbins - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_toff[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    const int k = i - s_toff[lo];
+    const int c = (lo + 1 < nbins ? s_off[lo + 1] : s_off[lo] + __ldg(counts + lo)) - s_off[lo];
+    items[i] = make_int4(lo, s_off[lo] + k * kTile, min(kTile, c - k * kTile), 0);
+  }
+  if (blockIdx.x == 0 && tid == 0) *num_items = total;
 }
 
 // Root level: a single bin holding every active patch.  One atomic per CTA.
@@ -536,7 +588,7 @@ namespace {
 struct WsLayout {
   size_t total = 0;
   size_t R, Xpad, tol, active, perm, path_ws, leaf_sel, Lf, yv, S_ws, c_ws, counts, offsets, tile_off, cursor, items,
-      num_items;
+      num_items, cursor2;
 };
 
 WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method,
@@ -568,7 +620,9 @@ WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int 
   w.yv = add((size_t)N * K * 4);
   w.S_ws = add((size_t)N * K * 4);
   w.c_ws = add((size_t)N * K * 4);
-  w.counts = add((size_t)(bin_off[LB] + kRootStripes) * 4);
+  // bin counters, one set per iteration parity (scatter_scan_kernel), then the root stripes
+  w.counts = add((size_t)(2 * bin_off[LB] + kRootStripes) * 4);
+  w.cursor2 = add((size_t)2 * bin_off[LB] * 4);
   w.offsets = add((size_t)(maxbins + 1) * 4);
   w.tile_off = add((size_t)(maxbins + 1) * 4);
   w.cursor = add((size_t)(maxbins + 1) * 4);
@@ -614,9 +668,14 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   int4* items = (int4*)(b + w.items);
   int* num_items = (int*)(b + w.num_items);
 
-  int* stripes = counts + bin_off[LB];
-  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)(bin_off[LB] + kRootStripes) * 4, st);
+  int* stripes = counts + 2 * bin_off[LB];
+  int* cursor2 = (int*)(b + w.cursor2);
+  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)(2 * bin_off[LB] + kRootStripes) * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(cursor2, 0, (size_t)2 * bin_off[LB] * 4, st);
   if (e != cudaSuccess) return e;
+  // counters written by the score passes of iteration `it` (and read by its scatters)
+  auto counts_of = [&](int it_) { return counts + (it_ & 1) * bin_off[LB]; };
+  auto cursor_of = [&](int it_) { return cursor2 + (it_ & 1) * bin_off[LB]; };
 
   UpdateCfg uc;
   update_config(d->ld, K, uc);
@@ -671,7 +730,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
     if (!t) {
       // exhaustive selection: (compact the active patches, then) one tensor-core scan
       if (!root_direct) {
-        e = launch_kernel(scan_kernel, 1, kScanThreads, scan_smem(1), st, true, counts, 1, offsets, items,
+        e = launch_kernel(scan_kernel, 1, kScanThreads, scan_smem(1), st, true, counts_of(it), 1, offsets, items,
                           num_items, tile_off, cursor, stripes);
         if (e == cudaSuccess)
           e = launch_kernel(scatter_root_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
@@ -690,20 +749,27 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       const StagedLevel& lv = t->staged_levels[l];
       const int nb = (int)(t->level_offsets[l + 1] - t->level_offsets[l]);
       const bool direct_pass = l == 0 && root_direct;
-      if (!direct_pass) {
-      e = launch_kernel(scan_kernel, 1, kScanThreads, scan_smem(nb), st, true, counts + bin_off[l], nb, offsets,
+      if (!direct_pass && l > 0 && nb <= kScanRun * kScatterThreads) {
+        // scan fused into the scatter; counters double-buffered by iteration parity
+        const int per = N >= (int64_t)sms * kScatterThreads * 8 ? 8 : N >= (int64_t)sms * kScatterThreads * 2 ? 2 : 1;
+        const int grid = (int)((N + kScatterThreads * per - 1) / (kScatterThreads * per));
+        auto k = per == 8 ? scatter_scan_kernel<8> : per == 2 ? scatter_scan_kernel<2> : scatter_scan_kernel<1>;
+        const size_t smem = (size_t)nb * 16;
+        if (smem > 48 * 1024 &&
+            (e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+          return e;
+        e = launch_kernel(k, grid, kScatterThreads, smem, st, true, N, (const int*)active, (const int*)path_ws, L, l,
+                          (int)t->level_offsets[l], nb, (const int*)(counts_of(it) + bin_off[l]),
+                          cursor_of(it) + bin_off[l], counts_of(it + 1) + bin_off[l], cursor_of(it + 1) + bin_off[l],
+                          perm, items, num_items);
+        if (e != cudaSuccess) return e;
+      } else if (!direct_pass) {
+      e = launch_kernel(scan_kernel, 1, kScanThreads, scan_smem(nb), st, true, counts_of(it) + bin_off[l], nb, offsets,
                         items, num_items, tile_off, cursor, l == 0 ? stripes : nullptr);
       if (e != cudaSuccess) return e;
       if (l == 0)
         e = launch_kernel(scatter_root_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
                           (const int*)offsets, cursor, perm);
-      else if (nb <= 4096) {
-        const int per = N >= (int64_t)sms * kScatterThreads * 8 ? 8 : N >= (int64_t)sms * kScatterThreads * 2 ? 2 : 1;
-        const int grid = (int)((N + kScatterThreads * per - 1) / (kScatterThreads * per));
-        auto k = per == 8 ? scatter_hist_kernel<8> : per == 2 ? scatter_hist_kernel<2> : scatter_hist_kernel<1>;
-        e = launch_kernel(k, grid, kScatterThreads, (size_t)nb * 8, st, true, N, (const int*)active,
-                          (const int*)path_ws, L, l, (int)t->level_offsets[l], nb, (const int*)offsets, cursor, perm);
-      }
       else
         e = launch_kernel(scatter_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
                           (const int*)path_ws, L, l, (int)t->level_offsets[l], (const int*)offsets, cursor,
@@ -718,7 +784,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       s.child_count = t->child_count; s.path_ws = path_ws; s.path_out = path; s.count = count;
       s.K = K; s.L = L; s.ip = ip; s.leaf_atom = t->leaf_atom;
       if (l + 1 < L) {
-        s.next_counts = counts + bin_off[l + 1];
+        s.next_counts = counts_of(it) + bin_off[l + 1];
         s.next_base = (int)t->level_offsets[l + 1];
       } else {
         s.leaf_sel = leaf_sel;
@@ -756,7 +822,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       ta.root_npad = t->staged_levels[0].npad;
       ta.root_cc = t->root_children;
       ta.root_cb = (int)t->level_offsets[1];
-      ta.next_counts = counts + bin_off[1];
+      ta.next_counts = counts_of(it + 1) + bin_off[1];
       ta.next_base = (int)t->level_offsets[1];
       ta.path_ws = path_ws;
       ta.L = L;

@@ -50,15 +50,34 @@ __host__ __device__ inline TsLayout ts_layout(int kch, int npad, bool last) {
 template <int KCH>
 __device__ __forceinline__ void gather_rows(const ScoreArgs& a, const int* rows_ids, int rows, uint32_t raw_s,
                                             int tid) {
-  constexpr int F = 8 * KCH;
+  constexpr int F = 8 * KCH;   // 16-byte chunks per residual row
+  if constexpr ((kThreads % F) == 0) {
+    // each thread keeps one chunk column c and walks rows r0, r0 + RS, ...: the
+    // source offset, the swizzled destination and the row stride are loop
+    // invariants, so a chunk costs one row-id load, one wide multiply-add and
+    // the copy (16 consecutive threads still cover a whole 256-byte row)
+    constexpr int RS = kThreads / F;
+    const int c = tid % F;
+    const int r0 = tid / F;
+    const char* base = reinterpret_cast<const char*>(a.R) + 16 * c;
+    const int ldb = a.ld * 4;
+#pragma unroll
+    for (int k = 0; k < kT / RS; ++k) {
+      const int row = r0 + k * RS;
+      const int rid = rows_ids[row];   // -1 past the tile's rows and for skipped patches
+      const uint32_t off = (uint32_t)(c >> 3) * (kT * 128u) + sw128_offset(row, c & 7);
+      cp_async16_row(raw_s + off, base + (int64_t)rid * ldb, rid);
+    }
+  } else {
 #pragma unroll 4
-  for (int e = tid; e < kT * F; e += kThreads) {
-    const int row = e / F;
-    const int c = e - row * F;
-    const uint32_t off = (uint32_t)(c >> 3) * (kT * 128u) + sw128_offset(row, c & 7);
-    const int rid = row < rows ? rows_ids[row] : -1;
-    const bool ok = rid >= 0;
-    cp_async16(raw_s + off, a.R + (ok ? (int64_t)rid * a.ld + 4 * c : 0), ok ? 16u : 0u);
+    for (int e = tid; e < kT * F; e += kThreads) {
+      const int row = e / F;
+      const int c = e - row * F;
+      const uint32_t off = (uint32_t)(c >> 3) * (kT * 128u) + sw128_offset(row, c & 7);
+      const int rid = row < rows ? rows_ids[row] : -1;
+      const bool ok = rid >= 0;
+      cp_async16(raw_s + off, a.R + (ok ? (int64_t)rid * a.ld + 4 * c : 0), ok ? 16u : 0u);
+    }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -136,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
 
   int4 it = i0 < i1 ? item_at(a, i0) : make_int4(0, 0, 0, 0);
   if (i0 < i1) {
-    if (tid < it.z) s_rows[tid] = row_at(a, it, tid);
+    s_rows[tid] = tid < it.z ? row_at(a, it, tid) : -1;   // kThreads == kT: every slot written
     if (tid == 0) {
       mbar_arrive_expect_tx(&bars[0], tb);
       const uint8_t* src = reinterpret_cast<const uint8_t*>(a.table) + (size_t)it.x * tb;
@@ -195,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
       __syncthreads();
       if (kc == KCH - 1 && has_next) {
         // every row is in TMEM: the landing plane and the rows buffer are free
-        if (tid < nit.z) s_rows[(buf ^ 1) * kT + tid] = nperm;
+        s_rows[(buf ^ 1) * kT + tid] = tid < nit.z ? nperm : -1;
       }
       if (tid == 0) {
         if (kc == 0 && table_pending) {

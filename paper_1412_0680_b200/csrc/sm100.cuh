@@ -109,6 +109,14 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
                : "memory");
 }
 
+// 16-byte copy of row `rid` (byte address `src`) only when rid >= 0: nothing
+// is written for a skipped row (its slot keeps stale data whose results are
+// discarded).
+__device__ __forceinline__ void cp_async16_row(uint32_t dst, const void* src, int rid) {
+  asm volatile("{\n .reg .pred p;\n setp.ge.s32 p, %2, 0;\n @p cp.async.cg.shared.global [%0], [%1], 16;\n}"
+               ::"r"(dst), "l"(src), "r"(rid) : "memory");
+}
+
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
