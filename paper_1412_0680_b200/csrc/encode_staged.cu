@@ -690,7 +690,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   // lockstep OMP update (update_omp8_kernel): K <= 8 with rows of <= 160 floats or K <= 16 with <= 128; the
   // atom Gram table when the dictionary is small enough, dot products otherwise
   const bool lockstep = method == kMethodOMP && lockstep_lanes(d->ld, K) != 0 && g_update_omp8;
-  u.gram = lockstep && g_gram ? ensure_gram(const_cast<DictHandle*>(d), st) : nullptr;
+  u.gram = lockstep && g_gram && K <= 8 ? ensure_gram(const_cast<DictHandle*>(d), st) : nullptr;
   u.m = d->m;
   // stage the support atoms in shared memory when the patch groups fit comfortably
   u.cache_atoms = update_smem_bytes(uc, K, d->ld, true) <= 96 * 1024 ? 1 : 0;

@@ -369,11 +369,28 @@ __device__ __forceinline__ float group_reduce_scatter(float (&p)[G], int gl) {
 template <int G>
 __device__ __forceinline__ float group_bcast(float v, int k) { return __shfl_sync(kFull, v, k, G); }
 
+// Reduce-scatter of NR * G values over the G lanes of a group: on return r[i]
+// on lane gl holds the group sum of p[gl + G * i].
+template <int G, int NR>
+__device__ __forceinline__ void group_reduce_scatter_n(float (&p)[NR * G], int gl, float (&r)[NR]) {
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    float q[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k) q[k] = p[G * i + k];
+    r[i] = group_reduce_scatter<G>(q, gl);
+  }
+}
+
+// Lane gl owns rows gl + G * i (i < NR) of the inverse Cholesky factor M (and the
+// matching y_j, c_j): NR = 1 while the support fits the group, 2 up to 2G atoms.
 template <int G, int CPL, int T, bool GRAM>
-__global__ void __launch_bounds__(128, G == 8 ? (CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : STMP_OMP8_MINB) : 5) : 6)
+__global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T < G ? STMP_OMP8_MINB : 5)) : 5)
     update_omp8_kernel(UpdateArgs a) {
   constexpr bool kSupSmem = sup_smem<T, GRAM>();
-  static_assert(T < G, "lockstep support index must fit the patch group");
+  constexpr int NR = T < G ? 1 : 2;     // Cholesky rows per lane
+  constexpr int NV = NR * G;            // reduce-scatter width
+  static_assert(T < 2 * G, "lockstep support index must fit two rows per lane");
   pdl_enter();
   const int64_t N = a.N;
   const int64_t p = (int64_t)blockIdx.x * (128 / G) + threadIdx.x / G;
@@ -399,13 +416,17 @@ __global__ void __launch_bounds__(128, G == 8 ? (CPL <= 2 ? (T == 0 ? STMP_OMP8_
   int S[T + 1];
 #pragma unroll
   for (int k = 0; k < T; ++k) S[k] = sm100::ld_now(a.S_ws + k * N + pc);
-  const bool row_live = gl < T;
-  const float cj = row_live ? sm100::ld_now(a.c_ws + gl * N + pc) : 0.f;
-  const float yj = row_live ? sm100::ld_now(a.yv + gl * N + pc) : 0.f;
-  float mrow[T + 1];
-  const float* Mrow = a.Lf + (int64_t)(gl * (gl + 1) / 2) * N + pc;
+  float cj[NR], yj[NR], mrow[NR][T + 1];
 #pragma unroll
-  for (int k = 0; k < T; ++k) mrow[k] = (row_live && k <= gl) ? sm100::ld_now(Mrow + k * N) : 0.f;
+  for (int i = 0; i < NR; ++i) {
+    const int j = gl + G * i;
+    const bool live = j < T;
+    cj[i] = live ? sm100::ld_now(a.c_ws + j * N + pc) : 0.f;
+    yj[i] = live ? sm100::ld_now(a.yv + j * N + pc) : 0.f;
+    const float* Mrow = a.Lf + (int64_t)(j * (j + 1) / 2) * N + pc;
+#pragma unroll
+    for (int k = 0; k < T; ++k) mrow[i][k] = (live && k <= j) ? sm100::ld_now(Mrow + k * N) : 0.f;
+  }
   const bool act = act_in != 0;
   if (!__any_sync(kFull, act)) return;   // warp-uniform: nothing to do, nothing to count
   // inactive patches run along on valid (atom 0) addresses; nothing of theirs is stored
@@ -462,10 +483,10 @@ __global__ void __launch_bounds__(128, G == 8 ? (CPL <= 2 ? (T == 0 ? STMP_OMP8_
     gtt = __ldg(grow + atom);
     bt = gsum_full<G>(av.dot(x));
   } else {
-    // value k < T: a . a_{S_k};  T: a . a;  T + 1: a . x (if it fits the group)
-    float pv[G];
+    // value k < T: a . a_{S_k};  T: a . a;  T + 1: a . x (if it fits)
+    float pv[NV];
 #pragma unroll
-    for (int k = 0; k < G; ++k) pv[k] = 0.f;
+    for (int k = 0; k < NV; ++k) pv[k] = 0.f;
 #pragma unroll
     for (int k = 0; k < T; ++k) {
       Sl sv;
@@ -473,25 +494,34 @@ __global__ void __launch_bounds__(128, G == 8 ? (CPL <= 2 ? (T == 0 ? STMP_OMP8_
       pv[k] = sv.dot(av);
     }
     pv[T] = av.dot(av);
-    constexpr bool kBtInRs = T + 1 < G;
-    float bt_part = av.dot(x);
+    constexpr bool kBtInRs = T + 1 < NV;
+    const float bt_part = av.dot(x);
     if constexpr (kBtInRs) pv[T + 1] = bt_part;
-    const float mine = group_reduce_scatter<G>(pv, gl);
+    float mine[NR];
+    group_reduce_scatter_n<G, NR>(pv, gl, mine);
 #pragma unroll
-    for (int k = 0; k < T; ++k) g[k] = group_bcast<G>(mine, k);
-    gtt = group_bcast<G>(mine, T);
-    if constexpr (kBtInRs) bt = group_bcast<G>(mine, T + 1);
+    for (int k = 0; k < T; ++k) g[k] = group_bcast<G>(mine[k / G], k % G);
+    gtt = group_bcast<G>(mine[T / G], T % G);
+    if constexpr (kBtInRs) bt = group_bcast<G>(mine[(T + 1) / G], (T + 1) % G);
     else bt = gsum_full<G>(bt_part);
   }
-  // a . (A_S c_prev), lane k holding c_prev_k:  the a . r of pursuit.py:217
-  float gmine = 0.f;   // g[gl] without dynamic indexing
+  // w = M g (lane: its rows); one butterfly for a.(A_S c_prev), w.w, w.y
+  float wj[NR];
+  float gc = 0.f, wsum = 0.f, wy = 0.f;
 #pragma unroll
-  for (int k = 0; k < T; ++k) gmine = k == gl ? g[k] : gmine;
-  // w = M g (lane j: row j); one butterfly for a.(A_S c_prev), w.w, w.y
-  float wj = 0.f;
+  for (int i = 0; i < NR; ++i) {
+    float gm = 0.f;   // g[gl + G i] without dynamic indexing
+    float w = 0.f;
 #pragma unroll
-  for (int k = 0; k < T; ++k) wj = fmaf(mrow[k], g[k], wj);
-  float gc = gmine * cj, wsum = wj * wj, wy = wj * yj;
+    for (int k = 0; k < T; ++k) {
+      gm = k == gl + G * i ? g[k] : gm;
+      w = fmaf(mrow[i][k], g[k], w);
+    }
+    wj[i] = w;
+    gc = fmaf(gm, cj[i], gc);
+    wsum = fmaf(w, w, wsum);
+    wy = fmaf(w, yj[i], wy);
+  }
 #pragma unroll
   for (int o = G >> 1; o; o >>= 1) {
     gc += __shfl_xor_sync(kFull, gc, o);
@@ -503,19 +533,32 @@ __global__ void __launch_bounds__(128, G == 8 ? (CPL <= 2 ? (T == 0 ? STMP_OMP8_
   const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
   const float inv_d = 1.f / dg;
   const float yy = (bt - wy) * inv_d;
-  // column sums colw_k = sum_j w_j M[j][k]: lane k receives its own column
-  float pc_[G];
+  // column sums colw_k = sum_j w_j M[j][k]: lane gl receives columns gl + G i
+  float pcol[NV];
 #pragma unroll
-  for (int k = 0; k < G; ++k) pc_[k] = k < T ? wj * mrow[k < T ? k : 0] : 0.f;
-  const float colw = group_reduce_scatter<G>(pc_, gl);
+  for (int k = 0; k < NV; ++k) {
+    float v = 0.f;
+    if (k < T) {
+#pragma unroll
+      for (int i = 0; i < NR; ++i) v = fmaf(wj[i], mrow[i][k < T ? k : 0], v);
+    }
+    pcol[k] = v;
+  }
+  float colw[NR];
+  group_reduce_scatter_n<G, NR>(pcol, gl, colw);
   // new row T of M: (-(1/d) w^T M, 1/d);  c_new = c_prev + m_T y_T
-  const float mt_mine = gl < T ? -inv_d * colw : (gl == T ? inv_d : 0.f);
-  const float c_new = gl < T ? fmaf(mt_mine, yy, cj) : (gl == T ? inv_d * yy : 0.f);
+  float mt[NR], cn[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    const int j = gl + G * i;
+    mt[i] = j < T ? -inv_d * colw[i] : (j == T ? inv_d : 0.f);
+    cn[i] = j < T ? fmaf(mt[i], yy, cj[i]) : (j == T ? inv_d * yy : 0.f);
+  }
   S[T] = atom;
   bool act_next = false;
   float c[T + 1];
 #pragma unroll
-  for (int k = 0; k <= T; ++k) c[k] = group_bcast<G>(ok ? c_new : cj, k);
+  for (int k = 0; k <= T; ++k) c[k] = group_bcast<G>(ok ? cn[k / G] : cj[k / G], k % G);
   if (__any_sync(kFull, ok)) {
     // residual r = x - A_S c (support rows from L1 / L2 / shared memory) - c_T a
     Sl r;
@@ -544,9 +587,13 @@ __global__ void __launch_bounds__(128, G == 8 ? (CPL <= 2 ? (T == 0 ? STMP_OMP8_
       r.store(a.R + p * a.ld, gl, F);
       act_next = (T + 1 < K) && rn > a.tol[p];
       if (act_next) {
-        if (gl <= T) {
-          a.Lf[(int64_t)(T * (T + 1) / 2 + gl) * N + p] = mt_mine;
-          a.c_ws[gl * N + p] = c_new;
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+          const int j = gl + G * i;
+          if (j <= T) {
+            a.Lf[(int64_t)(T * (T + 1) / 2 + j) * N + p] = mt[i];
+            a.c_ws[j * N + p] = cn[i];
+          }
         }
         if (gl == 0) {
           a.yv[T * N + p] = yy;
@@ -564,12 +611,16 @@ __global__ void __launch_bounds__(128, G == 8 ? (CPL <= 2 ? (T == 0 ? STMP_OMP8_
   if (act && !act_next) {
     // final rows of the caller's idx / coef (T or T + 1 entries; the rest stay -1 / 0 from init)
     const int n_out = ok ? T + 1 : T;
-    if (gl < n_out) {
-      int s_mine = S[0];
 #pragma unroll
-      for (int k = 1; k <= T; ++k) s_mine = k == gl ? S[k] : s_mine;
-      a.idx[p * K + gl] = s_mine;
-      a.coef[p * K + gl] = ok ? c_new : cj;
+    for (int i = 0; i < NR; ++i) {
+      const int j = gl + G * i;
+      if (j < n_out) {
+        int s_mine = S[0];
+#pragma unroll
+        for (int k = 1; k <= T; ++k) s_mine = k == j ? S[k] : s_mine;
+        a.idx[p * K + j] = s_mine;
+        a.coef[p * K + j] = ok ? cn[i] : cj[i];
+      }
     }
   }
   if (act && gl == 0) a.active[p] = act_next ? 1 : 0;
@@ -579,8 +630,9 @@ __global__ void __launch_bounds__(128, G == 8 ? (CPL <= 2 ? (T == 0 ? STMP_OMP8_
 }  // namespace
 
 int lockstep_lanes(int ld, int K) {
+  // 8 lanes per patch; each lane owns one Cholesky row up to 8 atoms, two up to 16
   if (K <= 8 && ld <= 160) return 8;
-  if (K <= 16 && ld <= 128) return 16;
+  if (K <= 16 && ld <= 64) return 8;
   return 0;
 }
 
@@ -606,13 +658,13 @@ cudaError_t launch_update_omp8(const UpdateArgs& a, cudaStream_t st) {
   STMP_OMP8_CASE(g, cp, 3, gr) STMP_OMP8_CASE(g, cp, 4, gr) STMP_OMP8_CASE(g, cp, 5, gr)               \
   STMP_OMP8_CASE(g, cp, 6, gr) STMP_OMP8_CASE(g, cp, 7, gr)
 #define STMP_OMP16_ITERS(cp, gr)                                                                        \
-  STMP_OMP8_ITERS(16, cp, gr) STMP_OMP8_CASE(16, cp, 8, gr) STMP_OMP8_CASE(16, cp, 9, gr)              \
-  STMP_OMP8_CASE(16, cp, 10, gr) STMP_OMP8_CASE(16, cp, 11, gr) STMP_OMP8_CASE(16, cp, 12, gr)         \
-  STMP_OMP8_CASE(16, cp, 13, gr) STMP_OMP8_CASE(16, cp, 14, gr) STMP_OMP8_CASE(16, cp, 15, gr)
+  STMP_OMP8_CASE(8, cp, 8, gr) STMP_OMP8_CASE(8, cp, 9, gr) STMP_OMP8_CASE(8, cp, 10, gr)                   \
+  STMP_OMP8_CASE(8, cp, 11, gr) STMP_OMP8_CASE(8, cp, 12, gr) STMP_OMP8_CASE(8, cp, 13, gr)                 \
+  STMP_OMP8_CASE(8, cp, 14, gr) STMP_OMP8_CASE(8, cp, 15, gr)
     STMP_OMP8_ITERS(8, 1, 1) STMP_OMP8_ITERS(8, 2, 1) STMP_OMP8_ITERS(8, 3, 1) STMP_OMP8_ITERS(8, 4, 1)
     STMP_OMP8_ITERS(8, 5, 1) STMP_OMP8_ITERS(8, 1, 0) STMP_OMP8_ITERS(8, 2, 0) STMP_OMP8_ITERS(8, 3, 0)
     STMP_OMP8_ITERS(8, 4, 0) STMP_OMP8_ITERS(8, 5, 0)
-    STMP_OMP16_ITERS(1, 1) STMP_OMP16_ITERS(2, 1) STMP_OMP16_ITERS(1, 0) STMP_OMP16_ITERS(2, 0)
+    STMP_OMP16_ITERS(1, 0) STMP_OMP16_ITERS(2, 0)
 #undef STMP_OMP16_ITERS
 #undef STMP_OMP8_ITERS
 #undef STMP_OMP8_CASE
