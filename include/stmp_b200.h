@@ -112,12 +112,34 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
                      int32_t* idx, float* coef, int32_t* count, float* resnorm, int32_t* ip,
                      int64_t chunk);
 
+/* Batch driver around the encoder: the per-patch arithmetic
+ * of pipelines._code_patches (pkg/src/stmp/pipelines.py:180-217) on the device.
+ *
+ * stmp_dc_split replaces pipelines.py:201-203: for each measured patch
+ * y = Y[p] (f32, device, row stride ldy), dc[p] = (y . dc_meas) / denom (f64,
+ * denom = dc_meas . dc_meas) and Yc[p] = f32(y - dc[p] * dc_meas), the input
+ * the encoder codes.  dc_meas is a device f64 [n] vector.                     */
+int stmp_dc_split(const float* Y, int64_t N, int64_t ldy, int32_t n, const double* dc_meas, double denom,
+                  float* Yc, int64_t ldc, double* dc, void* stream);
+
+/* stmp_reconstruct replaces lift_code (pkg/src/stmp/operators.py:199-215),
+ * reconstruct (pkg/src/stmp/pursuit.py:224-232) and "+ dc"
+ * (pipelines.py:204): out[p] = sum_{k < count[p]} (coef[p,k] / scale[idx[p,k]])
+ * * base_atom[idx[p,k]] + dc[p], in f64, entries in selection order, with the
+ * multiply and the add rounded separately as in NumPy.  `base` holds the
+ * full-space atoms (ProjectedDictionary.base); scale (device f64 [m]) and dc
+ * (device f64 [N]) may be NULL for 1 and 0.  Unusable atoms must be rejected
+ * by the caller before (lift_code raises RuntimeError, operators.py:209-213). */
+int stmp_reconstruct(const stmp_dict* base, const int32_t* idx, const float* coef, const int32_t* count, int64_t N,
+                     int32_t K, const double* scale, const double* dc, double* out, int64_t ldo, void* stream);
+
 /* Process-wide tuning knobs (no reference counterpart):
  *   "path": 0 auto (default), 1 fused warp-per-patch kernel, 2 staged tensor-core pipeline;
  *   "staged_min_batch": batch size from which `auto` picks the staged pipeline;
  *   "score_kernel": staged score pass 0 single-role, 1 warp-specialised, 2 TMEM A operand (default),
  *                   3 streamed table (always used for nodes whose table exceeds shared memory);
- *   "update_kernel": staged update 0 generic, 1 Gram-table K<=8 (default), 2 tile + fused root;
+ *   "update_kernel": staged update 0 generic, 1 lockstep OMP (default), 2 tile + fused root;
+ *   "gram": 1 lockstep update reads the atom Gram table (m <= 32768, K <= 8), 0 support-row dots (default);
  *   "pdl": 1 (default) launch the staged kernels with programmatic dependent launch, 0 plain;
  *   "score_tma": 1 gather the score pass's rows with TMA tile::gather4, 0 per-thread cp.async (default);
  *   "graphs": 1 (default) replay repeated staged encodes (same buffers, sizes, stream) as CUDA graphs. */

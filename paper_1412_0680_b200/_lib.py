@@ -44,6 +44,10 @@ EXPORTS = {
     "stmp_stream_sync": (C.c_int, [C.c_void_p]),
     "stmp_set_option": (C.c_int, [C.c_char_p, C.c_int64]),
     "stmp_kernel_launches": (C.c_int, [C.c_void_p]),
+    "stmp_dc_split": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.c_double,
+                                C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "stmp_reconstruct": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
 }
 
 PATH_AUTO, PATH_FUSED, PATH_STAGED = 0, 1, 2

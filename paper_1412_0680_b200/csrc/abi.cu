@@ -562,4 +562,35 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
   return rc;
 }
 
+int stmp_dc_split(const float* Y, int64_t N, int64_t ldy, int32_t n, const double* dc_meas, double denom,
+                  float* Yc, int64_t ldc, double* dc, void* stream) {
+  g_err.clear();
+  if (N < 0) return fail(STMP_EINVAL, "patch count must be non-negative, got %lld", (long long)N);
+  if (n < 1) return fail(STMP_EINVAL, "measurement dimension must be positive, got %d", n);
+  if (ldy < n || ldc < n) return fail(STMP_EINVAL, "row stride below the measurement dimension %d", n);
+  if (!(denom > 0.0)) return fail(STMP_EINVAL, "dc_meas . dc_meas must be positive, got %g", denom);
+  if (N > 0 && (Y == nullptr || dc_meas == nullptr || Yc == nullptr || dc == nullptr))
+    return fail(STMP_EINVAL, "NULL buffer");
+  if (int rc = check_device()) return rc;
+  cudaError_t e = stmp::launch_dc_split(Y, N, ldy, n, dc_meas, denom, Yc, ldc, dc, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "dc_split");
+  return STMP_OK;
+}
+
+int stmp_reconstruct(const stmp_dict* base, const int32_t* idx, const float* coef, const int32_t* count, int64_t N,
+                     int32_t K, const double* scale, const double* dc, double* out, int64_t ldo, void* stream) {
+  g_err.clear();
+  if (base == nullptr) return fail(STMP_EINVAL, "dictionary handle is NULL");
+  if (N < 0) return fail(STMP_EINVAL, "patch count must be non-negative, got %lld", (long long)N);
+  if (K < 1) return fail(STMP_EINVAL, "sparsity K must be at least 1, got %d", K);
+  if (ldo < base->n) return fail(STMP_EINVAL, "output row stride below the atom dimension %d", base->n);
+  if (N > 0 && (idx == nullptr || coef == nullptr || count == nullptr || out == nullptr))
+    return fail(STMP_EINVAL, "NULL buffer");
+  if (int rc = check_device()) return rc;
+  cudaError_t e = stmp::launch_reconstruct(base, idx, coef, count, N, K, scale, dc, out, ldo,
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "reconstruct");
+  return STMP_OK;
+}
+
 }  // extern "C"

@@ -36,6 +36,13 @@ struct FusedArgs {
 };
 
 int fused_vpl_for(int n);
+
+// batch driver (driver.cu): DC split before the encoder, lift + reconstruct after it
+cudaError_t launch_dc_split(const float* Y, int64_t N, int64_t ldy, int n, const double* dc_meas, double denom,
+                            float* Yc, int64_t ldc, double* dc, cudaStream_t st);
+cudaError_t launch_reconstruct(const DictHandle* d, const int32_t* idx, const float* coef, const int32_t* count,
+                               int64_t N, int K, const double* scale, const double* dc, double* out, int64_t ldo,
+                               cudaStream_t st);
 cudaError_t launch_encode_fused(const FusedArgs& a, cudaStream_t stream);
 
 }  // namespace stmp
