@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T
   const int64_t p = (int64_t)blockIdx.x * (128 / G) + threadIdx.x / G;
   const int gl = threadIdx.x % G;
   const int K = a.K;
-  const int F = a.ld >> 2;
+  constexpr int F = G * CPL;   // 16-byte chunks per row: ld is a multiple of 32, so F == G * CPL exactly
   using Sl = Slice<G, CPL>;
   const bool inb = p < N;
   const int64_t pc = inb ? p : 0;
