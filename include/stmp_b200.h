@@ -133,6 +133,39 @@ int stmp_dc_split(const float* Y, int64_t N, int64_t ldy, int32_t n, const doubl
 int stmp_reconstruct(const stmp_dict* base, const int32_t* idx, const float* coef, const int32_t* count, int64_t N,
                      int32_t K, const double* scale, const double* dc, double* out, int64_t ldo, void* stream);
 
+/* Data formats either side of the path.  Device buffers;
+ * the geometry arrays (rank entries) are HOST arrays, the window starts a
+ * DEVICE int64 array: axis 0's nstarts[0] starts, then axis 1's, ...
+ * (PatchLayout.axis_starts, pkg/src/stmp/tensor.py:49-99).
+ *
+ * stmp_extract_patches replaces extract_patches (tensor.py:104-111): row p of
+ * out[N x n] is window p of the row-major f32 tensor t, windows in row-major
+ * origin order, values in row-major window order; bit-exact.
+ * stmp_aggregate_patches replaces aggregate_patches (tensor.py:114-136): each
+ * cell of out (f32, tensor shape) is the f64 mean of every covering patch
+ * value, summed in origin order -- bitwise the reference's result.           */
+int stmp_extract_patches(const float* t, int32_t rank, const int64_t* shape, const int64_t* patch,
+                         const int64_t* nstarts, const int64_t* starts, float* out, void* stream);
+int stmp_aggregate_patches(const float* patches, int32_t rank, const int64_t* shape, const int64_t* patch,
+                           const int64_t* nstarts, const int64_t* starts, float* out, void* stream);
+
+/* stmp_apply_operator replaces apply_batch (pkg/src/stmp/operators.py:115-141)
+ * for N f32 rows X[N x n_in] -> f64 rows Y[N x n_out]:
+ *   STMP_OP_ROW_SELECT      rows (device int64 [n_rows]) kept, in order;
+ *   STMP_OP_CODED_EXPOSURE  mask (device f32 [pixels x frames], binary): the
+ *                           patch is (pixels, windows, frames) row-major and
+ *                           each output sums its frames times the pixel's mask;
+ *   STMP_OP_BLOCK_AVERAGE   in_shape / factors (host int64 [rank]): the mean
+ *                           of each factor block.
+ * (IDENTITY is a copy and needs no kernel.)  f64 arithmetic; sums in index
+ * order, so results equal NumPy's pairwise sums to rounding (1e-15 relative). */
+#define STMP_OP_ROW_SELECT 1
+#define STMP_OP_CODED_EXPOSURE 2
+#define STMP_OP_BLOCK_AVERAGE 3
+int stmp_apply_operator(int32_t kind, const float* X, int64_t N, int32_t n_in, const int64_t* rows, int32_t n_rows,
+                        const float* mask, int32_t pixels, int32_t windows, int32_t frames, int32_t rank,
+                        const int64_t* in_shape, const int64_t* factors, double* Y, void* stream);
+
 /* Process-wide tuning knobs (no reference counterpart):
  *   "path": 0 auto (default), 1 fused warp-per-patch kernel, 2 staged tensor-core pipeline;
  *   "staged_min_batch": batch size from which `auto` picks the staged pipeline;

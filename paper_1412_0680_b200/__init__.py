@@ -27,6 +27,7 @@ from .pursuit import (
     retained_count,
     stmp_select,
 )
+from .patches import PatchLayout, aggregate_patches, apply_batch, extract_patches
 from .pipelines import code_patches
 from .tree import FlatTree, from_reference_tree, load_structure, read_tree_file, write_tree_file
 
@@ -35,5 +36,5 @@ __all__ = [
     "GpuDictionary", "GpuTree", "ScoreCounter", "SearchParams", "SparseCode", "TreeSelector",
     "encode", "encode_host", "exact_select", "fingerprint_atoms", "matching_pursuit",
     "orthogonal_matching_pursuit", "predicted_ip_count", "retained_count", "stmp_select",
-    "code_patches", "FlatTree", "from_reference_tree", "load_structure", "read_tree_file", "write_tree_file",
+    "code_patches", "PatchLayout", "aggregate_patches", "apply_batch", "extract_patches", "FlatTree", "from_reference_tree", "load_structure", "read_tree_file", "write_tree_file",
 ]

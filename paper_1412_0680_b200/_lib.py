@@ -48,9 +48,17 @@ EXPORTS = {
                                 C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "stmp_reconstruct": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "stmp_extract_patches": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p]),
+    "stmp_aggregate_patches": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_void_p]),
+    "stmp_apply_operator": (C.c_int, [C.c_int32, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32,
+                                      C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 
 PATH_AUTO, PATH_FUSED, PATH_STAGED = 0, 1, 2
+OP_ROW_SELECT, OP_CODED_EXPOSURE, OP_BLOCK_AVERAGE = 1, 2, 3
 
 
 def set_option(key: str, value: int) -> None:

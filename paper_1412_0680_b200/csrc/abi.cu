@@ -593,4 +593,84 @@ int stmp_reconstruct(const stmp_dict* base, const int32_t* idx, const float* coe
   return STMP_OK;
 }
 
+static int check_geometry(int32_t rank, const int64_t* shape, const int64_t* patch, const int64_t* nstarts) {
+  if (rank < 1 || rank > stmp::kMaxRank) return fail(STMP_EINVAL, "rank must lie in [1, %d], got %d", stmp::kMaxRank, rank);
+  if (shape == nullptr || patch == nullptr || nstarts == nullptr) return fail(STMP_EINVAL, "NULL geometry array");
+  for (int a = 0; a < rank; ++a) {
+    if (shape[a] < 1 || patch[a] < 1 || nstarts[a] < 1)
+      return fail(STMP_EINVAL, "non-positive extent on axis %d", a);
+    if (patch[a] > shape[a])
+      return fail(STMP_EINVAL, "patch extent %lld exceeds tensor extent %lld on axis %d", (long long)patch[a],
+                  (long long)shape[a], a);
+  }
+  return STMP_OK;
+}
+
+int stmp_extract_patches(const float* t, int32_t rank, const int64_t* shape, const int64_t* patch,
+                         const int64_t* nstarts, const int64_t* starts, float* out, void* stream) {
+  g_err.clear();
+  if (int rc = check_geometry(rank, shape, patch, nstarts)) return rc;
+  if (t == nullptr || starts == nullptr || out == nullptr) return fail(STMP_EINVAL, "NULL buffer");
+  if (int rc = check_device()) return rc;
+  cudaError_t e = stmp::launch_extract(t, rank, shape, patch, nstarts, starts, out, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "extract_patches");
+  return STMP_OK;
+}
+
+int stmp_aggregate_patches(const float* patches, int32_t rank, const int64_t* shape, const int64_t* patch,
+                           const int64_t* nstarts, const int64_t* starts, float* out, void* stream) {
+  g_err.clear();
+  if (int rc = check_geometry(rank, shape, patch, nstarts)) return rc;
+  if (patches == nullptr || starts == nullptr || out == nullptr) return fail(STMP_EINVAL, "NULL buffer");
+  if (int rc = check_device()) return rc;
+  cudaError_t e = stmp::launch_aggregate(patches, rank, shape, patch, nstarts, starts, out,
+                                         static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "aggregate_patches");
+  return STMP_OK;
+}
+
+int stmp_apply_operator(int32_t kind, const float* X, int64_t N, int32_t n_in, const int64_t* rows, int32_t n_rows,
+                        const float* mask, int32_t pixels, int32_t windows, int32_t frames, int32_t rank,
+                        const int64_t* in_shape, const int64_t* factors, double* Y, void* stream) {
+  g_err.clear();
+  if (N < 0) return fail(STMP_EINVAL, "patch count must be non-negative, got %lld", (long long)N);
+  if (n_in < 1) return fail(STMP_EINVAL, "operator input dimension must be positive, got %d", n_in);
+  if (N > 0 && (X == nullptr || Y == nullptr)) return fail(STMP_EINVAL, "NULL buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  switch (kind) {
+    case STMP_OP_ROW_SELECT:
+      if (rows == nullptr || n_rows < 1) return fail(STMP_EINVAL, "row selection keeps no coordinates");
+      if (int rc = check_device()) return rc;
+      e = stmp::launch_row_select(X, N, n_in, rows, n_rows, Y, st);
+      break;
+    case STMP_OP_CODED_EXPOSURE:
+      if (mask == nullptr || pixels < 1 || windows < 1 || frames < 1 ||
+          (int64_t)pixels * windows * frames != n_in)
+        return fail(STMP_EINVAL, "coded exposure geometry %d x %d x %d does not match dimension %d", pixels, windows,
+                    frames, n_in);
+      if (int rc = check_device()) return rc;
+      e = stmp::launch_coded_exposure(X, N, n_in, mask, pixels, windows, frames, Y, st);
+      break;
+    case STMP_OP_BLOCK_AVERAGE: {
+      if (rank < 1 || rank > stmp::kMaxRank || in_shape == nullptr || factors == nullptr)
+        return fail(STMP_EINVAL, "block average needs 1..%d axes", stmp::kMaxRank);
+      int64_t prod = 1;
+      for (int a = 0; a < rank; ++a) {
+        if (factors[a] < 1 || in_shape[a] % factors[a] != 0)
+          return fail(STMP_EINVAL, "factor %lld must divide extent %lld", (long long)factors[a], (long long)in_shape[a]);
+        prod *= in_shape[a];
+      }
+      if (prod != n_in) return fail(STMP_EINVAL, "block shape does not match dimension %d", n_in);
+      if (int rc = check_device()) return rc;
+      e = stmp::launch_block_average(X, N, rank, in_shape, factors, Y, st);
+      break;
+    }
+    default:
+      return fail(STMP_EINVAL, "unknown operator kind %d", kind);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "apply_operator");
+  return STMP_OK;
+}
+
 }  // extern "C"

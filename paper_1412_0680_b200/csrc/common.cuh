@@ -46,6 +46,7 @@ inline cudaError_t launch_kernel(void (*k)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMaxRank = 8;   // tensor / patch ranks of the data-format kernels (tensor_ops.cu)
 
 // ScoreCounter update of one patch: both int32 counters {all, centroid} in one
 // 64-bit add (the low word never carries: counts stay far below 2^32).

@@ -43,6 +43,18 @@ cudaError_t launch_dc_split(const float* Y, int64_t N, int64_t ldy, int n, const
 cudaError_t launch_reconstruct(const DictHandle* d, const int32_t* idx, const float* coef, const int32_t* count,
                                int64_t N, int K, const double* scale, const double* dc, double* out, int64_t ldo,
                                cudaStream_t st);
+
+// data formats either side of the path (tensor_ops.cu)
+cudaError_t launch_extract(const float* t, int rank, const int64_t* shape, const int64_t* patch,
+                           const int64_t* nstarts, const int64_t* starts_dev, float* out, cudaStream_t st);
+cudaError_t launch_aggregate(const float* patches, int rank, const int64_t* shape, const int64_t* patch,
+                             const int64_t* nstarts, const int64_t* starts_dev, float* out, cudaStream_t st);
+cudaError_t launch_row_select(const float* X, int64_t N, int n_in, const int64_t* rows_dev, int n_out, double* Y,
+                              cudaStream_t st);
+cudaError_t launch_coded_exposure(const float* X, int64_t N, int n_in, const float* mask_dev, int pixels,
+                                  int windows, int frames, double* Y, cudaStream_t st);
+cudaError_t launch_block_average(const float* X, int64_t N, int rank, const int64_t* in_shape,
+                                 const int64_t* factors, double* Y, cudaStream_t st);
 cudaError_t launch_encode_fused(const FusedArgs& a, cudaStream_t stream);
 
 }  // namespace stmp
