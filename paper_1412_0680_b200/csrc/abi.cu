@@ -45,7 +45,7 @@ struct GraphEntry {
   uint64_t stamp = 0;
 };
 std::mutex g_graph_mu;
-GraphEntry g_graph_cache[8];
+GraphEntry g_graph_cache[32];   // host path: 3 streams x ramped chunk sizes
 uint64_t g_graph_clock = 0;
 
 int fail(int code, const char* fmt, ...) {
@@ -535,11 +535,26 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
   const size_t wsz = stmp_encode_workspace(d, t, chunk, K, method);
   for (int i = 0; i < kHostStreams; ++i)
     if (int rc = ensure_stage(g_host[i], chunk, d->n, K, wsz)) return rc;
+  // Chunk schedule: ramp up (chunk/4, chunk/2) so the first encode starts
+  // after a short copy, full chunks in the middle, ramp down at the end so the
+  // last encode + D2H (the part no copy overlaps) is short.
+  std::vector<int64_t> sizes;
+  if (N >= 4 * chunk && chunk >= 4096) {
+    const int64_t ramp[2] = {chunk / 4, chunk / 2};
+    int64_t mid = N - 2 * (ramp[0] + ramp[1]);
+    sizes.push_back(ramp[0]);
+    sizes.push_back(ramp[1]);
+    for (; mid > 0; mid -= chunk) sizes.push_back(std::min(chunk, mid));
+    sizes.push_back(ramp[1]);
+    sizes.push_back(ramp[0]);
+  } else {
+    for (int64_t s0 = 0; s0 < N; s0 += chunk) sizes.push_back(std::min(chunk, N - s0));
+  }
   int rc = STMP_OK;
-  int64_t ci = 0;
-  for (int64_t s0 = 0; s0 < N && rc == STMP_OK; s0 += chunk, ++ci) {
+  int64_t s0 = 0;
+  for (size_t ci = 0; ci < sizes.size() && rc == STMP_OK; s0 += sizes[ci], ++ci) {
     HostStage& h = g_host[ci % kHostStreams];
-    const int64_t rows = std::min(chunk, N - s0);
+    const int64_t rows = sizes[ci];
     cudaError_t e = ldx == d->n
         ? cudaMemcpyAsync(h.dX, X + s0 * ldx, rows * d->n * sizeof(float), cudaMemcpyHostToDevice, h.st)
         : cudaMemcpy2DAsync(h.dX, d->n * sizeof(float), X + s0 * ldx, ldx * sizeof(float),
