@@ -743,6 +743,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       s.table = xtable; s.npad = xtable_block_width(d->ld); s.kchunks = d->ld / 32;
       s.nblocks = (int)((d->m + s.npad - 1) / s.npad); s.m_atoms = (int)d->m;
       s.leaf_sel = leaf_sel; s.ip = ip; s.K = K; s.L = 0;
+      s.ks_last = (d->n - 32 * (s.kchunks - 1) + 7) / 8;
       if ((e = launch_exact_scan(s, sms, st)) != cudaSuccess) return e;
     }
     for (int l = (tile && it > 0) ? 1 : 0; l < L; ++l) {
@@ -783,6 +784,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       s.level = l; s.level_base = (int)t->level_offsets[l]; s.child_begin = t->child_begin;
       s.child_count = t->child_count; s.path_ws = path_ws; s.path_out = path; s.count = count;
       s.K = K; s.L = L; s.ip = ip; s.leaf_atom = t->leaf_atom;
+      s.ks_last = (d->n - 32 * (s.kchunks - 1) + 7) / 8;
       if (l + 1 < L) {
         s.next_counts = counts_of(it) + bin_off[l + 1];
         s.next_base = (int)t->level_offsets[l + 1];

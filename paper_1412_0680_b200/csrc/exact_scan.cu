@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
           const uint32_t ah = tmem + (uint32_t)ab * 64u + ks * 8;
           const uint32_t al = ah + 32;
           const uint32_t o = ks * 32u;
+          if (c == kch - 1 && ks >= a.ks_last) break;   // zero padding on both operands
           mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bh + o), idesc, (c | ks) ? 1u : 0u);
           mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bl + o), idesc, 1u);
           mma_tf32_ts(dcol, al, sw128_kmajor_desc(bh + o), idesc, 1u);

@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
           const uint32_t ah = tmem + kColA + ks * 8;
           const uint32_t al = ah + 32;
           const uint32_t o = ks * 32u;
+          if (kc == KCH - 1 && ks >= a.ks_last) break;   // zero padding on both operands
           mma_tf32_ts(tmem + kColAcc, ah, sw128_kmajor_desc(bh + o), idesc, (kc | ks) ? 1u : 0u);
           mma_tf32_ts(tmem + kColAcc, ah, sw128_kmajor_desc(bl + o), idesc, 1u);
           mma_tf32_ts(tmem + kColAcc, al, sw128_kmajor_desc(bh + o), idesc, 1u);

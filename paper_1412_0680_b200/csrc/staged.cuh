@@ -33,6 +33,8 @@ struct ScoreArgs {
   int nblocks;           // exhaustive scan: atom blocks of npad atoms
   int m_atoms;           // exhaustive scan: dictionary size
   const int* active;     // root pass in patch order (perm == nullptr): skip inactive rows
+  int ks_last;           // 8-column k-steps holding data in the last 32-column chunk (1..4): the
+                         // rest are zero padding on both operands and their MMAs are skipped
 };
 
 // Work items of a score pass: (bin, first slot in perm, rows) from the scan, or

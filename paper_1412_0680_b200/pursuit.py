@@ -373,7 +373,7 @@ def encode_host(selector, X: np.ndarray, K: int, method: str = "omp", tol: float
     """End-to-end encode from host memory (``stmp_encode_host``): chunked H2D
     (ramped chunk sizes; 2^17 measured best on config 1: 178 M patches/s with
     pinned buffers against a 55 GB/s H2D copy floor of 217 M/s),
-    encode and D2H overlapped on two streams.  Pass pinned buffers (e.g. torch
+    encode and D2H overlapped on three streams.  Pass pinned buffers (e.g. torch
     ``pin_memory()`` tensors' numpy views) for full copy bandwidth."""
     if method not in ("mp", "omp"):
         raise ValueError(f"unknown method {method!r}")
