@@ -29,7 +29,7 @@ constexpr uint32_t kColA = 0;   // A_hi chunk: 32 columns, A_lo chunk: next 32
 constexpr uint32_t kColAcc = 64;
 
 struct TsLayout {
-  uint32_t raw, btab, rows, hist, bars, slot, total;
+  uint32_t raw, btab, rows, hist, leaf, bars, slot, total;
 };
 
 __host__ __device__ inline uint32_t align_up_u(uint32_t v, uint32_t a) { return (v + a - 1) & ~(a - 1); }
@@ -41,6 +41,7 @@ __host__ __device__ inline TsLayout ts_layout(int kch, int npad, bool last) {
   L.btab = o; o += align_up_u(table_bytes(kch, npad, last), 1024u);
   L.rows = o; o += 2 * kT * 4;
   L.hist = o; o += 256 * 4;
+  L.leaf = o; o += 2 * 256 * 4;   // last level: the tile's leaf records, copied out of the table block
   L.bars = align_up_u(o, 8); o = L.bars + 3 * 8;
   L.slot = o; o += 16;
   L.total = o + 1024;
@@ -100,8 +101,8 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
   uint8_t* raw = base + Ly.raw;
   uint8_t* btab = base + Ly.btab;
   const uint32_t tb = table_bytes(KCH, npad, last);
-  const int* s_leaf_info = reinterpret_cast<const int*>(btab + (size_t)KCH * 2 * npad * 128);
-  const int* s_leaf_cnt = s_leaf_info + npad;
+  const int* t_leaf = reinterpret_cast<const int*>(btab + (size_t)KCH * 2 * npad * 128);   // in the table block
+  int* s_leaf_info = reinterpret_cast<int*>(base + Ly.leaf);   // copy: the block is refilled early
   int* s_rows = reinterpret_cast<int*>(base + Ly.rows);
   int* s_hist = reinterpret_cast<int*>(base + Ly.hist);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + Ly.bars);
@@ -248,6 +249,24 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
     mbar_wait(&bars[1], mma_phase);
     mma_phase ^= 1u;
     tc_fence_after();
+    // the MMAs are done with the table block: copy the leaf records out and
+    // start the next tile's table load now, so it overlaps this epilogue
+    const bool reload = has_next && nit.x != loaded_bin;
+    if (reload) {
+      if (last)
+        for (int j = tid; j < 2 * npad; j += kThreads) s_leaf_info[j] = t_leaf[j];
+      fence_proxy_async_smem();   // generic reads of the block before its async refill
+      __syncthreads();
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&bars[0], tb);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.table) + (size_t)nit.x * tb;
+        for (uint32_t off = 0; off < tb; off += 65536u)
+          bulk_g2s(btab + off, src + off, min(65536u, tb - off), &bars[0]);
+      }
+      table_pending = true;
+      loaded_bin = nit.x;
+    }
+    const int* leaf_rec = reload ? s_leaf_info : t_leaf;
 
     int best = 0;
     float bestv = -1.f;
@@ -268,23 +287,10 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
     const int child = cb + best;
     int leaf_info = 0, leaf_cnt = 0;
     if (last && valid) {
-      leaf_info = s_leaf_info[best];
-      leaf_cnt = s_leaf_cnt[best];
+      leaf_info = leaf_rec[best];
+      leaf_cnt = leaf_rec[npad + best];
     }
-    // generic-proxy reads of the table block (leaf metadata) must be ordered
-    // before the async-proxy bulk copy that refills it
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (has_next && nit.x != loaded_bin) {
-      if (tid == 0) {
-        mbar_arrive_expect_tx(&bars[0], tb);
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.table) + (size_t)nit.x * tb;
-        for (uint32_t off = 0; off < tb; off += 65536u)
-          bulk_g2s(btab + off, src + off, min(65536u, tb - off), &bars[0]);
-      }
-      table_pending = true;
-      loaded_bin = nit.x;
-    }
+    __syncthreads();   // every row's leaf record read before the next tile copies records again
     if (valid) {
       a.path_ws[(int64_t)p * a.L + a.level] = child;
       if (a.path_out) a.path_out[((int64_t)p * a.K + a.count[p]) * a.L + a.level] = child;
