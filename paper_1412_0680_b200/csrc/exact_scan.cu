@@ -34,7 +34,8 @@ constexpr int kT = 128;
 constexpr int kStagers = 128;
 constexpr int kThreads = kStagers + 64;
 constexpr uint32_t kSlot = kT * 128u;
-constexpr uint32_t kColAcc = 128;   // TMEM: A buffers [0,64) and [64,128), accumulators from 128
+constexpr int kNAB = 4;                    // TMEM A buffers (64 columns: hi | lo of one K chunk)
+constexpr uint32_t kColAcc = 64u * kNAB;   // TMEM: A buffers [0, 256), accumulators from 256
 
 struct XsLayout {
   uint32_t land, btab, bars, slot, total;
@@ -45,7 +46,7 @@ __host__ __device__ inline XsLayout xs_layout(int bw, int na, int nb) {
   uint32_t o = 0;
   L.land = o; o += (uint32_t)na * kSlot;
   L.btab = o; o += (uint32_t)nb * (uint32_t)bw * 256u;
-  L.bars = o; o = L.bars + (uint32_t)(2 * nb + 8) * 8;
+  L.bars = o; o = L.bars + (uint32_t)(2 * nb + 2 * kNAB + 4) * 8;
   L.slot = o; o += 16;
   L.total = o + 1024;
   return L;
@@ -69,8 +70,8 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
   uint64_t* full = reinterpret_cast<uint64_t*>(base + Ly.bars);
   uint64_t* done = full + NB;
   uint64_t* astaged = done + NB;
-  uint64_t* aempty = astaged + 2;
-  uint64_t* accfull = aempty + 2;
+  uint64_t* aempty = astaged + kNAB;
+  uint64_t* accfull = aempty + kNAB;
   uint64_t* accempty = accfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + Ly.slot);
 
@@ -80,9 +81,11 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
       mbar_init(&full[b], 1);
       mbar_init(&done[b], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kNAB; ++b) {
       mbar_init(&astaged[b], kStagers);
       mbar_init(&aempty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&accfull[b], 1);
       mbar_init(&accempty[b], kStagers);
     }
@@ -119,11 +122,11 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
       const uint32_t b_s = smem_u32(base + Ly.btab);
       for (int g = 0; g < total; ++g) {
         const int bs = g / kch, c = g - bs * kch;   // bs: block sequence number of this CTA
-        const int ab = g & 1, s = g % NB;
+        const int ab = g % kNAB, s = g % NB;
         const int acc = nacc == 2 ? (bs & 1) : 0;
         const uint32_t dcol = tmem + kColAcc + (uint32_t)acc * (uint32_t)bw;
         if (c == 0 && bs >= nacc) mbar_wait(&accempty[acc], (uint32_t)(bs / nacc - 1) & 1u);
-        mbar_wait(&astaged[ab], (uint32_t)(g >> 1) & 1u);
+        mbar_wait(&astaged[ab], (uint32_t)(g / kNAB) & 1u);
         mbar_wait(&full[s], (uint32_t)(g / NB) & 1u);
         tc_fence_after();
         const uint32_t bh = b_s + s * bslot;
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
     for (int g = 0; g < total; ++g) {
       const int item = i0 + g / per_item, rem = g % per_item;
       const int blk = rem / kch, c = rem - blk * kch;
-      const int bs = g / kch, ab = g & 1;
+      const int bs = g / kch, ab = g % kNAB;
       if (rem == 0) {
         const int4 it = item_at(a, item);
         cur_p = tid < it.z ? row_at(a, it, tid) : -1;
@@ -206,8 +209,8 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
       }
       __syncwarp();
       issue_a(g + NA);
-      if (g >= 2) {
-        mbar_wait(&aempty[ab], (uint32_t)((g >> 1) - 1) & 1u);
+      if (g >= kNAB) {
+        mbar_wait(&aempty[ab], (uint32_t)(g / kNAB - 1) & 1u);
         tc_fence_after();
       }
       tmem_st32(tmem + lane_base + (uint32_t)ab * 64u, hi);

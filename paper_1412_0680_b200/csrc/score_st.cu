@@ -18,8 +18,8 @@
 //     tile's end a commit that hands the accumulator to the epilogue;
 //   * warp 5, table producer: one bulk copy per chunk (hi | lo planes, npad
 //     rows x 128 B each, SW128) into a ring of NB slots, refilled as soon as
-//     the MMAs of the slot's previous chunk retire, plus each tile's leaf
-//     metadata block on the last level.
+//     the MMAs of the slot's previous chunk retire (the last level's leaf
+//     records are read by the epilogue straight from the table block in L2).
 // The accumulator is double-buffered when 128 + 2 * npad TMEM columns fit, so
 // a tile's epilogue overlaps the next tile's MMAs.
 // Semantics: pkg/src/stmp/pursuit.py:134-162 (greedy level choice, first max of
@@ -39,10 +39,11 @@ constexpr int kT = 128;
 constexpr int kStagers = 128;
 constexpr int kThreads = kStagers + 64;   // + MMA warp + producer warp
 constexpr uint32_t kSlot = kT * 128u;     // one landing slot: 128 rows x 32 floats
-constexpr uint32_t kColAcc = 128;         // TMEM: A buffers at [0,64) and [64,128), accumulators from 128
+constexpr int kNAB = 4;                   // TMEM A buffers (64 columns each: hi | lo of one K chunk)
+constexpr uint32_t kColAcc = 64u * kNAB;  // TMEM: A buffers at [0, 256), accumulators from 256
 
 struct StLayout {
-  uint32_t land, btab, leaf, hist, bars, slot, total;
+  uint32_t land, btab, hist, bars, slot, total;
 };
 
 __host__ __device__ inline uint32_t st_align(uint32_t v, uint32_t a) { return (v + a - 1) & ~(a - 1); }
@@ -54,10 +55,9 @@ __host__ __device__ inline StLayout st_layout(int npad, bool last, int na, int n
   uint32_t o = 0;
   L.land = o; o += (uint32_t)na * kSlot;
   L.btab = o; o += (uint32_t)nb * st_bslot(npad);
-  L.leaf = o; o += last ? 2u * (uint32_t)npad * 8u : 0u;
   o = st_align(o, 16);
   L.hist = o; o += 256 * 4;
-  L.bars = st_align(o, 8); o = L.bars + (uint32_t)(2 * nb + 12) * 8;
+  L.bars = st_align(o, 8); o = L.bars + (uint32_t)(2 * nb + 2 * kNAB + 4) * 8;
   L.slot = o; o += 16;
   L.total = o + 1024;
   return L;
@@ -80,12 +80,10 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
   int* s_hist = reinterpret_cast<int*>(base + Ly.hist);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + Ly.bars);   // [NB] table chunk landed (tx)
   uint64_t* done = full + NB;          // [NB] MMAs reading the slot retired (commit)
-  uint64_t* astaged = done + NB;       // [2] A buffer written by the 128 stagers
-  uint64_t* aempty = astaged + 2;      // [2] MMAs reading the A buffer retired (commit)
-  uint64_t* accfull = aempty + 2;      // [2] accumulator complete (commit)
+  uint64_t* astaged = done + NB;       // [kNAB] A buffer written by the 128 stagers
+  uint64_t* aempty = astaged + kNAB;   // [kNAB] MMAs reading the A buffer retired (commit)
+  uint64_t* accfull = aempty + kNAB;   // [2] accumulator complete (commit)
   uint64_t* accempty = accfull + 2;    // [2] accumulator read back by the 128 stagers
-  uint64_t* leaffull = accempty + 2;   // [2] leaf block landed (tx)
-  uint64_t* leafempty = leaffull + 2;  // [2] leaf block read by the 128 stagers
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + Ly.slot);
 
   if (warp == 0) tmem_alloc(tmem_slot, a.tmem_cols);
@@ -94,13 +92,13 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       mbar_init(&full[b], 1);
       mbar_init(&done[b], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kNAB; ++b) {
       mbar_init(&astaged[b], kStagers);
       mbar_init(&aempty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&accfull[b], 1);
       mbar_init(&accempty[b], kStagers);
-      mbar_init(&leaffull[b], 1);
-      mbar_init(&leafempty[b], kStagers);
     }
     fence_mbar_init();
   }
@@ -125,17 +123,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       int bin = 0;
       for (int g = 0; g < total; ++g) {
         const int seq = g / kch, c = g - seq * kch;
-        if (c == 0) {
-          bin = item_at(a, i0 + seq).x;
-          if (last) {
-            const int b = seq & 1;
-            if (seq >= 2) mbar_wait(&leafempty[b], (uint32_t)((seq >> 1) - 1) & 1u);
-            mbar_arrive_expect_tx(&leaffull[b], 8u * npad);
-            bulk_g2s(base + Ly.leaf + b * (8u * npad),
-                     reinterpret_cast<const uint8_t*>(a.table) + (size_t)bin * tb + (size_t)kch * chunk_bytes,
-                     8u * npad, &leaffull[b]);
-          }
-        }
+        if (c == 0) bin = item_at(a, i0 + seq).x;
         const int s = g % NB;
         if (g >= NB) mbar_wait(&done[s], (uint32_t)(g / NB - 1) & 1u);
         mbar_arrive_expect_tx(&full[s], chunk_bytes);
@@ -151,11 +139,11 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       const uint32_t b_s = smem_u32(base + Ly.btab);
       for (int g = 0; g < total; ++g) {
         const int seq = g / kch, c = g - seq * kch;
-        const int ab = g & 1, s = g % NB;
+        const int ab = g % kNAB, s = g % NB;
         const int acc = nacc == 2 ? (seq & 1) : 0;
         const uint32_t dcol = tmem + kColAcc + (uint32_t)acc * accw;
         if (c == 0 && seq >= nacc) mbar_wait(&accempty[acc], (uint32_t)(seq / nacc - 1) & 1u);
-        mbar_wait(&astaged[ab], (uint32_t)(g >> 1) & 1u);
+        mbar_wait(&astaged[ab], (uint32_t)(g / kNAB) & 1u);
         mbar_wait(&full[s], (uint32_t)(g / NB) & 1u);
         tc_fence_after();
         const uint32_t bh = b_s + s * bslot;
@@ -212,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
     int cur_p = -1, cur_rows = 0, cur_bin = 0;
     for (int g = 0; g < total; ++g) {
       const int seq = g / kch, c = g - seq * kch;
-      const int ab = g & 1;
+      const int ab = g % kNAB;
       if (c == 0) {
         const int4 it = item_at(a, i0 + seq);
         cur_bin = it.x;
@@ -235,8 +223,8 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       }
       __syncwarp();      // every lane has read its row before the slot is refilled
       issue_a(g + NA);
-      if (g >= 2) {
-        mbar_wait(&aempty[ab], (uint32_t)((g >> 1) - 1) & 1u);
+      if (g >= kNAB) {
+        mbar_wait(&aempty[ab], (uint32_t)(g / kNAB - 1) & 1u);
         tc_fence_after();
       }
       tmem_st32(tmem + lane_base + (uint32_t)ab * 64u, hi);
@@ -272,16 +260,11 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       const bool valid = tid < cur_rows && cur_p >= 0;
       const int p = cur_p;
       int leaf_info = 0, leaf_cnt = 0;
-      if (last) {
-        const int b = seq & 1;
-        mbar_wait(&leaffull[b], (uint32_t)(seq >> 1) & 1u);
-        const int* info = reinterpret_cast<const int*>(base + Ly.leaf + b * (8u * npad));
-        if (valid) {
-          leaf_info = info[best];
-          leaf_cnt = info[npad + best];
-        }
-        fence_proxy_async_smem();   // generic reads before the producer's async refill
-        mbar_arrive(&leafempty[b]);
+      if (last && valid) {   // the winner's leaf record, straight from the (L2-resident) table block
+        const int* info = reinterpret_cast<const int*>(reinterpret_cast<const uint8_t*>(a.table) +
+                                                       (size_t)cur_bin * tb + (size_t)kch * chunk_bytes);
+        leaf_info = __ldg(info + best);
+        leaf_cnt = __ldg(info + npad + best);
       }
       if (valid) {
         const int child = cb + best;
@@ -314,9 +297,10 @@ struct StCfg {
   int na, nb;
 };
 
-// ring depths: wide nodes (c2: 64 KB table chunks) get two table slots; narrow
+// ring depths: wide nodes (c2: 64 KB table chunks) get three table slots and a
+// two-deep landing ring (the table refill latency is the one to hide); narrow
 // ones (c4: 8-16 KB) a deep ring on both sides
-inline StCfg st_cfg(int npad) { return npad > 128 ? StCfg{4, 2} : (npad > 64 ? StCfg{4, 4} : StCfg{6, 6}); }
+inline StCfg st_cfg(int npad) { return npad > 128 ? StCfg{2, 3} : (npad > 64 ? StCfg{4, 4} : StCfg{6, 6}); }
 
 template <int NA, int NB>
 cudaError_t launch_st(ScoreArgs s, int sms, cudaStream_t st) {
@@ -344,7 +328,7 @@ bool score_st_fits(int kchunks, int npad, bool last) {
 cudaError_t launch_score_st(const ScoreArgs& s, int sms, cudaStream_t st) {
   if (!score_st_fits(s.kchunks, s.npad, s.leaf_sel != nullptr)) return cudaErrorNotSupported;
   const StCfg c = st_cfg(s.npad);
-  if (c.nb == 2) return launch_st<4, 2>(s, sms, st);
+  if (c.nb == 3) return launch_st<2, 3>(s, sms, st);
   if (c.nb == 4) return launch_st<4, 4>(s, sms, st);
   return launch_st<6, 6>(s, sms, st);
 }
