@@ -29,6 +29,7 @@ int g_pdl = 1;          // programmatic dependent launch between staged kernels
 int g_root_direct = 1;  // root pass over the batch in patch order (no scan / scatter at level 0)
 int g_update_tile = 0;  // 1: tile OMP update fused with the next root scoring (update_tile.cu)
 int g_update_omp8 = 1;  // 1: lockstep OMP update (update_omp8_kernel, encode_update.cu)
+int g_update_wide = 1;  // one-CTA-per-patch OMP update for rows wider than 160 floats
 int g_gram = 0;         // 1: atom Gram table for the lockstep update (m <= kGramMaxAtoms); off: measured slower than the support-row dots (c1 update 2.09 vs 1.83 ms)
 int g_score_ws = 2;  // 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM (default), 3 streamed table
 
@@ -714,6 +715,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int scatter_blocks = (int)((N + 255) / 256);
   const size_t usmem = update_smem_bytes(uc, K, d->ld, u.cache_atoms != 0);
+  const bool wide = method == kMethodOMP && !lockstep && g_update_wide && wide_update_cpt(d->ld) != 0;
   // tile update: OMP refit + next-iteration root scoring in one kernel
   const bool tile = t && g_update_tile && u.gram != nullptr && update_tile_supported(d, t, K, method);
   // the root bin holds every active patch: its pass can walk the batch in patch
@@ -833,7 +835,9 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       e = launch_update_tile(ta, st);
     } else {
       u.iter = it;
-      e = lockstep ? launch_update_omp8(u, st) : launch_update(uc, u, ublocks, usmem, st);
+      if (lockstep) e = launch_update_omp8(u, st);
+      else if (wide) e = launch_update_wide(u, st);
+      else e = launch_update(uc, u, ublocks, usmem, st);
     }
     if (e != cudaSuccess) return e;
   }

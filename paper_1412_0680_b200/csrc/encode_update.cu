@@ -129,8 +129,13 @@ __global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
 // Shared scratch per patch group (floats): S[K] | c[K] | y[K] | M[K(K+1)/2] | g[K] | w[K] | cn[K]
 __host__ __device__ inline int upd_scalar_floats(int K) { return (6 * K + K * (K + 1) / 2 + 3) & ~3; }
 
+#ifndef STMP_UPD32_MINB
+#define STMP_UPD32_MINB 3
+#endif
+// wide rows (G = 32, up to 16 chunks per lane) hold four row slices in registers;
+// STMP_UPD32_MINB trades registers (spills to L1) for resident warps
 template <int G, int CPL>
-__global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
+__global__ void __launch_bounds__(128, G == 32 ? STMP_UPD32_MINB : 1) update_kernel(UpdateArgs a) {
   pdl_enter();
   extern __shared__ __align__(16) float upd_smem[];
   const int gpb = blockDim.x / G;
@@ -301,6 +306,182 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
     if (gl == 0) a.active[p] = act ? 1 : 0;
   }
   count_root(act && gl == 0, a.root_count);
+}
+
+// ------------------------------------------------------------------ OMP update, wide rows
+// One CTA of 128 threads per patch for rows too wide for a lane group to hold
+// (config 4: 1600 floats): each thread keeps CPT 16-byte chunks of a row, so a
+// row slice is 4*CPT registers instead of 52 and 12-20 warps stay resident per
+// SM (the 32-lane version ran at 8).  Every dot product is one warp butterfly
+// plus a 4-entry shared-memory sum; the small solve (t <= K) runs redundantly
+// in every thread from shared memory, so it needs no further communication.
+// Same state layout and semantics as update_kernel's OMP branch.
+template <int CPT>
+__global__ void __launch_bounds__(128) update_wide_kernel(UpdateArgs a) {
+  pdl_enter();
+  extern __shared__ __align__(16) float wsm[];
+  const int K = a.K;
+  const int64_t p = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int F = a.ld >> 2;
+  int* S_s = reinterpret_cast<int*>(wsm);           // [K]
+  float* c_s = wsm + K;                             // [K] current coefficients
+  float* y_s = c_s + K;                             // [K]
+  float* M_s = y_s + K;                             // [K(K+1)/2] packed M = L^{-1}
+  float* g_s = M_s + K * (K + 1) / 2;               // [K + 2] Gram column, a.a, a.x
+  float* red = g_s + K + 2;                         // [4][K + 2] per-warp partial sums
+  float* cn_s = red + 4 * (K + 2);                  // [K] new coefficients
+  __shared__ int s_atom;
+  if (!a.active[p]) return;   // CTA-uniform
+  const int t = a.count[p];
+  const int lsel = a.leaf_sel[p];
+  for (int i = tid; i < K; i += 128) {
+    S_s[i] = a.idx[p * K + i];
+    c_s[i] = a.coef[p * K + i];
+    y_s[i] = a.yv[p * K + i];
+  }
+  for (int i = tid; i < K * (K + 1) / 2; i += 128) M_s[i] = a.Lf[p * (int64_t)(K * (K + 1) / 2) + i];
+  auto load = [&](const float* row, float4 (&v)[CPT]) {
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const int c = tid + 128 * i;
+      v[i] = c < F ? __ldg(reinterpret_cast<const float4*>(row) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto dot = [&](const float4 (&u)[CPT], const float4 (&v)[CPT]) {
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      s = fmaf(u[i].x, v[i].x, s);
+      s = fmaf(u[i].y, v[i].y, s);
+      s = fmaf(u[i].z, v[i].z, s);
+      s = fmaf(u[i].w, v[i].w, s);
+    }
+    return s;
+  };
+  // warp butterfly, lane 0 stores the warp's partial of value j
+  auto part = [&](float s, int j) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if (lane == 0) red[warp * (K + 2) + j] = s;
+  };
+  float4 x[CPT], av[CPT];
+  load(a.X2 + p * a.ld2, x);
+  int atom = lsel;
+  if (lsel < 0) {   // multi-atom leaf: max |a . r|, ties to the lowest atom index
+    float4 r[CPT];
+    load(a.R_in + p * a.ld, r);
+    const int node = -1 - lsel;
+    const int cb = __ldg(a.child_begin + node), cc = __ldg(a.child_count + node);
+    float bestv = -1.f;
+    atom = __ldg(a.leaf_atom + cb);
+    for (int j = 0; j < cc; ++j) {
+      const int aj = __ldg(a.leaf_atom + cb + j);
+      float4 v[CPT];
+      load(a.atoms + (int64_t)aj * a.ld, v);
+      __syncthreads();   // red is reused
+      part(dot(v, r), 0);
+      __syncthreads();
+      const float mv = fabsf(red[0] + red[K + 2] + red[2 * (K + 2)] + red[3 * (K + 2)]);
+      if (mv > bestv || (mv == bestv && aj < atom)) { bestv = mv; atom = aj; }
+    }
+  }
+  load(a.atoms + (int64_t)atom * a.ld, av);
+  __syncthreads();   // state in shared memory
+  // Gram column against the support, a.a and a.x: one partial per value and warp
+  for (int k = 0; k < t; ++k) {
+    float4 sv[CPT];
+    load(a.atoms + (int64_t)S_s[k] * a.ld, sv);
+    part(dot(sv, av), k);
+  }
+  part(dot(av, av), t);
+  part(dot(av, x), t + 1);
+  __syncthreads();
+  for (int j = tid; j < t + 2; j += 128)
+    g_s[j] = red[j] + red[(K + 2) + j] + red[2 * (K + 2) + j] + red[3 * (K + 2) + j];
+  __syncthreads();
+  bool dup = false;
+  for (int k = 0; k < t; ++k) dup |= S_s[k] == atom;
+  float gc = 0.f;
+  for (int k = 0; k < t; ++k) gc = fmaf(g_s[k], c_s[k], gc);
+  const float gtt = g_s[t], bt = g_s[t + 1];
+  const float score = bt - gc;   // a . r for r = x - A_S c_prev (pursuit.py:217 check)
+  bool act = true;
+  if (dup || score == 0.f) {
+    act = false;   // re-selection (or a zero score) ends the loop
+  } else {
+    // inverse-Cholesky refit (same algebra as update_kernel), every thread redundantly:
+    //   w = M g, d = sqrt(a.a + ridge - w.w), y_t = (b_t - w.y) / d,
+    //   new row of M: (-(1/d) w^T M, 1/d), c_new = c_prev + m_t y_t
+    float wsum = 0.f, wy = 0.f;
+    for (int j = 0; j < t; ++j) {
+      const float* Mj = M_s + j * (j + 1) / 2;
+      float w = 0.f;
+      for (int k = 0; k <= j; ++k) w = fmaf(Mj[k], g_s[k], w);
+      red[j] = w;   // (all warps' partial sums were consumed above)
+      wsum = fmaf(w, w, wsum);
+      wy = fmaf(w, y_s[j], wy);
+    }
+    const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
+    const float inv_d = 1.f / dg;
+    const float yy = (bt - wy) * inv_d;
+    __syncthreads();   // w (red) written identically by every thread
+    float* Mt = a.Lf + p * (int64_t)(K * (K + 1) / 2) + t * (t + 1) / 2;
+    for (int k = tid; k <= t; k += 128) {
+      float mk = inv_d;
+      if (k < t) {
+        float s1 = 0.f;
+        for (int j = k; j < t; ++j) s1 = fmaf(red[j], M_s[j * (j + 1) / 2 + k], s1);
+        mk = -inv_d * s1;
+      }
+      const float ck = k < t ? fmaf(mk, yy, c_s[k]) : inv_d * yy;
+      Mt[k] = mk;
+      cn_s[k] = ck;
+      a.coef[p * K + k] = ck;
+    }
+    if (tid == 0) s_atom = atom;
+    __syncthreads();
+    // residual r = x - A_S c - c_t a (support rows again, now from L2)
+    float4 r[CPT];
+    const float ct = cn_s[t];
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      r[i].x = fmaf(-ct, av[i].x, x[i].x);
+      r[i].y = fmaf(-ct, av[i].y, x[i].y);
+      r[i].z = fmaf(-ct, av[i].z, x[i].z);
+      r[i].w = fmaf(-ct, av[i].w, x[i].w);
+    }
+    for (int k = 0; k < t; ++k) {
+      float4 sv[CPT];
+      load(a.atoms + (int64_t)S_s[k] * a.ld, sv);
+      const float ck = cn_s[k];
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        r[i].x = fmaf(-ck, sv[i].x, r[i].x);
+        r[i].y = fmaf(-ck, sv[i].y, r[i].y);
+        r[i].z = fmaf(-ck, sv[i].z, r[i].z);
+        r[i].w = fmaf(-ck, sv[i].w, r[i].w);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const int c = tid + 128 * i;
+      if (c < F) reinterpret_cast<float4*>(a.R + p * a.ld)[c] = r[i];
+    }
+    part(dot(r, r), 0);
+    __syncthreads();
+    const float rn = sqrtf(red[0] + red[K + 2] + red[2 * (K + 2)] + red[3 * (K + 2)]);
+    act = (t + 1 < K) && rn > a.tol[p];
+    if (tid == 0) {
+      a.yv[p * (int64_t)K + t] = yy;
+      a.idx[p * K + t] = s_atom;
+      a.count[p] = t + 1;
+      a.resnorm[p] = rn;
+    }
+  }
+  if (tid == 0) a.active[p] = act ? 1 : 0;
+  if (tid == 0 && act && a.root_count)
+    atomicAdd(&a.root_count[blockIdx.x & (kRootStripes - 1)], 1);
 }
 
 // ------------------------------------------------------------------ OMP update, K <= 8
@@ -718,6 +899,29 @@ cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, s
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+// wide-row OMP update: one CTA per patch (ld > 160 floats, OMP)
+int wide_update_cpt(int ld) { return ld > 160 && ld <= 2048 ? (ld / 4 + 127) / 128 : 0; }
+
+cudaError_t launch_update_wide(const UpdateArgs& a, cudaStream_t st) {
+  const int cpt = wide_update_cpt(a.ld);
+  const int K = a.K;
+  const size_t smem = (size_t)(3 * K + K * (K + 1) / 2 + 5 * (K + 2) + K) * 4;
+  switch (cpt) {
+#define STMP_WIDE_CASE(c)                                                                     \
+  case c: {                                                                                   \
+    if (smem > 48 * 1024) {                                                                   \
+      cudaError_t err = cudaFuncSetAttribute(update_wide_kernel<c>,                           \
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (err != cudaSuccess) return err;                                                     \
+    }                                                                                         \
+    return launch_kernel(update_wide_kernel<c>, (unsigned)a.N, 128, smem, st, true, a);       \
+  }
+    STMP_WIDE_CASE(1) STMP_WIDE_CASE(2) STMP_WIDE_CASE(3) STMP_WIDE_CASE(4)
+#undef STMP_WIDE_CASE
+    default: return cudaErrorNotSupported;
+  }
 }
 
 size_t update_smem_bytes(const UpdateCfg& c, int K, int ld, bool cache_atoms) {

@@ -129,6 +129,10 @@ size_t update_smem_bytes(const UpdateCfg& c, int K, int ld, bool cache_atoms);
 // all solver state in registers, support size a.iter fixed at compile time,
 // state in the [entry][patch] layout.  Returns cudaErrorNotSupported when not applicable.
 cudaError_t launch_update_omp8(const UpdateArgs& a, cudaStream_t st);
+// OMP update with one CTA per patch for rows wider than 160 floats (0: not applicable)
+int wide_update_cpt(int ld);
+cudaError_t launch_update_wide(const UpdateArgs& a, cudaStream_t st);
+extern int g_update_wide;
 // lanes per patch of the lockstep OMP update for this shape (8 or 16), 0 if unsupported
 int lockstep_lanes(int ld, int K);
 // Build the [m, m] Gram matrix of the (padded) dictionary on `st`; returns nullptr if
