@@ -500,6 +500,9 @@ __global__ void __launch_bounds__(128) update_wide_kernel(UpdateArgs a) {
 #ifndef STMP_OMP8_MINB0
 #define STMP_OMP8_MINB0 10
 #endif
+#ifndef STMP_OMP8_MINBW
+#define STMP_OMP8_MINBW 5   // rows of 96-160 floats
+#endif
 #ifndef STMP_SUP_SMEM
 #define STMP_SUP_SMEM 1
 #endif
@@ -566,7 +569,8 @@ __device__ __forceinline__ void group_reduce_scatter_n(float (&p)[NR * G], int g
 // Lane gl owns rows gl + G * i (i < NR) of the inverse Cholesky factor M (and the
 // matching y_j, c_j): NR = 1 while the support fits the group, 2 up to 2G atoms.
 template <int G, int CPL, int T, bool GRAM>
-__global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T < G ? STMP_OMP8_MINB : 5)) : 5)
+__global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T < G ? STMP_OMP8_MINB : 5))
+                                                : STMP_OMP8_MINBW)
     update_omp8_kernel(UpdateArgs a) {
   constexpr bool kSupSmem = sup_smem<T, GRAM>();
   constexpr int NR = T < G ? 1 : 2;     // Cholesky rows per lane
