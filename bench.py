@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--score-kernel", type=int, default=2, choices=[0, 1, 2],
                     help="tcgen05 score pass: 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM")
     ap.add_argument("--update-kernel", type=int, default=1, choices=[0, 1, 2],
-                    help="staged OMP update: 0 generic, 1 Gram-table K<=8, 2 tile + fused root scoring")
+                    help="staged OMP update: 0 generic, 1 lockstep (K<=16) / wide-row, 2 tile + fused root scoring")
     ap.add_argument("--pdl", type=int, default=1, choices=[0, 1],
                     help="programmatic dependent launch between the staged kernels")
     ap.add_argument("--path", type=int, default=0, choices=[0, 1, 2],
@@ -325,8 +325,9 @@ def main():
     per_step = launches / max(1, args.steps)
     if per_step > 1:
         score = "exact_scan (tensor-core GEMM + argmax)" if exhaustive else "score_ts / score_st (tcgen05 3xTF32)"
-        kernel_desc = (f"staged pipeline, {per_step:.0f} launches per step: init + K x (levels x (scan, scatter, "
-                       f"{score}) + update); achieved is over the whole step")
+        kernel_desc = (f"staged pipeline, {per_step:.0f} launches per step: init + K x (root {score} pass over the "
+                       f"batch + per deeper level (fused scan + scatter, {score}) + OMP/MP update); achieved is over "
+                       f"the whole step")
     else:
         kernel_desc = "encode_fused_kernel (one launch per step)"
     peaks = {}
