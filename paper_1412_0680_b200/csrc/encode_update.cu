@@ -129,13 +129,10 @@ __global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
 // Shared scratch per patch group (floats): S[K] | c[K] | y[K] | M[K(K+1)/2] | g[K] | w[K] | cn[K]
 __host__ __device__ inline int upd_scalar_floats(int K) { return (6 * K + K * (K + 1) / 2 + 3) & ~3; }
 
-#ifndef STMP_UPD32_MINB
-#define STMP_UPD32_MINB 3
-#endif
-// wide rows (G = 32, up to 16 chunks per lane) hold four row slices in registers;
-// STMP_UPD32_MINB trades registers (spills to L1) for resident warps
+// (no minimum-blocks bound: an explicit one, even 1, makes ptxas spend more
+// registers -- 88 instead of 60 for <8, 2> -- and costs config 1 MP 0.5 ms)
 template <int G, int CPL>
-__global__ void __launch_bounds__(128, G == 32 ? STMP_UPD32_MINB : 1) update_kernel(UpdateArgs a) {
+__global__ void __launch_bounds__(128) update_kernel(UpdateArgs a) {
   pdl_enter();
   extern __shared__ __align__(16) float upd_smem[];
   const int gpb = blockDim.x / G;

@@ -89,7 +89,6 @@ __device__ __forceinline__ void gather_rows(const ScoreArgs& a, const int* rows_
 // from 16 instructions per row to half an instruction per row.
 template <int KCH, bool TMA>
 __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, const __grid_constant__ CUtensorMap rmap) {
-  pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* base = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -143,6 +142,9 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  // TMEM, barriers and the histogram are set up while the previous kernel
+  // drains (programmatic dependent launch); nothing above reads its output
+  pdl_enter();
 
   const int num_items = item_count(a);
   const int per = (num_items + gridDim.x - 1) / gridDim.x;
