@@ -298,9 +298,9 @@ def main():
                     resnorm=torch.empty(N, dtype=torch.float32).pin_memory().numpy(),
                     ip=torch.empty((N, 2), dtype=torch.int32).pin_memory().numpy())
         Xn = Xp.numpy()
-        for _ in range(2):
+        for _ in range(max(3, args.warmup)):
             P.encode_host(sel, Xn, cfg.K, args.method, out=outs)
-        e2e_steps = max(3, min(args.steps, 10))
+        e2e_steps = max(5, min(args.steps, 20))
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
