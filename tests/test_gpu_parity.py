@@ -367,3 +367,61 @@ def test_config1_full_size_properties(path):
     head = run(sel, X[:3000], cfg.K, "omp", paths=False)
     np.testing.assert_array_equal(head["idx"], res.idx[:3000].cpu().numpy())
     np.testing.assert_array_equal(head["coef"], res.coef[:3000].cpu().numpy())
+
+
+# ----------------------------------------------------------------- synthetic shapes for the update variants
+
+def _synthetic(seed, m, n, counts_by_depth, branching):
+    """Random unit atoms and a random tree over them (any centroids define a
+    valid greedy descent; the oracle scores the same centroids)."""
+    from paper_1412_0680_b200 import tree as T
+    rng = np.random.default_rng(seed)
+    atoms = rng.standard_normal((m, n))
+    atoms = (atoms / np.linalg.norm(atoms, axis=1, keepdims=True)).astype(np.float32)
+    n_internal = sum(len(c) for c in counts_by_depth)
+    leaf_atom = rng.permutation(m)
+    # centroids: the normalised mean of each node's descendant atoms (like a k-means tree)
+    cent = np.zeros((n_internal, n), dtype=np.float32)
+    flat = T._from_counts(branching, n, P().fingerprint_atoms(atoms), counts_by_depth, cent, leaf_atom)
+    off = flat.level_offsets
+    L = len(branching)
+    sums = np.zeros((n_internal, n))
+    for v in range(off[L], off[L + 1]):
+        sums[v] = atoms[leaf_atom[flat.child_begin[v]:flat.child_begin[v] + flat.child_count[v]]].sum(0)
+    for d in range(L - 1, -1, -1):
+        for v in range(off[d], off[d + 1]):
+            sums[v] = sums[flat.child_begin[v]:flat.child_begin[v] + flat.child_count[v]].sum(0)
+    cent = (sums / np.linalg.norm(sums, axis=1, keepdims=True)).astype(np.float32)
+    flat = T._from_counts(branching, n, P().fingerprint_atoms(atoms), counts_by_depth, cent, leaf_atom)
+    return atoms, flat
+
+
+@pytest.mark.parametrize("shape", ["k16-lockstep-two-rows", "wide-multi-atom-leaves"])
+def test_update_variants_match_oracle(shape):
+    """K = 16 on 64-dim rows (lockstep update, two Cholesky rows per lane) and
+    200-dim rows with two-atom leaves (one-CTA-per-patch wide update, leaf
+    scoring inside the update), staged pipeline, against the f64 oracle."""
+    from paper_1412_0680_b200 import _lib
+    if shape.startswith("k16"):
+        m, n, K, cbd, br = 512, 64, 16, [[8], [8] * 8, [8] * 64, [1] * 512], (8, 8, 8)
+    else:
+        m, n, K, cbd, br = 128, 200, 6, [[8], [8] * 8, [2] * 64], (8, 8)
+    atoms, flat = _synthetic(7, m, n, cbd, br)
+    rng = np.random.default_rng(8)
+    N = 4096
+    X = np.zeros((N, n), dtype=np.float64)
+    for p in range(N):
+        sup = rng.choice(m, 4, replace=False)
+        X[p] = rng.standard_normal(4) @ atoms[sup].astype(np.float64) + 0.05 * rng.standard_normal(n)
+    X = X.astype(np.float32)
+    sel = P().TreeSelector(flat, atoms, 1 / 8)
+    _lib.set_option("path", _lib.PATH_STAGED)
+    try:
+        out = run(sel, X, K, "omp")
+    finally:
+        restore_defaults(_lib)
+    a64 = atoms.astype(np.float64)
+    rows = slice(0, 512)   # the oracle on a prefix keeps the test short; the GPU encoded all N
+    ref = oracle_pack(O.tree_selector(O.OracleTree.from_flat(flat), a64, 1 / 8), a64, X[rows], K, "omp")
+    rep = compare({k: v[rows] for k, v in out.items()}, ref, X[rows], check_path=True)
+    assert rep.ok, rep.summary()
