@@ -226,16 +226,13 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
       tc_fence_after();
       const int a0 = blk * bw;
       const int cnt = min(bw, m - a0);
-      for (int col0 = 0; col0 < bw; col0 += 32) {
-        float v[32];
-        tmem_ld32(tmem + lane_base + kColAcc + (uint32_t)acc * (uint32_t)bw + (uint32_t)col0, v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float mv = fabsf(v[j]);
-          if (col0 + j < cnt && mv > bestv) {
-            bestv = mv;
-            best = a0 + col0 + j;
-          }
+      {
+        float bv;
+        int bi;
+        tmem_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * (uint32_t)bw, bw, cnt, bv, bi);
+        if (bv > bestv) {   // strict: an earlier block keeps ties (lowest atom index)
+          bestv = bv;
+          best = a0 + bi;
         }
       }
       tc_fence_before();

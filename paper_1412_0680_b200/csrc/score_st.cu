@@ -243,18 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       const int cc = __ldg(a.child_count + gnode);
       int best = 0;
       float bestv = -1.f;
-      for (int col0 = 0; col0 < npad; col0 += 32) {
-        float v[32];
-        tmem_ld32(tmem + lane_base + kColAcc + (uint32_t)acc * accw + (uint32_t)col0, v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float mv = fabsf(v[j]);
-          if (col0 + j < cc && mv > bestv) {
-            bestv = mv;
-            best = col0 + j;
-          }
-        }
-      }
+      tmem_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * accw, (int)accw, npad, bestv, best);
       tc_fence_before();
       mbar_arrive(&accempty[acc]);
       const bool valid = tid < cur_rows && cur_p >= 0;

@@ -272,18 +272,7 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
 
     int best = 0;
     float bestv = -1.f;
-    for (int col0 = 0; col0 < npad; col0 += 32) {
-      float v[32];
-      tmem_ld32(tmem + lane_base + kColAcc + (uint32_t)col0, v);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float mv = fabsf(v[j]);
-        if (col0 + j < cc && mv > bestv) {
-          bestv = mv;
-          best = col0 + j;
-        }
-      }
-    }
+    tmem_abs_argmax(tmem + lane_base + kColAcc, (npad + 31) & ~31, npad, bestv, best);
     const int p = row < rows ? rows_ids[row] : -1;
     const bool valid = p >= 0;
     const int child = cb + best;

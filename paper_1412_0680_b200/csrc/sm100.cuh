@@ -210,6 +210,48 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// First maximum of |acc| over the ncols (a multiple of 32) columns of this
+// thread's TMEM lane starting at taddr, ties to the lowest column (the argmax
+// of pursuit.py:151,159-161 / np.argmax): pass 1 keeps only the running max
+// and the first 32-column chunk that reaches it (one FMNMX per column); pass 2
+// re-reads the chunks (tcgen05.ld is warp-collective) and resolves the column
+// inside this thread's winning chunk.  Columns in [nvalid, ncols) were never
+// written and are masked; columns between the valid children and nvalid must
+// hold exact zeros (zero table rows): they can never be the first maximum.
+__device__ __forceinline__ void tmem_abs_argmax(uint32_t taddr, int ncols, int nvalid, float& bestv, int& best) {
+  float m = -1.f;
+  int bc = 0;
+  for (int c0 = 0; c0 < ncols; c0 += 32) {
+    float v[32];
+    tmem_ld32(taddr + (uint32_t)c0, v);
+    if (c0 + 32 > nvalid) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = c0 + j < nvalid ? v[j] : 0.f;
+    }
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+      for (int j = 0; j < w; ++j) v[j] = fmaxf(fabsf(v[j]), fabsf(v[j + w]));
+    const float t = fabsf(v[0]);
+    if (t > m) {
+      m = t;
+      bc = c0;
+    }
+  }
+  int idx = 0;
+  for (int c0 = 0; c0 < ncols; c0 += 32) {
+    float v[32];
+    tmem_ld32(taddr + (uint32_t)c0, v);
+    if (c0 == bc) {
+      idx = 31;
+#pragma unroll
+      for (int j = 31; j >= 0; --j) idx = (c0 + j < nvalid && fabsf(v[j]) == m) ? j : idx;
+    }
+  }
+  bestv = m;
+  best = bc + idx;
+}
+
 // K-major operand tile, 128-byte swizzle: rows of 128 B (32 f32), 8-row atoms
 // 1024 B apart.  `saddr` may be offset inside a row by the K step (32 B per
 // 8 tf32); the swizzle is applied on absolute address bits, so the atom base
