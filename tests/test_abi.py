@@ -112,3 +112,29 @@ def test_options_and_launch_counter(lib):
     _lib.set_option("score_kernel", 2)
     _lib.set_option("path", _lib.PATH_AUTO)
     assert _lib.kernel_launches() == before   # option changes launch nothing
+
+
+def test_data_format_entry_points_validate_before_touching_the_device(lib):
+    """Argument errors of the driver / data-format entry points are ValueErrors
+    (STMP_EINVAL) raised before any device work, as in the reference
+    (pipelines.py, tensor.py:59-79, operators.py:122-124)."""
+    shape = np.array([4, 4], dtype=np.int64)
+    patch = np.array([5, 2], dtype=np.int64)   # patch larger than the tensor
+    nst = np.array([1, 2], dtype=np.int64)
+    dummy = C.c_void_p(16)
+    assert lib.stmp_extract_patches(dummy, 2, shape.ctypes.data, patch.ctypes.data, nst.ctypes.data, dummy,
+                                    dummy, None) == _lib.STMP_EINVAL
+    assert b"exceeds tensor extent" in lib.stmp_last_error()
+    assert lib.stmp_aggregate_patches(dummy, 0, shape.ctypes.data, patch.ctypes.data, nst.ctypes.data, dummy,
+                                      dummy, None) == _lib.STMP_EINVAL
+    assert lib.stmp_apply_operator(99, dummy, 4, 8, None, 0, None, 0, 0, 0, 0, None, None, dummy,
+                                   None) == _lib.STMP_EINVAL
+    assert lib.stmp_apply_operator(_lib.OP_CODED_EXPOSURE, dummy, 4, 8, None, 0, dummy, 3, 1, 2, 0, None, None,
+                                   dummy, None) == _lib.STMP_EINVAL   # 3 x 1 x 2 != 8
+    ins = np.array([4, 6], dtype=np.int64)
+    fac = np.array([3, 3], dtype=np.int64)                           # 3 does not divide 4
+    assert lib.stmp_apply_operator(_lib.OP_BLOCK_AVERAGE, dummy, 4, 24, None, 0, None, 0, 0, 0, 2,
+                                   ins.ctypes.data, fac.ctypes.data, dummy, None) == _lib.STMP_EINVAL
+    assert lib.stmp_dc_split(dummy, 4, 8, 8, dummy, 0.0, dummy, 8, dummy, None) == _lib.STMP_EINVAL
+    assert lib.stmp_dc_split(dummy, -1, 8, 8, dummy, 1.0, dummy, 8, dummy, None) == _lib.STMP_EINVAL
+    assert lib.stmp_reconstruct(None, dummy, dummy, dummy, 4, 2, None, None, dummy, 8, None) == _lib.STMP_EINVAL
