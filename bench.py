@@ -344,7 +344,10 @@ def main():
         bf16 = float(peaks.get("bf16_tflops", 1590.0))
         achieved = rm["flops_per_patch"] * N / (launch_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                "frac": achieved / bf16, "traffic": None}
+                "frac": achieved / bf16, "traffic": None,
+                # the path computes fp32-accurate scores as 3xTF32 (three tf32 products per
+                # k-step); against that arithmetic's peak (dense TF32 = bf16 / 2):
+                "peak_3xtf32": bf16 / 6.0, "frac_3xtf32": achieved / (bf16 / 6.0)}
     roof.update({
         "peak_source": "MEASURED_PEAKS.json" if peaks else "B200_PROFILING.md fallback",
         "model": "SURVEY §8d per-patch algorithmic bytes/FLOPs x patches per launch / mean launch time",
