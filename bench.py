@@ -4,8 +4,9 @@ Contract:
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--method omp|mp]
                   [--selector tree|exact] [--impl ours|reference]
 One process per GPU (torchrun for N>1).  A step is one encode of the config's
-whole patch batch (config 1 by default: 1,048,576 patches, 16384x64 dictionary,
-tree 32x32x16, OMP K=8), inputs already resident in HBM.  Weak scaling: every
+whole patch batch, inputs already resident in HBM.  Default: config 4, the
+largest single-GPU BASELINE config (524,288 light-field patches, 131072x1600
+dictionary, tree 64x64x32, tree-OMP K=12); the others via --config.  Weak scaling: every
 rank encodes its own N patches (independent patch shards, no data-path
 collective); timing is the max over ranks of device-event time.
 
@@ -46,7 +47,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--method", default="omp", choices=["omp", "mp"])
     ap.add_argument("--selector", default="tree", choices=["tree", "exact"])
     ap.add_argument("--patches", type=int, default=0, help="override N per GPU")
@@ -54,10 +55,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--score-kernel", type=int, default=2, choices=[0, 1, 2],
-                    help="tcgen05 score pass: 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM")
-    ap.add_argument("--update-kernel", type=int, default=1, choices=[0, 1, 2],
-                    help="staged OMP update: 0 generic, 1 lockstep (K<=16) / wide-row, 2 tile + fused root scoring")
+    ap.add_argument("--score-kernel", type=int, default=2, choices=[2, 3],
+                    help="tcgen05 score pass: 2 node table in shared memory where it fits, 3 streamed table")
+    ap.add_argument("--update-kernel", type=int, default=1, choices=[0, 1],
+                    help="staged OMP update: 0 generic, 1 lockstep (K<=16) / wide-row")
     ap.add_argument("--pdl", type=int, default=1, choices=[0, 1],
                     help="programmatic dependent launch between the staged kernels")
     ap.add_argument("--path", type=int, default=0, choices=[0, 1, 2],
@@ -68,8 +69,7 @@ def parse():
 
 
 def tree_path(cid):
-    for p in (os.path.join(ROOT, "tests", "golden", "trees", f"c{cid}.npz"),
-              os.path.join(ROOT, "artifacts", "trees", f"c{cid}.npz")):
+    for p in (os.path.join(ROOT, "tests", "golden", "trees", f"c{cid}.npz"),):
         if os.path.exists(p):
             return p
     raise FileNotFoundError(f"no shipped tree structure for config {cid}")
@@ -139,14 +139,18 @@ def _cpu_worker(args):
     st = _POOL_STATE
     sel = (O.tree_selector(st["otree"], st["a64"], st["alpha"]) if st["otree"] is not None
            else O.exact_selector(st["a64"]))
+    out = []
     for x in st["X"][lo:hi]:
-        O.encode_one(sel, st["a64"], x, st["K"], st["method"])
-    return hi - lo
+        r = O.encode_one(sel, st["a64"], x, st["K"], st["method"])
+        r.pop("residual", None)
+        out.append(r)
+    return out
 
 
-def cpu_rate(wl, flat, X, K, method, selector, seconds, cores=None):
+def cpu_rate(wl, flat, X, K, method, selector, seconds, cores=None, results=None):
     """Time the reference CPU algorithm (oracle port, f64 NumPy, per-patch loop as
-    in pkg/src/stmp/pipelines.py:199-206) on a fork pool of all host cores."""
+    in pkg/src/stmp/pipelines.py:199-206) on a fork pool of all host cores.
+    The per-patch results (rows [0, done) of X) are appended to ``results``."""
     from oracle import stmp_oracle as O
     cores = cores or len(os.sched_getaffinity(0))
     a64 = wl.atoms.astype(np.float64)
@@ -162,10 +166,13 @@ def cpu_rate(wl, flat, X, K, method, selector, seconds, cores=None):
               range(0, sample, max(1, sample // (cores * 4)))]
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        pool.map(_cpu_worker, bounds[:1])  # warm the workers
+        pool.map(_cpu_worker, [(0, 1)] * cores)  # warm the workers
         t0 = time.perf_counter()
-        done = sum(pool.map(_cpu_worker, bounds))
+        parts = pool.map(_cpu_worker, bounds)
         wall = time.perf_counter() - t0
+    done = sum(len(p) for p in parts)
+    if results is not None:
+        results.extend(r for p in parts for r in p)
     return done / wall, cores, done, wall
 
 
@@ -186,7 +193,7 @@ def main():
     rank, world, local = dist_env()
     cfg = W.CONFIGS[args.config]
     exhaustive = args.selector == "exact"
-    N = args.patches or (cfg.N if not exhaustive else min(cfg.N, 65536))
+    N = args.patches or cfg.N
     workload = f"{cfg.name}/{'tree' if not exhaustive else 'exhaustive'}-{args.method.upper()}"
 
     if args.impl == "reference":
@@ -194,7 +201,7 @@ def main():
             return
         wl = W.make_dictionary(cfg)
         flat = T.load_structure(tree_path(cfg.cid), wl.atoms) if not exhaustive else None
-        sample_rows = min(N, 65536 if cfg.n <= 256 else 4096)
+        sample_rows = min(N, 65536)
         X = W.make_patches(wl, sample_rows)
         # size each step to ~3 s of the whole CPU so the run ends within minutes
         rate0, cores, _, _ = cpu_rate(wl, flat, X, cfg.K, args.method, args.selector, 3.0)
@@ -241,7 +248,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     wl = W.make_dictionary(cfg)
-    flat = T.load_structure(tree_path(cfg.cid), wl.atoms)
+    flat = T.load_structure(tree_path(cfg.cid), wl.atoms) if not exhaustive else None
     chunk_start = rank * (-(-N // cfg.chunk) * cfg.chunk)  # distinct patch shard per rank
     X_host = W.make_patches(wl, N, start=chunk_start)
     sel = P.ExactSelector(wl.atoms) if exhaustive else P.TreeSelector(flat, wl.atoms, cfg.alpha)
@@ -270,9 +277,10 @@ def main():
           for _ in range(args.steps)]
     lc0 = _lib.kernel_launches()
     e0.record(stream)
+    res = None
     for i in range(args.steps):
         ev[i][0].record(stream)
-        step()
+        res = step()
         ev[i][1].record(stream)
     e1.record(stream)
     launches = _lib.kernel_launches() - lc0   # counted by the library at each launch site
@@ -363,12 +371,22 @@ def main():
             roof["traffic"] = tr.get("bytes_per_launch")
 
     cpu = None
+    parity = None
     if not args.no_cpu_baseline and world == 1:
-        rate, cores, done, wall = cpu_rate(wl, flat, X_host[:65536 if cfg.n <= 256 else 4096],
-                                           cfg.K, args.method, args.selector, args.cpu_seconds)
+        from oracle import stmp_oracle as O
+        from oracle.parity import compare
+        oracle_res = []
+        rate, cores, done, wall = cpu_rate(wl, flat, X_host[:65536], cfg.K, args.method, args.selector,
+                                           args.cpu_seconds, results=oracle_res)
         cpu = {"value": rate, "unit": "patches/s", "cores": cores, "kind": "port",
                "sample": f"{done} patches (prefix of the batch) in {wall:.1f}s, oracle port of the "
                          f"reference (f64 NumPy per-patch loop), {cores}-process pool on {cpu_model()}"}
+        # parity of the last timed step's outputs on the same prefix (SURVEY §8c contract)
+        ref = O.pack(oracle_res, cfg.K)
+        gpu = {k: getattr(res, k)[:done].cpu().numpy() for k in ("idx", "coef", "count", "resnorm", "ip")}
+        rep = compare(gpu, ref, X_host[:done], check_path=False)
+        parity = rep.as_dict()
+        parity["reference"] = "f64 oracle (the cpu_baseline run) on the same prefix; near ties = top-2 gap < 1e-5"
 
     line = {
         "metric": METRIC, "value": value, "unit": "patches/s", "n_gpus": world,
@@ -381,6 +399,7 @@ def main():
                    "l2": f"inputs {N * cfg.n * 4 / 1e6:.0f} MB vs 126 MB L2 (no explicit flush)"},
         "roofline": roof,
         "cpu_baseline": cpu,
+        "parity": parity,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks,

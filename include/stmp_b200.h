@@ -86,10 +86,12 @@ void stmp_tree_free(stmp_tree* t);
  *   level), anything else is STMP_EINVAL.
  *   method: STMP_METHOD_MP / STMP_METHOD_OMP / STMP_METHOD_SELECT.
  *   tol_abs < 0 means the reference default 1e-6 * ||x|| (pursuit.py:207-209).
- * Outputs (device; optional ones may be NULL):
+ * Outputs (device; idx, coef, count and resnorm are required, path and ip
+ * may be NULL):
  *   idx[N*K] int32 selected atoms in selection order (-1 padded),
  *   coef[N*K] f32 (MP: step scores; OMP: final refit; SELECT: signed score),
- *   count[N] int32 atoms selected, resnorm[N] f32 final ||r||,
+ *   count[N] int32 atoms selected, resnorm[N] f32 final ||r|| (the staged
+ *   pipeline also keeps its per-patch iteration state in count),
  *   path[N*K*L] int32 BFS node id kept at each level (optional),
  *   ip[N*2] int32 {inner products, centroid inner products} per patch
  *   (ScoreCounter, pkg/src/stmp/dictionary.py:40-65) (optional; 8-byte aligned).

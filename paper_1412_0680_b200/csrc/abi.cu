@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -47,6 +48,20 @@ struct GraphEntry {
 std::mutex g_graph_mu;
 GraphEntry g_graph_cache[32];   // host path: 3 streams x ramped chunk sizes
 uint64_t g_graph_clock = 0;
+std::atomic<uint64_t> g_generation{0};   // handle ids: a freed handle's id is never reused
+
+// Drop every cached graph that was built for handle generation `gen` (called
+// when a dictionary or tree is freed: its graphs reference its device memory).
+void purge_graphs(uint64_t gen) {
+  std::lock_guard<std::mutex> lock(g_graph_mu);
+  for (GraphEntry& ge : g_graph_cache) {
+    if (!ge.seen) continue;
+    if ((uint64_t)ge.key.v[8] == gen || (uint64_t)ge.key.v[10] == gen) {
+      if (ge.exec) cudaGraphExecDestroy(ge.exec);
+      ge = GraphEntry();
+    }
+  }
+}
 
 int fail(int code, const char* fmt, ...) {
   char buf[1024];
@@ -175,6 +190,7 @@ int stmp_dict_create(const float* atoms, int64_t m, int32_t n, int32_t atoms_on_
   d->vpl = vpl;
   d->ld = 32 * vpl;
   d->fingerprint = fingerprint;
+  d->generation = ++g_generation;
   const size_t bytes = (size_t)m * d->ld * sizeof(float);
   cudaError_t e = cudaMalloc(&d->atoms, bytes);
   if (e == cudaSuccess) e = cudaMemsetAsync(d->atoms, 0, bytes, s);
@@ -194,8 +210,8 @@ int stmp_dict_create(const float* atoms, int64_t m, int32_t n, int32_t atoms_on_
 
 void stmp_dict_free(stmp_dict* d) {
   if (d == nullptr) return;
+  purge_graphs(d->generation);
   cudaFree(d->atoms);
-  cudaFree(d->gram);
   cudaFree(d->xtable);
   delete d;
 }
@@ -256,6 +272,7 @@ int stmp_tree_create(const stmp_dict* d, int32_t levels, const int32_t* branchin
   t->n = d->n;
   t->ld = d->ld;
   t->fingerprint = fingerprint;
+  t->generation = ++g_generation;
   t->dict = d;
   t->root_children = child_count[0];
   for (int64_t v = 0; v < ni; ++v) t->max_children = std::max(t->max_children, child_count[v]);
@@ -288,6 +305,7 @@ int stmp_tree_create(const stmp_dict* d, int32_t levels, const int32_t* branchin
 
 void stmp_tree_free(stmp_tree* t) {
   if (t == nullptr) return;
+  purge_graphs(t->generation);
   cudaFree(t->child_begin);
   cudaFree(t->child_count);
   cudaFree(t->leaf_atom);
@@ -311,11 +329,6 @@ int stmp_set_option(const char* key, int64_t value) {
     g_path_mode = (int)value;
     return STMP_OK;
   }
-  if (strcmp(key, "score_tma") == 0) {
-    if (value < 0 || value > 1) return fail(STMP_EINVAL, "score_tma must be 0 or 1");
-    stmp::g_score_tma = (int)value;
-    return STMP_OK;
-  }
   if (strcmp(key, "root_direct") == 0) {
     if (value < 0 || value > 1) return fail(STMP_EINVAL, "root_direct must be 0 or 1");
     stmp::g_root_direct = (int)value;
@@ -332,22 +345,15 @@ int stmp_set_option(const char* key, int64_t value) {
     return STMP_OK;
   }
   if (strcmp(key, "update_kernel") == 0) {
-    if (value < 0 || value > 2)
-      return fail(STMP_EINVAL, "update_kernel must be 0 (generic), 1 (K<=8 Gram-table OMP) or 2 (tile + fused root)");
-    stmp::g_update_omp8 = value >= 1 ? 1 : 0;
-    stmp::g_update_tile = value == 2 ? 1 : 0;
+    if (value < 0 || value > 1)
+      return fail(STMP_EINVAL, "update_kernel must be 0 (generic) or 1 (lockstep / wide-row OMP)");
+    stmp::g_update_omp8 = (int)value;
     return STMP_OK;
   }
   if (strcmp(key, "score_kernel") == 0) {
-    if (value < 0 || value > 3)
-      return fail(STMP_EINVAL,
-                  "score_kernel must be 0 (single-role), 1 (warp-specialized), 2 (A in TMEM) or 3 (streamed table)");
+    if (value < 2 || value > 3)
+      return fail(STMP_EINVAL, "score_kernel must be 2 (node table in shared memory) or 3 (streamed table)");
     stmp::g_score_ws = (int)value;
-    return STMP_OK;
-  }
-  if (strcmp(key, "gram") == 0) {
-    if (value < 0 || value > 1) return fail(STMP_EINVAL, "gram must be 0 or 1");
-    stmp::g_gram = (int)value;
     return STMP_OK;
   }
   if (strcmp(key, "staged_min_batch") == 0) {
@@ -399,8 +405,8 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
   g_err.clear();
   if (int rc = validate_encode(d, t, N, ldx, K, method, alpha, tol_abs)) return rc;
   if (N == 0) return STMP_OK;
-  if (X == nullptr || idx == nullptr || coef == nullptr)
-    return fail(STMP_EINVAL, "X, idx and coef must be device pointers");
+  if (X == nullptr || idx == nullptr || coef == nullptr || count == nullptr || resnorm == nullptr)
+    return fail(STMP_EINVAL, "X, idx, coef, count and resnorm must be device pointers");
   if (reinterpret_cast<uintptr_t>(ip) % 8 != 0)
     return fail(STMP_EINVAL, "ip must be 8-byte aligned (its two counters are updated as one 64-bit word)");
   if (use_staged(d, t, N, K, method)) {
@@ -422,10 +428,14 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
     }
     GraphKey k;
     memset(&k, 0, sizeof(k));
-    const void* ps[14] = {d, t, X, idx, coef, count, resnorm, path, ip, workspace, stream, nullptr, nullptr, nullptr};
+    // handles enter the key by generation, not address: a new handle allocated
+    // where a freed one lived must not replay the freed one's graph
+    const void* ps[14] = {nullptr, nullptr, X, idx, coef, count, resnorm, path, ip, workspace, stream, nullptr,
+                          nullptr, nullptr};
     for (int i = 0; i < 14; ++i) k.p[i] = ps[i];
     const int64_t vs[13] = {N, ldx, K, method, (int64_t)workspace_bytes, stmp::g_root_direct, stmp::g_score_ws,
-                            stmp::g_update_omp8, stmp::g_update_tile, stmp::g_pdl, stmp::g_score_tma, 0, stmp::g_gram};
+                            stmp::g_update_omp8, (int64_t)d->generation, stmp::g_pdl,
+                            t ? (int64_t)t->generation : 0, 0, 0};
     memcpy(k.v, vs, sizeof(vs));
     memcpy(&k.v[11], &tol, sizeof(float));
     std::lock_guard<std::mutex> lock(g_graph_mu);
@@ -525,8 +535,8 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
   g_err.clear();
   if (int rc = validate_encode(d, t, N, ldx, K, method, alpha, tol_abs)) return rc;
   if (N == 0) return STMP_OK;
-  if (X == nullptr || idx == nullptr || coef == nullptr)
-    return fail(STMP_EINVAL, "X, idx and coef must be host pointers");
+  if (X == nullptr || idx == nullptr || coef == nullptr || count == nullptr || resnorm == nullptr)
+    return fail(STMP_EINVAL, "X, idx, coef, count and resnorm must be host pointers");
   if (chunk <= 0) chunk = 1 << 17;
   if (chunk > N) chunk = N;
   // Persistent staging: device buffers and streams are kept between calls
@@ -565,8 +575,8 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
     if (rc != STMP_OK) break;
     e = cudaMemcpyAsync(idx + s0 * K, h.dI, rows * K * sizeof(int32_t), cudaMemcpyDeviceToHost, h.st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(coef + s0 * K, h.dC, rows * K * sizeof(float), cudaMemcpyDeviceToHost, h.st);
-    if (e == cudaSuccess && count) e = cudaMemcpyAsync(count + s0, h.dN, rows * sizeof(int32_t), cudaMemcpyDeviceToHost, h.st);
-    if (e == cudaSuccess && resnorm) e = cudaMemcpyAsync(resnorm + s0, h.dR, rows * sizeof(float), cudaMemcpyDeviceToHost, h.st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(count + s0, h.dN, rows * sizeof(int32_t), cudaMemcpyDeviceToHost, h.st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(resnorm + s0, h.dR, rows * sizeof(float), cudaMemcpyDeviceToHost, h.st);
     if (e == cudaSuccess && ip) e = cudaMemcpyAsync(ip + 2 * s0, h.dP, rows * 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, h.st);
     if (e != cudaSuccess) rc = cuda_fail(e, "D2H");
   }

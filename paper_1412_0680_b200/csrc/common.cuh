@@ -64,14 +64,11 @@ struct DictHandle {
   int ld = 0;              // padded row stride = 32 * vpl
   int vpl = 0;             // values per lane for the warp-per-patch kernels
   uint64_t fingerprint = 0;
-  float* gram = nullptr;   // optional [m, m] f32 atom Gram matrix (built lazily, small m only)
-  bool gram_tried = false;
+  uint64_t generation = 0; // process-unique id (the graph cache keys on it, never on the address)
   float* xtable = nullptr; // tf32 hi/lo atom blocks for the exhaustive scan (built lazily)
   bool xtable_tried = false;
 };
 
-// Gram table policy: m^2 floats must stay below this (c0: 64 MB, c1: 1 GB).
-constexpr int64_t kGramMaxAtoms = 32768;
 
 
 struct StagedLevel {
@@ -96,6 +93,7 @@ struct TreeHandle {
   int max_children = 0;         // over all internal nodes
   int max_leaf_children = 0;    // over depth-L nodes
   uint64_t fingerprint = 0;
+  uint64_t generation = 0;      // process-unique id (graph cache key)
   const DictHandle* dict = nullptr;
 };
 

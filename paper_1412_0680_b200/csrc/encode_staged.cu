@@ -27,223 +27,15 @@ using namespace sm100;
 
 int g_pdl = 1;          // programmatic dependent launch between staged kernels
 int g_root_direct = 1;  // root pass over the batch in patch order (no scan / scatter at level 0)
-int g_update_tile = 0;  // 1: tile OMP update fused with the next root scoring (update_tile.cu)
 int g_update_omp8 = 1;  // 1: lockstep OMP update (update_omp8_kernel, encode_update.cu)
 int g_update_wide = 1;  // one-CTA-per-patch OMP update for rows wider than 160 floats
-int g_gram = 0;         // 1: atom Gram table for the lockstep update (m <= kGramMaxAtoms); off: measured slower than the support-row dots (c1 update 2.09 vs 1.83 ms)
-int g_score_ws = 2;  // 0 single-role, 1 warp-specialized multi-stage, 2 A operand in TMEM (default), 3 streamed table
+int g_score_ws = 2;  // 2: A operand in TMEM, whole node table in shared memory (default); 3: streamed table
 
 namespace {
 
 constexpr int kTile = 128;          // patches per work item (= UMMA M)
 constexpr int kScoreThreads = 128;  // 4 warps: warp w owns TMEM lanes 32w..32w+31
 
-
-template <int KCH>
-__device__ __forceinline__ void issue_gather(const ScoreArgs& a, const int* rows_ids, int rows,
-                                             uint32_t a_hi_s, int tid) {
-  constexpr int F = 8 * KCH;  // float4 per residual row
-#pragma unroll 4
-  for (int e = tid; e < kTile * F; e += kScoreThreads) {
-    const int row = e / F;
-    const int c = e - row * F;
-    const uint32_t off = (uint32_t)(c >> 3) * (kTile * 128u) + sw128_offset(row, c & 7);
-    const bool ok = row < rows;
-    const float* src = a.R + (ok ? (int64_t)rows_ids[row] * a.ld + 4 * c : 0);
-    cp_async16(a_hi_s + off, src, ok ? 16u : 0u);
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-// ------------------------------------------------------------------ score (tcgen05)
-template <int KCH>
-__global__ void __launch_bounds__(kScoreThreads, 1) score_tc_kernel(ScoreArgs a) {
-  pdl_enter();
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = smem_u32(smem_raw);
-  uint8_t* base = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  constexpr int kch = KCH;
-  const int npad = a.npad;
-  const bool last = a.leaf_sel != nullptr;
-  float* Ahi = reinterpret_cast<float*>(base);
-  float* Alo = Ahi + kch * kTile * 32;
-  uint8_t* Btab = reinterpret_cast<uint8_t*>(Alo + kch * kTile * 32);
-  const uint32_t tbytes = table_bytes(kch, npad, last);
-  const int* s_leaf_info = reinterpret_cast<const int*>(Btab + (size_t)kch * 2 * npad * 128);
-  const int* s_leaf_cnt = s_leaf_info + npad;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(Btab + ((tbytes + 15u) & ~15u));
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
-  int* s_rows = reinterpret_cast<int*>(tmem_slot + 4);  // [2][kTile] double-buffered patch ids
-  int* s_hist = s_rows + 2 * kTile;                      // [256] local counts of the winning child
-
-  if (warp == 0) tmem_alloc(tmem_slot, a.tmem_cols);
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-  }
-  for (int i = tid; i < 256; i += kScoreThreads) s_hist[i] = 0;
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  const int num_items = *a.num_items;
-  const int per = (num_items + gridDim.x - 1) / gridDim.x;
-  const int i0 = blockIdx.x * per;
-  const int i1 = min(num_items, i0 + per);
-  const uint32_t idesc = idesc_tf32(kTile, npad);
-  const uint32_t a_hi_s = smem_u32(Ahi), a_lo_s = smem_u32(Alo), b_s = smem_u32(Btab);
-  constexpr int F = 8 * KCH;
-  uint32_t tab_phase = 0, mma_phase = 0;
-  int loaded_bin = -1;
-
-  // prologue: first item's rows, table and gather in flight
-  int4 it = i0 < i1 ? a.items[i0] : make_int4(0, 0, 0, 0);
-  if (i0 < i1) {
-    if (tid < it.z) s_rows[tid] = a.perm[it.y + tid];
-    if (tid == 0) {
-      mbar_arrive_expect_tx(&bars[0], tbytes);
-      const uint8_t* src = reinterpret_cast<const uint8_t*>(a.table) + (size_t)it.x * tbytes;
-      for (uint32_t off = 0; off < tbytes; off += 65536u)
-        bulk_g2s(Btab + off, src + off, min(65536u, tbytes - off), &bars[0]);
-    }
-    loaded_bin = it.x;
-    __syncthreads();
-    issue_gather<KCH>(a, s_rows, it.z, a_hi_s, tid);
-  }
-  bool table_pending = i0 < i1;
-
-  for (int item = i0; item < i1; ++item) {
-    const int buf = (item - i0) & 1;
-    const int* rows_ids = s_rows + buf * kTile;
-    const int bin = it.x, rows = it.z;
-    const int gnode = a.level_base + bin;
-    const int cb = __ldg(a.child_begin + gnode);
-    const int cc = __ldg(a.child_count + gnode);
-
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-    // split the gathered rows into tf32 hi / lo planes in place
-#pragma unroll 4
-    for (int e = tid; e < kTile * F; e += kScoreThreads) {
-      const int row = e / F;
-      const int c = e - row * F;
-      const uint32_t off = (uint32_t)(c >> 3) * (kTile * 128u) + sw128_offset(row, c & 7);
-      float4* ph = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Ahi) + off);
-      const float4 v = *ph;
-      float4 h, l;
-      h.x = tf32_hi(v.x); h.y = tf32_hi(v.y); h.z = tf32_hi(v.z); h.w = tf32_hi(v.w);
-      l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
-      *ph = h;
-      *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(Alo) + off) = l;
-    }
-    fence_proxy_async_smem();
-    __syncthreads();
-
-    if (tid == 0) {
-      if (table_pending) {
-        mbar_wait(&bars[0], tab_phase);
-        tab_phase ^= 1u;
-      }
-      tc_fence_after();
-#pragma unroll
-      for (int kc = 0; kc < kch; ++kc) {
-        const uint32_t ah = a_hi_s + kc * (kTile * 128u);
-        const uint32_t al = a_lo_s + kc * (kTile * 128u);
-        const uint32_t bh = b_s + kc * (2u * npad * 128u);
-        const uint32_t bl = bh + npad * 128u;
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const uint32_t o = ks * 32u;
-          mma_tf32(tmem, sw128_kmajor_desc(ah + o), sw128_kmajor_desc(bh + o), idesc, (kc | ks) ? 1u : 0u);
-          mma_tf32(tmem, sw128_kmajor_desc(ah + o), sw128_kmajor_desc(bl + o), idesc, 1u);
-          mma_tf32(tmem, sw128_kmajor_desc(al + o), sw128_kmajor_desc(bh + o), idesc, 1u);
-        }
-      }
-      mma_commit(&bars[1]);
-    }
-    table_pending = false;
-    __syncwarp();
-    mbar_wait(&bars[1], mma_phase);
-    mma_phase ^= 1u;
-    tc_fence_after();
-
-    // A planes are free again: start the next item's gather (and its table if
-    // the bin changes) before this item's epilogue, so the loads overlap it
-    int4 nit = make_int4(0, 0, 0, 0);
-    const bool has_next = item + 1 < i1;
-    int nperm = 0;
-    if (has_next) {
-      nit = a.items[item + 1];
-      if (tid < nit.z) nperm = a.perm[nit.y + tid];  // consumed after the argmax
-    }
-    int best = 0;
-    float bestv = -1.f;
-    for (int col0 = 0; col0 < npad; col0 += 32) {
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)col0, v);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float m = fabsf(v[j]);
-        if (col0 + j < cc && m > bestv) {
-          bestv = m;
-          best = col0 + j;
-        }
-      }
-    }
-    const int row = tid;
-    const bool valid = row < rows;
-    const int p = valid ? rows_ids[row] : 0;
-    const int child = cb + best;
-    int leaf_info = 0, leaf_cnt = 0;
-    if (last && valid) {  // read before a table refill overwrites the block
-      leaf_info = s_leaf_info[best];
-      leaf_cnt = s_leaf_cnt[best];
-    }
-    if (has_next && tid < nit.z) s_rows[(buf ^ 1) * kTile + tid] = nperm;
-    fence_proxy_async_smem();  // leaf metadata reads before the async-proxy table refill
-    __syncthreads();  // s_rows of the next item visible; leaf metadata read
-    if (has_next) {
-      const bool new_tab = nit.x != loaded_bin;
-      if (new_tab && tid == 0) {
-        mbar_arrive_expect_tx(&bars[0], tbytes);
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.table) + (size_t)nit.x * tbytes;
-        for (uint32_t off = 0; off < tbytes; off += 65536u)
-          bulk_g2s(Btab + off, src + off, min(65536u, tbytes - off), &bars[0]);
-      }
-      table_pending = new_tab;
-      loaded_bin = nit.x;
-      issue_gather<KCH>(a, s_rows + (buf ^ 1) * kTile, nit.z, a_hi_s, tid);
-    }
-
-    if (valid) {
-      a.path_ws[(int64_t)p * a.L + a.level] = child;
-      if (a.path_out) a.path_out[((int64_t)p * a.K + a.count[p]) * a.L + a.level] = child;
-      if (a.next_counts) atomicAdd(&s_hist[best], 1);
-      if (last) a.leaf_sel[p] = leaf_info;
-      if (a.ip) {  // ScoreCounter: cc centroids at this level (+ the leaf atoms), fire-and-forget
-        add_ip(a.ip, p, cc + leaf_cnt, cc);
-      }
-    }
-    if (a.next_counts) {
-      __syncthreads();
-      for (int j = tid; j < cc; j += kScoreThreads) {
-        const int h = s_hist[j];
-        if (h) atomicAdd(&a.next_counts[cb + j - a.next_base], h);
-        s_hist[j] = 0;
-      }
-    }
-    tc_fence_before();
-    it = nit;
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 0) tmem_dealloc(tmem, a.tmem_cols);
-}
 
 // ------------------------------------------------------------------ scan (one CTA)
 constexpr int kScanThreads = 1024;
@@ -470,16 +262,6 @@ __global__ void __launch_bounds__(256) scatter_root_kernel(int64_t N, const int*
   if (act) perm[offsets[0] + base + warp_off[warp] + __popc(m & ((1u << lane) - 1u))] = (int)p;
 }
 
-template <int KCH>
-cudaError_t launch_score(const ScoreArgs& s, int sms, cudaStream_t st) {
-  const size_t smem = score_smem_bytes(KCH, s.npad);
-  cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<KCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const int per_sm = std::max(1, (int)((227 * 1024) / smem));
-  const int grid = sms * std::min(per_sm, 2);
-  return launch_kernel(score_tc_kernel<KCH>, grid, kScoreThreads, smem, st, true, s);
-}
-
 }  // namespace
 
 size_t score_smem_bytes(int kchunks, int npad) {
@@ -688,10 +470,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   u.tol_abs = tol_abs; u.idx = idx; u.coef = coef; u.count = count; u.resnorm = resnorm;
   u.ip = ip; u.path_out = path; u.Lf = Lf; u.yv = yv; u.tol = tol; u.active = active;
   u.root_count = stripes; u.N = N; u.S_ws = S_ws; u.c_ws = c_ws; u.leaf_sel = leaf_sel;
-  // lockstep OMP update (update_omp8_kernel): K <= 8 with rows of <= 160 floats or K <= 16 with <= 128; the
-  // atom Gram table when the dictionary is small enough, dot products otherwise
+  // lockstep OMP update (update_omp8_kernel): K <= 8 with rows of <= 160 floats or K <= 16 with <= 64
   const bool lockstep = method == kMethodOMP && lockstep_lanes(d->ld, K) != 0 && g_update_omp8;
-  u.gram = lockstep && g_gram && K <= 8 ? ensure_gram(const_cast<DictHandle*>(d), st) : nullptr;
   u.m = d->m;
   // stage the support atoms in shared memory when the patch groups fit comfortably
   u.cache_atoms = update_smem_bytes(uc, K, d->ld, true) <= 96 * 1024 ? 1 : 0;
@@ -716,14 +496,10 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   const int scatter_blocks = (int)((N + 255) / 256);
   const size_t usmem = update_smem_bytes(uc, K, d->ld, u.cache_atoms != 0);
   const bool wide = method == kMethodOMP && !lockstep && g_update_wide && wide_update_cpt(d->ld) != 0;
-  // tile update: OMP refit + next-iteration root scoring in one kernel
-  const bool tile = t && g_update_tile && u.gram != nullptr && update_tile_supported(d, t, K, method);
   // the root bin holds every active patch: its pass can walk the batch in patch
   // order (inactive rows skipped) instead of compacting them (score_ts / score_st /
   // exact_scan only)
-  const bool root_direct = g_root_direct && !tile && (!t || g_score_ws >= 2 ||
-                                                      score_smem_bytes(d->ld / 32, t->staged_levels[0].npad) >
-                                                          227 * 1024);
+  const bool root_direct = g_root_direct != 0;
   if (root_direct) u.root_count = nullptr;
   const float* xtable = t ? nullptr : ensure_xtable(const_cast<DictHandle*>(d), st);
   if (!t && xtable == nullptr) return cudaErrorMemoryAllocation;
@@ -748,7 +524,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       s.ks_last = (d->n - 32 * (s.kchunks - 1) + 7) / 8;
       if ((e = launch_exact_scan(s, sms, st)) != cudaSuccess) return e;
     }
-    for (int l = (tile && it > 0) ? 1 : 0; l < L; ++l) {
+    for (int l = 0; l < L; ++l) {
       const StagedLevel& lv = t->staged_levels[l];
       const int nb = (int)(t->level_offsets[l + 1] - t->level_offsets[l]);
       const bool direct_pass = l == 0 && root_direct;
@@ -795,50 +571,17 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       }
       s.tmem_cols = lv.tmem_cols;
       const bool whole = score_smem_bytes(s.kchunks, lv.npad) <= 227 * 1024;
-      if (g_score_ws == 3 || !whole) {
+      if (g_score_ws == 3 || !whole || !score_ts_fits(s.kchunks, lv.npad, l + 1 == L))
         e = launch_score_st(s, sms, st);
-      } else if (g_score_ws == 2 && score_ts_fits(s.kchunks, lv.npad, l + 1 == L)) {
+      else
         e = launch_score_ts(s, sms, st);
-      } else if (g_score_ws == 1 && score_ws_fits(s.kchunks, lv.npad, l + 1 == L)) {
-        int cols = 32;
-        while (cols < 2 * lv.npad) cols <<= 1;
-        s.tmem_cols = cols;
-        e = launch_score_ws(s, sms, st);
-      } else switch (s.kchunks) {
-        case 1: e = launch_score<1>(s, sms, st); break;
-        case 2: e = launch_score<2>(s, sms, st); break;
-        case 3: e = launch_score<3>(s, sms, st); break;
-        case 4: e = launch_score<4>(s, sms, st); break;
-        case 5: e = launch_score<5>(s, sms, st); break;
-        case 6: e = launch_score<6>(s, sms, st); break;
-        case 8: e = launch_score<8>(s, sms, st); break;
-        default: e = cudaErrorInvalidValue;
-      }
       if (e != cudaSuccess) return e;
     }
     u.R_in = it == 0 ? R0 : R;
-    if (tile) {
-      TileArgs ta{};
-      ta.u = u;
-      ta.S_ws = S_ws;
-      ta.c_ws = c_ws;
-      ta.root_table = t->staged_tables[0];
-      ta.root_npad = t->staged_levels[0].npad;
-      ta.root_cc = t->root_children;
-      ta.root_cb = (int)t->level_offsets[1];
-      ta.next_counts = counts_of(it + 1) + bin_off[1];
-      ta.next_base = (int)t->level_offsets[1];
-      ta.path_ws = path_ws;
-      ta.L = L;
-      ta.iter = it;
-      ta.do_root = it + 1 < K ? 1 : 0;
-      e = launch_update_tile(ta, st);
-    } else {
-      u.iter = it;
-      if (lockstep) e = launch_update_omp8(u, st);
-      else if (wide) e = launch_update_wide(u, st);
-      else e = launch_update(uc, u, ublocks, usmem, st);
-    }
+    u.iter = it;
+    if (lockstep) e = launch_update_omp8(u, st);
+    else if (wide) e = launch_update_wide(u, st);
+    else e = launch_update(uc, u, ublocks, usmem, st);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -500,15 +500,7 @@ __global__ void __launch_bounds__(128) update_wide_kernel(UpdateArgs a) {
 #ifndef STMP_OMP8_MINBW
 #define STMP_OMP8_MINBW 5   // rows of 96-160 floats
 #endif
-#ifndef STMP_SUP_SMEM
-#define STMP_SUP_SMEM 1
-#endif
-// support rows through shared memory (cp.async) only while they are few: at
-// larger T the shared-memory footprint costs more L1 than it saves latency
-template <int T, bool GRAM>
-constexpr bool sup_smem() { return STMP_SUP_SMEM && GRAM && T >= 1 && T <= 3; }
-// GRAM = false (dictionaries too large for a Gram table): the Gram column is
-// T group dot products against the support rows, which the residual rebuild
+// The Gram column is T group dot products against the support rows, which the residual rebuild
 // reads again (from L1 / L2).
 // G = 16 lanes per patch (rows of <= 128 floats) lifts the support limit to 16.
 //
@@ -565,11 +557,10 @@ __device__ __forceinline__ void group_reduce_scatter_n(float (&p)[NR * G], int g
 
 // Lane gl owns rows gl + G * i (i < NR) of the inverse Cholesky factor M (and the
 // matching y_j, c_j): NR = 1 while the support fits the group, 2 up to 2G atoms.
-template <int G, int CPL, int T, bool GRAM>
+template <int G, int CPL, int T>
 __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T < G ? STMP_OMP8_MINB : 5))
                                                 : STMP_OMP8_MINBW)
     update_omp8_kernel(UpdateArgs a) {
-  constexpr bool kSupSmem = sup_smem<T, GRAM>();
   constexpr int NR = T < G ? 1 : 2;     // Cholesky rows per lane
   constexpr int NV = NR * G;            // reduce-scatter width
   static_assert(T < 2 * G, "lockstep support index must fit two rows per lane");
@@ -636,21 +627,6 @@ __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T
       if (in && (mv > bestv || (mv == bestv && aj < atom))) { bestv = mv; atom = aj; }
     }
   }
-  // support rows, needed after the refit: cp.async into this group's shared
-  // slice now, so their L2 round trip overlaps the new atom's
-  extern __shared__ float4 s_sup[];   // [128 / G groups][T][F] 16-byte chunks
-  float4* sup = s_sup + (size_t)((threadIdx.x / G) * T) * F;
-  if constexpr (kSupSmem) {
-#pragma unroll
-    for (int k = 0; k < T; ++k)
-#pragma unroll
-      for (int i = 0; i < CPL; ++i) {
-        const int ch = gl + G * i;
-        if (ch < F)
-          sm100::cp_async16(sm100::smem_u32(sup + k * F + ch), a.atoms + (int64_t)S[k] * a.ld + 4 * ch, 16u);
-      }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
   Sl av;
   av.load(a.atoms + (int64_t)atom * a.ld, gl, F);
   float g[T + 1];
@@ -658,13 +634,7 @@ __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T
 #pragma unroll
   for (int k = 0; k < T; ++k) dup |= S[k] == atom;
   float gtt, bt;
-  if constexpr (GRAM) {
-    const float* grow = a.gram + (int64_t)atom * a.m;
-#pragma unroll
-    for (int k = 0; k < T; ++k) g[k] = __ldg(grow + S[k]);
-    gtt = __ldg(grow + atom);
-    bt = gsum_full<G>(av.dot(x));
-  } else {
+  {
     // value k < T: a . a_{S_k};  T: a . a;  T + 1: a . x (if it fits)
     float pv[NV];
 #pragma unroll
@@ -746,15 +716,13 @@ __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T
     Sl r;
 #pragma unroll
     for (int i = 0; i < CPL * 4; ++i) r.v[i] = fmaf(-c[T], av.v[i], x.v[i]);
-    if constexpr (kSupSmem) asm volatile("cp.async.wait_all;" ::: "memory");   // own copies only: no barrier
 #pragma unroll
     for (int k = 0; k < T; ++k)
 #pragma unroll
       for (int i = 0; i < CPL; ++i) {
         const int ch = gl + G * i;
         if (ch < F) {
-          const float4 q = kSupSmem ? sup[k * F + ch]
-                                    : __ldg(reinterpret_cast<const float4*>(a.atoms + (int64_t)S[k] * a.ld) + ch);
+          const float4 q = __ldg(reinterpret_cast<const float4*>(a.atoms + (int64_t)S[k] * a.ld) + ch);
           r.v[4 * i] = fmaf(-c[k], q.x, r.v[4 * i]);
           r.v[4 * i + 1] = fmaf(-c[k], q.y, r.v[4 * i + 1]);
           r.v[4 * i + 2] = fmaf(-c[k], q.z, r.v[4 * i + 2]);
@@ -787,8 +755,6 @@ __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T
         a.resnorm[p] = rn;
       }
     }
-  } else if constexpr (kSupSmem) {
-    asm volatile("cp.async.wait_all;" ::: "memory");   // no copy may outlive the CTA's smem
   }
   if (act && !act_next) {
     // final rows of the caller's idx / coef (T or T + 1 entries; the rest stay -1 / 0 from init)
@@ -823,30 +789,17 @@ cudaError_t launch_update_omp8(const UpdateArgs& a, cudaStream_t st) {
   if (G == 0 || a.method != kMethodOMP || a.S_ws == nullptr) return cudaErrorNotSupported;
   const int blocks = (int)((a.N + (128 / G) - 1) / (128 / G));
   const int cpl = (a.ld / 4 + G - 1) / G;
-  const int gram = a.gram != nullptr ? 1 : 0;
-  switch (((G * 8 + cpl) * 16 + a.iter) * 2 + gram) {
-#define STMP_OMP8_CASE(g, cp, t, gr)                                                                   \
-  case ((g * 8 + cp) * 16 + t) * 2 + gr: {                                                           \
-    const size_t smem = sup_smem<t, gr != 0>() ? (size_t)(128 / g) * t * (a.ld / 4) * 16 : 0;       \
-    if (smem > 48 * 1024) {                                                                          \
-      cudaError_t err = cudaFuncSetAttribute(update_omp8_kernel<g, cp, t, gr != 0>,                  \
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-      if (err != cudaSuccess) return err;                                                            \
-    }                                                                                                \
-    return launch_kernel(update_omp8_kernel<g, cp, t, gr != 0>, blocks, 128, smem, st, true, a);    \
-  }
-#define STMP_OMP8_ITERS(g, cp, gr)                                                                      \
-  STMP_OMP8_CASE(g, cp, 0, gr) STMP_OMP8_CASE(g, cp, 1, gr) STMP_OMP8_CASE(g, cp, 2, gr)               \
-  STMP_OMP8_CASE(g, cp, 3, gr) STMP_OMP8_CASE(g, cp, 4, gr) STMP_OMP8_CASE(g, cp, 5, gr)               \
-  STMP_OMP8_CASE(g, cp, 6, gr) STMP_OMP8_CASE(g, cp, 7, gr)
-#define STMP_OMP16_ITERS(cp, gr)                                                                        \
-  STMP_OMP8_CASE(8, cp, 8, gr) STMP_OMP8_CASE(8, cp, 9, gr) STMP_OMP8_CASE(8, cp, 10, gr)                   \
-  STMP_OMP8_CASE(8, cp, 11, gr) STMP_OMP8_CASE(8, cp, 12, gr) STMP_OMP8_CASE(8, cp, 13, gr)                 \
-  STMP_OMP8_CASE(8, cp, 14, gr) STMP_OMP8_CASE(8, cp, 15, gr)
-    STMP_OMP8_ITERS(8, 1, 1) STMP_OMP8_ITERS(8, 2, 1) STMP_OMP8_ITERS(8, 3, 1) STMP_OMP8_ITERS(8, 4, 1)
-    STMP_OMP8_ITERS(8, 5, 1) STMP_OMP8_ITERS(8, 1, 0) STMP_OMP8_ITERS(8, 2, 0) STMP_OMP8_ITERS(8, 3, 0)
-    STMP_OMP8_ITERS(8, 4, 0) STMP_OMP8_ITERS(8, 5, 0)
-    STMP_OMP16_ITERS(1, 0) STMP_OMP16_ITERS(2, 0)
+  switch ((G * 8 + cpl) * 16 + a.iter) {
+#define STMP_OMP8_CASE(g, cp, t) \
+  case (g * 8 + cp) * 16 + t: return launch_kernel(update_omp8_kernel<g, cp, t>, blocks, 128, 0, st, true, a);
+#define STMP_OMP8_ITERS(g, cp)                                                                          \
+  STMP_OMP8_CASE(g, cp, 0) STMP_OMP8_CASE(g, cp, 1) STMP_OMP8_CASE(g, cp, 2) STMP_OMP8_CASE(g, cp, 3) \
+  STMP_OMP8_CASE(g, cp, 4) STMP_OMP8_CASE(g, cp, 5) STMP_OMP8_CASE(g, cp, 6) STMP_OMP8_CASE(g, cp, 7)
+#define STMP_OMP16_ITERS(cp)                                                                            \
+  STMP_OMP8_CASE(8, cp, 8) STMP_OMP8_CASE(8, cp, 9) STMP_OMP8_CASE(8, cp, 10) STMP_OMP8_CASE(8, cp, 11) \
+  STMP_OMP8_CASE(8, cp, 12) STMP_OMP8_CASE(8, cp, 13) STMP_OMP8_CASE(8, cp, 14) STMP_OMP8_CASE(8, cp, 15)
+    STMP_OMP8_ITERS(8, 1) STMP_OMP8_ITERS(8, 2) STMP_OMP8_ITERS(8, 3) STMP_OMP8_ITERS(8, 4) STMP_OMP8_ITERS(8, 5)
+    STMP_OMP16_ITERS(1) STMP_OMP16_ITERS(2)
 #undef STMP_OMP16_ITERS
 #undef STMP_OMP8_ITERS
 #undef STMP_OMP8_CASE

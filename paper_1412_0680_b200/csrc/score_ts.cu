@@ -9,7 +9,6 @@
 // footprint to one landing plane + one table, so four CTAs share an SM.  The
 // next tile's gather is launched as soon as its rows are staged in TMEM, so it
 // overlaps the MMAs and the argmax epilogue.
-#include <cuda.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -83,12 +82,8 @@ __device__ __forceinline__ void gather_rows(const ScoreArgs& a, const int* rows_
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// TMA = true: the tile's rows arrive by tensor-map gathers (tile::gather4, four
-// rows per instruction, issued by one warp, completion on bars[2]) instead of
-// 16-byte cp.async per thread and chunk -- the issue cost of the gather drops
-// from 16 instructions per row to half an instruction per row.
-template <int KCH, bool TMA>
-__global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, const __grid_constant__ CUtensorMap rmap) {
+template <int KCH>
+__global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* base = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -116,27 +111,8 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
   }
   for (int i = tid; i < 256; i += kThreads) s_hist[i] = 0;
   const int lane = tid & 31;
-  uint32_t g_phase = 0;
   // gather of one tile's rows (ids[0..rows)) into the landing plane
-  auto issue_gather = [&](const int* ids, int rows) {
-    if constexpr (TMA) {
-      if (warp == 0) {
-        if (lane == 0) {
-          fence_proxy_async_smem();
-          mbar_arrive_expect_tx(&bars[2], (uint32_t)KCH * kT * 128u);
-        }
-        __syncwarp();
-        const int r = 4 * lane;
-        const int q0 = r < rows ? ids[r] : -1, q1 = r + 1 < rows ? ids[r + 1] : -1;
-        const int q2 = r + 2 < rows ? ids[r + 2] : -1, q3 = r + 3 < rows ? ids[r + 3] : -1;
-#pragma unroll
-        for (int kc = 0; kc < KCH; ++kc)
-          tma_gather4(smem_u32(raw) + kc * (kT * 128u) + lane * 512u, &rmap, 32 * kc, q0, q1, q2, q3, &bars[2]);
-      }
-    } else {
-      gather_rows<KCH>(a, ids, rows, smem_u32(raw), tid);
-    }
-  };
+  auto issue_gather = [&](const int* ids, int rows) { gather_rows<KCH>(a, ids, rows, smem_u32(raw), tid); };
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -183,13 +159,8 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
     const int4 nit = has_next ? item_at(a, item + 1) : make_int4(0, 0, 0, 0);
     const int nperm = (has_next && tid < nit.z) ? row_at(a, nit, tid) : 0;
 
-    if constexpr (TMA) {
-      mbar_wait(&bars[2], g_phase);
-      g_phase ^= 1u;
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      __syncthreads();
-    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
     const int row = tid;
 #pragma unroll
     for (int kc = 0; kc < KCH; ++kc) {
@@ -308,36 +279,6 @@ __global__ void __launch_bounds__(kThreads, 4) score_ts_kernel(ScoreArgs a, cons
   if (warp == 0) tmem_dealloc(tmem, a.tmem_cols);
 }
 
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_tiled() {
-  static const EncodeTiledFn fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return static_cast<EncodeTiledFn>(nullptr);
-    return reinterpret_cast<EncodeTiledFn>(p);
-  }();
-  return fn;
-}
-
-// Tensor map of the residual rows [nrows, ld] f32: 32-column (128-byte) boxes
-// of one row, 128-byte swizzle -- the unit tile::gather4 moves four of.
-bool make_row_map(CUtensorMap* m, const float* base, int64_t nrows, int ld) {
-  const EncodeTiledFn fn = encode_tiled();
-  if (fn == nullptr || reinterpret_cast<uintptr_t>(base) % 16 != 0 || nrows <= 0 || nrows >= (1ll << 31)) return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)nrows};
-  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  const cuuint32_t box[2] = {32, 1};
-  const cuuint32_t estr[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <int KCH>
 cudaError_t launch_ts_kch(ScoreArgs s, int sms, cudaStream_t st) {
   const bool last = s.leaf_sel != nullptr;
@@ -345,21 +286,16 @@ cudaError_t launch_ts_kch(ScoreArgs s, int sms, cudaStream_t st) {
   int cols = 32;
   while (cols < (int)kColAcc + s.npad) cols <<= 1;
   s.tmem_cols = cols;
-  CUtensorMap map;
-  memset(&map, 0, sizeof(map));
-  const bool tma = g_score_tma && make_row_map(&map, s.R, s.nrows, s.ld);
-  auto kern = tma ? score_ts_kernel<KCH, true> : score_ts_kernel<KCH, false>;
+  auto kern = score_ts_kernel<KCH>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int by_smem = (int)((228 * 1024) / (smem + 1024));
   const int by_tmem = 512 / cols;
   const int per_sm = std::max(1, std::min(4, std::min(by_smem, by_tmem)));
-  return launch_kernel(kern, sms * per_sm, kThreads, smem, st, true, s, map);
+  return launch_kernel(kern, sms * per_sm, kThreads, smem, st, true, s);
 }
 
 }  // namespace
-
-int g_score_tma = 0;  // measured slower than per-thread cp.async on c1 (72.9 vs 65.7 us per pass)
 
 bool score_ts_fits(int kchunks, int npad, bool last) {
   if (kchunks < 1 || kchunks > 4 || npad > 256) return false;

@@ -84,35 +84,14 @@ struct UpdateArgs {
 
   int* root_count;       // kRootStripes counters of the next root bin
   const int* leaf_sel;   // written by the last score pass
-  const float* gram;     // optional [m, m] atom Gram matrix (enables the 8-lane OMP kernel)
   int64_t m;
   int cache_atoms;       // stage the support atoms in shared memory
   int64_t N;
-  // lockstep OMP kernels (update_omp8 / update_tile): state laid out [entry][patch]
+  // lockstep OMP kernel (update_omp8): state laid out [entry][patch]
   int* S_ws;             // support atoms [K][N]
   float* c_ws;           // coefficients [K][N]
   int iter;              // iteration index = support size of every active patch
 };
-
-// Tile-based OMP update + next-iteration root scoring (update_tile.cu).  Uses the
-// [entry][patch] state layout: Lf [K(K+1)/2][N], yv [K][N], S_ws [K][N], c_ws [K][N].
-struct TileArgs {
-  UpdateArgs u;
-  int* S_ws;
-  float* c_ws;
-  const float* root_table;  // staged table block of the root (bin 0, level 0)
-  int root_npad, root_cc, root_cb;
-  int* next_counts;         // level-1 bin counters
-  int next_base;
-  int* path_ws;
-  int L;
-  int iter;                 // iteration index (= support size of every active patch)
-  int do_root;              // score the root for the next iteration
-  int tmem_cols;
-};
-bool update_tile_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
-cudaError_t launch_update_tile(const TileArgs& a, cudaStream_t st);
-extern int g_update_tile;
 
 struct UpdateCfg {
   int G = 0;   // lanes per patch
@@ -125,9 +104,9 @@ cudaError_t launch_init(const UpdateCfg& c, const UpdateArgs& a, int blocks, cud
 cudaError_t launch_update(const UpdateCfg& c, const UpdateArgs& a, int blocks, size_t smem,
                           cudaStream_t st);
 size_t update_smem_bytes(const UpdateCfg& c, int K, int ld, bool cache_atoms);
-// OMP update specialised for K <= 8 with a Gram table: one lane per Cholesky row,
-// all solver state in registers, support size a.iter fixed at compile time,
-// state in the [entry][patch] layout.  Returns cudaErrorNotSupported when not applicable.
+// Lockstep OMP update (K <= 8 with rows of <= 160 floats, K <= 16 with <= 64):
+// 8 lanes per patch, each owning one or two rows of the inverse Cholesky factor,
+// support size a.iter fixed at compile time, state in the [entry][patch] layout.  Returns cudaErrorNotSupported when not applicable.
 cudaError_t launch_update_omp8(const UpdateArgs& a, cudaStream_t st);
 // OMP update with one CTA per patch for rows wider than 160 floats (0: not applicable)
 int wide_update_cpt(int ld);
@@ -135,9 +114,6 @@ cudaError_t launch_update_wide(const UpdateArgs& a, cudaStream_t st);
 extern int g_update_wide;
 // lanes per patch of the lockstep OMP update for this shape (8 or 16), 0 if unsupported
 int lockstep_lanes(int ld, int K);
-// Build the [m, m] Gram matrix of the (padded) dictionary on `st`; returns nullptr if
-// m exceeds kGramMaxAtoms or memory is short.
-const float* ensure_gram(DictHandle* d, cudaStream_t st);
 
 size_t score_smem_bytes(int kchunks, int npad);
 
@@ -149,12 +125,8 @@ __host__ __device__ inline uint32_t table_bytes(int kch, int npad, bool last) {
 }
 
 extern int g_score_ws;
-extern int g_score_tma;   // score_ts: tensor-map gathers (1) or per-thread cp.async (0)
 extern int g_update_omp8;
-extern int g_gram;
 extern int g_root_direct;
-bool score_ws_fits(int kchunks, int npad, bool last);
-cudaError_t launch_score_ws(const ScoreArgs& s, int sms, cudaStream_t st);
 bool score_ts_fits(int kchunks, int npad, bool last);
 // exhaustive selection (exact_scan.cu): dictionary blocks of xtable_block_width(ld)
 // atoms; a.table = ensure_xtable(d), a.npad = block width, a.leaf_sel = best atom

@@ -58,6 +58,21 @@ def code_patches(measured, dc_meas, selector, pd, params: SearchParams, threads:
     """
     import torch
     del threads
+    if stream is not None:
+        # every allocation, launch and host read runs on `stream`; the caller's
+        # stream then waits for it before the outputs are used
+        cur = torch.cuda.current_stream()
+        stream.wait_stream(cur)
+        with torch.cuda.stream(stream):
+            out = _code_patches(measured, dc_meas, selector, pd, params, method)
+        cur.wait_stream(stream)
+        return out
+    return _code_patches(measured, dc_meas, selector, pd, params, method)
+
+
+def _code_patches(measured, dc_meas, selector, pd, params, method):
+    import torch
+    stream = None   # the current stream (set by code_patches)
     on_device = isinstance(measured, torch.Tensor) and measured.is_cuda
     Y = _as_cuda_f32(measured)
     N, n_meas = Y.shape

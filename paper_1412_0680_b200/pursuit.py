@@ -16,9 +16,11 @@ SURVEY F4); other alphas raise ``ValueError`` instead of silently differing.
 
 from __future__ import annotations
 
+from collections import OrderedDict
 from dataclasses import dataclass, field
 import math
 import os
+import weakref
 
 import numpy as np
 
@@ -270,26 +272,51 @@ class _GpuSelector:
         return encode(self, X, K, method=method, tol=tol, paths=paths, stream=stream)
 
 
-_GPU_DICT_CACHE: dict = {}
+# Device copies of dictionaries: weakly keyed by the caller's Dictionary object
+# (dropped with it), and a small LRU for bare arrays keyed by content
+# (fingerprint, shape), so repeated selectors over the same array share one copy.
+_GPU_DICT_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_BARE_CACHE: OrderedDict = OrderedDict()
+_BARE_CACHE_SIZE = 4
 
 
 def _gpu_dict_for(dictionary) -> GpuDictionary:
-    key = id(dictionary)
-    hit = _GPU_DICT_CACHE.get(key)
-    if hit is not None and hit[0] is dictionary:
-        return hit[1]
+    try:
+        hit = _GPU_DICT_CACHE.get(dictionary)
+    except TypeError:          # not weak-referenceable: no cache
+        hit = None
+    if hit is not None:
+        return hit
     fp = dictionary.fingerprint() if hasattr(dictionary, "fingerprint") else None
     g = GpuDictionary(dictionary, fingerprint=fp)
-    _GPU_DICT_CACHE[key] = (dictionary, g)
+    try:
+        _GPU_DICT_CACHE[dictionary] = g
+    except TypeError:
+        pass
     return g
+
+
+def _as_dictionary(dictionary):
+    """The caller's Dictionary, or a shared wrapper for a bare atom array."""
+    if hasattr(dictionary, "atoms"):
+        return dictionary
+    d = Dictionary(dictionary)
+    key = (d.fingerprint(), d.atoms.shape)
+    hit = _BARE_CACHE.get(key)
+    if hit is not None:
+        _BARE_CACHE.move_to_end(key)
+        return hit
+    _BARE_CACHE[key] = d
+    while len(_BARE_CACHE) > _BARE_CACHE_SIZE:
+        _BARE_CACHE.popitem(last=False)
+    return d
 
 
 class ExactSelector(_GpuSelector):
     """GPU ``ExactSelector`` (pursuit.py:165-172)."""
 
     def __init__(self, dictionary):
-        if not hasattr(dictionary, "atoms"):
-            dictionary = Dictionary(dictionary)
+        dictionary = _as_dictionary(dictionary)
         self.dictionary = dictionary
         self.gdict = _gpu_dict_for(dictionary)
         self.tree = None
@@ -301,8 +328,7 @@ class TreeSelector(_GpuSelector):
     def __init__(self, tree, dictionary, alpha: float):
         if not 0.0 < alpha <= 1.0:
             raise ValueError(f"alpha must lie in (0, 1], got {alpha}")
-        if not hasattr(dictionary, "atoms"):
-            dictionary = Dictionary(dictionary)
+        dictionary = _as_dictionary(dictionary)
         flat = as_flat_tree(tree)
         fp = dictionary.fingerprint() if hasattr(dictionary, "fingerprint") else fingerprint_atoms(dictionary.atoms)
         if flat.fingerprint != fp:
@@ -344,6 +370,19 @@ def encode(selector, X, K: int, method: str = "omp", tol: float | None = None,
     g = selector.gdict
     if X.shape[1] != g.n:
         raise ValueError(f"patches have dimension {X.shape[1]}, dictionary atoms have {g.n}")
+    if stream is not None:
+        # allocate the outputs and the workspace on the launch stream, so the
+        # caching allocator never hands them to another stream while the
+        # kernels still run; the stream first waits for the producer of X
+        stream.wait_stream(torch.cuda.current_stream(X.device))
+        with torch.cuda.stream(stream):
+            return _encode_on_stream(selector, X, K, method, tol, paths, stream)
+    return _encode_on_stream(selector, X, K, method, tol, paths, None)
+
+
+def _encode_on_stream(selector, X, K, method, tol, paths, stream) -> EncodeResult:
+    import torch
+    g = selector.gdict
     N = X.shape[0]
     dev = X.device
     idx = torch.empty((N, K), dtype=torch.int32, device=dev)
@@ -388,6 +427,15 @@ def encode_host(selector, X: np.ndarray, K: int, method: str = "omp", tol: float
         out = dict(idx=np.empty((N, K), np.int32), coef=np.empty((N, K), np.float32),
                    count=np.empty(N, np.int32), resnorm=np.empty(N, np.float32),
                    ip=np.empty((N, 2), np.int32))
+    # the library writes through these pointers: shape, dtype and layout must be exact
+    for name, shape, dt in (("idx", (N, K), np.int32), ("coef", (N, K), np.float32),
+                            ("count", (N,), np.int32), ("resnorm", (N,), np.float32),
+                            ("ip", (N, 2), np.int32)):
+        a = out.get(name)
+        if not isinstance(a, np.ndarray) or a.shape != shape or a.dtype != dt or not a.flags.c_contiguous \
+                or not a.flags.writeable:
+            raise ValueError(f"out[{name!r}] must be a writeable C-contiguous {np.dtype(dt).name} array "
+                             f"of shape {shape}")
     lib = _lib.load()
     th = selector.tree.handle if selector.tree is not None else None
     _lib.check(lib.stmp_encode_host(
@@ -425,11 +473,31 @@ def orthogonal_matching_pursuit(selector, x, params: SearchParams, counter=None)
     return _single(selector, x, params, counter, "omp")
 
 
+# Per-call free functions reuse their selector (device tree tables included)
+# for the same (tree, dictionary, alpha): a small LRU holding the arguments.
+_SELECTOR_CACHE: OrderedDict = OrderedDict()
+_SELECTOR_CACHE_SIZE = 4
+
+
+def _cached_selector(key, args, make):
+    hit = _SELECTOR_CACHE.get(key)
+    if hit is not None and all(a is b for a, b in zip(hit[0], args)):
+        _SELECTOR_CACHE.move_to_end(key)
+        return hit[1]
+    sel = make()
+    _SELECTOR_CACHE[key] = (args, sel)
+    while len(_SELECTOR_CACHE) > _SELECTOR_CACHE_SIZE:
+        _SELECTOR_CACHE.popitem(last=False)
+    return sel
+
+
 def exact_select(d, r, counter=None):
     """GPU ``exact_select`` (pursuit.py:102-109)."""
-    return ExactSelector(d).select(r, counter)
+    sel = _cached_selector(("exact", id(d)), (d,), lambda: ExactSelector(d))
+    return sel.select(r, counter)
 
 
 def stmp_select(t, d, r, alpha: float, counter=None):
-    """GPU ``stmp_select`` (pursuit.py:112-162), greedy alpha only."""
-    return TreeSelector(t, d, alpha).select(r, counter)
+    """GPU ``stmp_select`` (pursuit.py:112-162)."""
+    sel = _cached_selector(("tree", id(t), id(d), float(alpha)), (t, d), lambda: TreeSelector(t, d, alpha))
+    return sel.select(r, counter)

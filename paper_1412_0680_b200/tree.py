@@ -30,7 +30,12 @@ import numpy as np
 
 TREE_MAGIC = b"STMPTREE"       # clustering.py:33
 TREE_VERSION = 1               # clustering.py:34
-STRUCTURE_FORMAT = "stmp-b200-tree-structure/1"
+STRUCTURE_FORMAT = "stmp-b200-tree-structure/1"          # structure + explicit centroids
+MEMBERSHIP_FORMAT = "stmp-b200-tree-structure/2"         # structure only; centroids rebuilt
+DEGENERATE_NORM = 1e-12        # clustering.py:35
+
+# how a node's centroid is recovered by load_structure (format 2)
+_ATOM, _MEAN, _EXPLICIT = 0, 1, 2
 
 
 from .errors import FormatError
@@ -258,9 +263,106 @@ def save_structure(t: FlatTree, atoms: np.ndarray, path) -> None:
     )
 
 
+def _members_by_node(t: FlatTree) -> list:
+    """Sorted member atoms of every internal node (BFS id order).  The reference
+    builds each node from ``members[part.assignments == cid]`` of an ascending
+    parent list (clustering.py:295-305), so member lists are ascending."""
+    L = t.levels
+    out = [None] * t.num_internal
+    lo, hi = t.depth_range(L)
+    for v in range(lo, hi):
+        b, c = int(t.child_begin[v]), int(t.child_count[v])
+        out[v] = np.sort(t.leaf_atom[b:b + c].astype(np.int64))
+    for d in range(L - 1, -1, -1):
+        lo, hi = t.depth_range(d)
+        for v in range(lo, hi):
+            b, c = int(t.child_begin[v]), int(t.child_count[v])
+            out[v] = np.sort(np.concatenate(out[b:b + c]))
+    return out
+
+
+def _mean_of(atoms: np.ndarray, members: np.ndarray) -> np.ndarray:
+    """The f64 member mean of ``_unit_mean`` (clustering.py:145-147)."""
+    block = atoms if members.size == atoms.shape[0] and members[0] == 0 and members[-1] == members.size - 1 \
+        else atoms[members]
+    return block.astype(np.float64).mean(axis=0)
+
+
+def save_membership(t: FlatTree, atoms: np.ndarray, path) -> None:
+    """Membership-only shipping format (about 0.5 MB for config 4 instead of 27 MB).
+
+    Every internal centroid of the reference tree is ``_unit_mean`` of the
+    node's member atoms (clustering.py:145-153, 291-298): the f64 mean, divided
+    by its norm, cast to f32.  The file keeps the structure, the f64 norm of
+    each node's mean (so the rebuild does not depend on the host BLAS's dot
+    product order) and explicit rows only for nodes whose centroid is not
+    reproduced bitwise (degenerate means); ``load_structure`` rebuilds the
+    rest and checks the SHA-256 of the whole centroid table.
+    """
+    members = _members_by_node(t)
+    mode = np.full(t.num_internal, _EXPLICIT, dtype=np.uint8)
+    norms = np.zeros(t.num_internal, dtype=np.float64)
+    L = t.levels
+    lo, hi = t.depth_range(L)
+    for v in range(t.num_internal):
+        if lo <= v < hi and members[v].size == 1 and \
+                (t.centroids[v].view(np.uint32) == atoms[members[v][0]].view(np.uint32)).all():
+            mode[v] = _ATOM
+            continue
+        mean = _mean_of(atoms, members[v])
+        nrm = float(np.linalg.norm(mean))
+        if nrm >= DEGENERATE_NORM and ((mean / nrm).astype(np.float32).view(np.uint32) ==
+                                       t.centroids[v].view(np.uint32)).all():
+            mode[v] = _MEAN
+            norms[v] = nrm
+    np.savez_compressed(
+        path,
+        format=np.array(MEMBERSHIP_FORMAT),
+        branching=np.asarray(t.branching, dtype=np.int64),
+        n=np.int64(t.n),
+        fingerprint=np.array([t.fingerprint], dtype=np.uint64),
+        child_count=t.child_count,
+        leaf_atom=t.leaf_atom,
+        mode=mode,
+        norms=norms[mode == _MEAN],
+        explicit=t.centroids[mode == _EXPLICIT],
+        digest=np.array(t.centroid_digest()),
+    )
+
+
+def _load_membership(z, path, atoms: np.ndarray) -> FlatTree:
+    branching = tuple(int(k) for k in z["branching"])
+    n = int(z["n"])
+    counts = z["child_count"].astype(np.int64)
+    L = len(branching)
+    counts_by_depth, lo, width = [], 0, 1
+    for d in range(L + 1):
+        counts_by_depth.append(counts[lo:lo + width])
+        lo, width = lo + width, int(counts[lo:lo + width].sum())
+    leaf_atom = z["leaf_atom"]
+    mode = z["mode"]
+    cent = np.zeros((counts.size, n), dtype=np.float32)
+    t = _from_counts(branching, n, int(z["fingerprint"][0]), counts_by_depth, cent, leaf_atom)
+    atoms = np.ascontiguousarray(atoms, dtype=np.float32)
+    if atoms.shape[1] != n:
+        raise TreeFormatError(f"{path}: dictionary dimension {atoms.shape[1]} != tree dimension {n}")
+    members = _members_by_node(t)
+    t.centroids[mode == _EXPLICIT] = z["explicit"]
+    mean_ids = np.flatnonzero(mode == _MEAN)
+    for v, nrm in zip(mean_ids, z["norms"]):
+        t.centroids[v] = (_mean_of(atoms, members[v]) / float(nrm)).astype(np.float32)
+    for v in np.flatnonzero(mode == _ATOM):
+        t.centroids[v] = atoms[members[v][0]]
+    if t.centroid_digest() != str(z["digest"]):
+        raise TreeFormatError(f"{path}: rebuilt centroids do not match the stored digest")
+    return t
+
+
 def load_structure(path, atoms: np.ndarray) -> FlatTree:
     """Rebuild a shipped tree against its (regenerated) dictionary and verify it bitwise."""
     z = np.load(path, allow_pickle=False)
+    if str(z["format"]) == MEMBERSHIP_FORMAT:
+        return _load_membership(z, path, atoms)
     if str(z["format"]) != STRUCTURE_FORMAT:
         raise TreeFormatError(f"{path}: not a {STRUCTURE_FORMAT} file")
     branching = tuple(int(k) for k in z["branching"])

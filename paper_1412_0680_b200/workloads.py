@@ -150,23 +150,13 @@ def _distinct_supports(rng: np.random.Generator, rows: int, m: int, s: int) -> n
         sup[dup] = rng.integers(0, m, size=(dup.size, s))
 
 
-def make_patches(wl: Workload, count: int | None = None, start: int = 0) -> np.ndarray:
-    """Patches ``[start, start + count)`` (default: the first N) as f32 [count, n];
-    ``start`` must be a multiple of the config's chunk size.
-
-    Each patch is ``sum_j c_j a_{s_j} + sigma * N(0,1)^n`` over ``sparsity``
-    distinct atoms, computed in f64 and cast to f32; c3 synthesises in
-    measurement space, ``y = Phi x + sigma * noise`` with x sparse in the base
-    dictionary (``Phi a`` rows kept from the projection).
-    """
+def _fill_chunks(wl: Workload, out: np.ndarray, start: int, chunk_ids) -> None:
     cfg = wl.cfg
-    count = cfg.N if count is None else int(count)
     src = wl.synth if wl.synth is not None else wl.atoms
-    if start % cfg.chunk:
-        raise ValueError(f"start {start} is not a multiple of the chunk size {cfg.chunk}")
-    out = np.empty((count, cfg.n), dtype=np.float32)
+    count = out.shape[0]
     c_first = start // cfg.chunk
-    for ci, pos in enumerate(range(0, count, cfg.chunk), start=c_first):
+    for ci in chunk_ids:
+        pos = (ci - c_first) * cfg.chunk
         rows = min(cfg.chunk, count - pos)
         full = cfg.chunk  # draw whole chunks so prefixes are stable
         rs = np.random.default_rng(seed_sequence(cfg.cid, 2, ci))
@@ -181,4 +171,56 @@ def make_patches(wl: Workload, count: int | None = None, start: int = 0) -> np.n
         for j in range(cfg.sparsity):
             x += coef[:, j:j + 1] * np.asarray(src[sup[:, j]], dtype=np.float64)
         out[pos:pos + rows] = x
+
+
+_FILL = {}
+
+
+def _fill_worker(args):
+    name, shape, start, ids = args
+    from multiprocessing import shared_memory
+    shm = shared_memory.SharedMemory(name=name)
+    try:
+        _fill_chunks(_FILL["wl"], np.ndarray(shape, dtype=np.float32, buffer=shm.buf), start, ids)
+    finally:
+        shm.close()
+    return len(ids)
+
+
+def make_patches(wl: Workload, count: int | None = None, start: int = 0, procs: int | None = None) -> np.ndarray:
+    """Patches ``[start, start + count)`` (default: the first N) as f32 [count, n];
+    ``start`` must be a multiple of the config's chunk size.
+
+    Each patch is ``sum_j c_j a_{s_j} + sigma * N(0,1)^n`` over ``sparsity``
+    distinct atoms, computed in f64 and cast to f32; c3 synthesises in
+    measurement space, ``y = Phi x + sigma * noise`` with x sparse in the base
+    dictionary (``Phi a`` rows kept from the projection).
+    """
+    cfg = wl.cfg
+    count = cfg.N if count is None else int(count)
+    if start % cfg.chunk:
+        raise ValueError(f"start {start} is not a multiple of the chunk size {cfg.chunk}")
+    c_first = start // cfg.chunk
+    ids = list(range(c_first, c_first + -(-count // cfg.chunk)))
+    import os
+    procs = procs if procs is not None else min(len(ids), len(os.sched_getaffinity(0)), 32)
+    if procs <= 1 or count * cfg.n < (1 << 26):
+        out = np.empty((count, cfg.n), dtype=np.float32)
+        _fill_chunks(wl, out, start, ids)
+        return out
+    # large batches: chunks are independent draws, so a fork pool fills disjoint
+    # row ranges of one shared buffer (same bytes as the serial loop)
+    import multiprocessing as mp
+    from multiprocessing import shared_memory
+    shm = shared_memory.SharedMemory(create=True, size=count * cfg.n * 4)
+    try:
+        _FILL["wl"] = wl
+        jobs = [(shm.name, (count, cfg.n), start, ids[i::procs]) for i in range(procs)]
+        with mp.get_context("fork").Pool(procs) as pool:
+            pool.map(_fill_worker, jobs)
+        out = np.array(np.ndarray((count, cfg.n), dtype=np.float32, buffer=shm.buf))
+    finally:
+        _FILL.clear()
+        shm.close()
+        shm.unlink()
     return out

@@ -156,3 +156,36 @@ def test_oracle_omp_refit_matches_reference(stmp_ref):
         x = rng.standard_normal(20)
         np.testing.assert_allclose(O.omp_refit(d.scoring_atoms, support, x),
                                    stmp_ref.omp_refit(d, support, x), rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("method", ["omp", "mp"])
+def test_batched_exact_oracle_equals_per_patch(method):
+    """oracle/parallel.py's GEMM-batched exhaustive oracle (used for the large
+    exhaustive parity prefixes) against the per-patch restatement."""
+    from oracle import parallel as OP
+    z = golden("pursuit_small.npz")
+    a64 = z["atoms"].astype(np.float64)
+    K = int(z["K"])
+    X = np.concatenate([z["X"], np.zeros((1, z["X"].shape[1]), np.float32)])
+    ref = O.pack(O.encode_batch(O.exact_selector(a64), a64, X, K, method), K)
+    got = O.pack(OP.encode_exact_batched(a64, X, K, method, block=7), K)
+    np.testing.assert_array_equal(got["idx"], ref["idx"])
+    np.testing.assert_array_equal(got["count"], ref["count"])
+    np.testing.assert_array_equal(got["ip"], ref["ip"])
+    np.testing.assert_allclose(got["coef"], ref["coef"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(got["resnorm"], ref["resnorm"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(got["gaps"], ref["gaps"], rtol=1e-9)
+    # and it reproduces the reference's own recorded exhaustive runs
+    np.testing.assert_array_equal(got["idx"][:-1], z[f"exact_{method}_idx"])
+
+
+def test_parallel_tree_oracle_equals_serial():
+    from oracle import parallel as OP
+    z = golden("pursuit_small.npz")
+    a64 = z["atoms"].astype(np.float64)
+    t = _tree(z)
+    K = int(z["K"])
+    ref = O.pack(O.encode_batch(O.tree_selector(t, a64, 1 / 16), a64, z["X"], K, "omp"), K)
+    got = O.pack(OP.encode_parallel(t, a64, z["X"], K, "omp", alpha=1 / 16, procs=2), K)
+    for k in ("idx", "coef", "count", "resnorm", "ip", "path", "gaps"):
+        np.testing.assert_array_equal(got[k], ref[k])

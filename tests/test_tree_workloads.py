@@ -50,7 +50,7 @@ def test_flatten_matches_reference_tree_file(stmp_ref, tmp_path):
     assert stmp_ref.validate_tree(back, d).ok
 
 
-@pytest.mark.parametrize("cid", [0, 1, 2])
+@pytest.mark.parametrize("cid", [0, 1, 2, 3, 4])
 def test_shipped_structures_rebuild_bitwise(cid):
     cfg = W.CONFIGS[cid]
     wl = W.make_dictionary(cfg)
@@ -88,3 +88,26 @@ def test_patch_prefix_is_stable_and_shards_are_disjoint():
     with pytest.raises(ValueError):
         W.make_patches(wl, 10, start=3)
     assert a.dtype == np.float32 and a.shape == (1000, 64)
+
+
+def test_membership_format_detects_a_wrong_rebuild(tmp_path):
+    """The membership-only file rebuilds centroids as _unit_mean of the members
+    (clustering.py:145-153); any disagreement fails the SHA-256 check loudly."""
+    cfg = W.CONFIGS[0]
+    wl = W.make_dictionary(cfg)
+    src = os.path.join(GOLDEN, "trees", "c0.npz")
+    z = dict(np.load(src))
+    assert str(z["format"]) == T.MEMBERSHIP_FORMAT
+    bad = dict(z)
+    bad["norms"] = z["norms"].copy()
+    bad["norms"][3] *= 1 + 1e-6
+    np.savez(tmp_path / "bad.npz", **bad)
+    with pytest.raises(T.TreeFormatError):
+        T.load_structure(tmp_path / "bad.npz", wl.atoms)
+    swapped = dict(z)
+    la = z["leaf_atom"].copy()
+    la[[0, 100]] = la[[100, 0]]
+    swapped["leaf_atom"] = la
+    np.savez(tmp_path / "swapped.npz", **swapped)
+    with pytest.raises(T.TreeFormatError):
+        T.load_structure(tmp_path / "swapped.npz", wl.atoms)

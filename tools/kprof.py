@@ -24,7 +24,7 @@ def main():
         _lib.set_option(k, int(v))
     cfg = W.CONFIGS[cid]
     wl = W.make_dictionary(cfg)
-    flat = T.load_structure(next(p for p in (f"tests/golden/trees/c{cid}.npz", f"artifacts/trees/c{cid}.npz") if os.path.exists(p)), wl.atoms)
+    flat = T.load_structure(f"tests/golden/trees/c{cid}.npz", wl.atoms)
     sel = P.ExactSelector(wl.atoms) if os.environ.get("SELECTOR") == "exact" else P.TreeSelector(flat, wl.atoms, cfg.alpha)
     X = torch.as_tensor(W.make_patches(wl, N)).cuda()
     for _ in range(3):

@@ -8,9 +8,10 @@ Runs only in the build container, where the reference is importable from
    ``project_dictionary`` on the same raw draw;
 2. calls the reference ``build_tree(d, branching, seed)``
    (pkg/src/stmp/clustering.py:285-316) and ``validate_tree``;
-3. flattens the tree and writes the compact structure file that the GPU box
-   rebuilds bitwise (``tree.load_structure``), plus the reference ``.tree``
-   bytes round-trip check.
+3. flattens the tree and writes the membership-only structure file from which
+   the GPU box rebuilds every centroid bitwise (``tree.save_membership`` /
+   ``tree.load_structure``, checked by the stored SHA-256), plus the
+   reference ``.tree`` bytes round-trip check.
 
 Usage: python tools/make_trees.py 0 1 2 3 [4] [--out DIR]
 """
@@ -58,7 +59,7 @@ def main():
         assert rep.ok, rep.violation
         flat = T.from_reference_tree(tree)
         path = os.path.join(args.out, f"c{cid}.npz")
-        T.save_structure(flat, wl.atoms, path)
+        T.save_membership(flat, wl.atoms, path)
         back = T.load_structure(path, wl.atoms)
         assert back.centroid_digest() == flat.centroid_digest()
         if cid <= 1:
