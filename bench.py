@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--profile-run", action="store_true",
+                    help="under ncu: only the warm-up and timed encodes (no e2e, CPU leg, peak GEMM or "
+                         "instrumented encode)")
     ap.add_argument("--score-kernel", type=int, default=2, choices=[2, 3],
                     help="tcgen05 score pass: 2 node table in shared memory where it fits, 3 streamed table")
     ap.add_argument("--update-kernel", type=int, default=1, choices=[0, 1],
@@ -174,6 +177,41 @@ def cpu_rate(wl, flat, X, K, method, selector, seconds, cores=None, results=None
     if results is not None:
         results.extend(r for p in parts for r in p)
     return done / wall, cores, done, wall
+
+
+def measure_tf32_tflops(n=8192, reps=10):
+    """Dense TF32 tensor-core rate of this GPU (cuBLAS fp32 GEMM with TF32),
+    measured live: the denominator of the 3xTF32 score passes' roofline."""
+    import torch
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        c = torch.empty(n, n, device="cuda")
+        for _ in range(3):
+            torch.matmul(a, b, out=c)
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b, out=c)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        del a, b, c
+        return 2 * n ** 3 / statistics.median(ts) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = old
+
+
+def demangle(name: str) -> str:
+    """Readable kernel name from a mangled one (the template arguments kept)."""
+    try:
+        out = subprocess.run(["c++filt", name], capture_output=True, text=True, timeout=5).stdout.strip()
+        return out.replace("stmp::", "").replace("(anonymous namespace)::", "") or name
+    except (OSError, subprocess.SubprocessError):
+        return name
 
 
 def cpu_model():
@@ -298,7 +336,7 @@ def main():
 
     # end-to-end through the host-buffer C ABI (pinned host memory)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.profile_run:
         Xp = torch.from_numpy(X_host).pin_memory()
         outs = dict(idx=torch.empty((N, cfg.K), dtype=torch.int32).pin_memory().numpy(),
                     coef=torch.empty((N, cfg.K), dtype=torch.float32).pin_memory().numpy(),
@@ -331,48 +369,75 @@ def main():
     value = world * N * args.steps / (total_ms / 1e3)
     launch_ms = statistics.mean(per_launch_ms)
     per_step = launches / max(1, args.steps)
-    if per_step > 1:
-        score = "exact_scan (tensor-core GEMM + argmax)" if exhaustive else "score_ts / score_st (tcgen05 3xTF32)"
-        kernel_desc = (f"staged pipeline, {per_step:.0f} launches per step: init + K x (root {score} pass over the "
-                       f"batch + per deeper level (fused scan + scatter, {score}) + OMP/MP update); achieved is over "
-                       f"the whole step")
-    else:
-        kernel_desc = "encode_fused_kernel (one launch per step)"
     peaks = {}
     pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(pk):
         peaks = json.load(open(pk))
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    rm = RL.model(cfg, N=N, method=args.method, exhaustive=exhaustive, hbm_gbs=hbm)
-    if rm["bound"] == "hbm":
-        achieved = rm["bytes_per_patch"] * N / (launch_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None}
+    bf16 = float(peaks.get("bf16_tflops", 1590.0))
+    tf32 = 0.0 if args.profile_run else measure_tf32_tflops()
+    rm = RL.model(cfg, N=N, method=args.method, exhaustive=exhaustive, hbm_gbs=hbm,
+                  tensor_tflops=(tf32 or 776.3) / 3)
+
+    # per-kernel device time: one more encode, eager, with CUDA events around
+    # every launch on the encode stream (outside the timed region: events between
+    # launches stop programmatic dependent launch and graph replay)
+    ktimes = {}
+    if not args.profile_run:
+        _lib.kernel_timing(True)
+        step()
+        torch.cuda.synchronize()
+        ktimes = _lib.kernel_times()
+        _lib.kernel_timing(False)
+    fams = {}
+    for name, (cnt, ms) in ktimes.items():
+        f = fams.setdefault(RL.family_of(name), {"launches": 0, "ms": 0.0, "kernels": []})
+        f["launches"] += cnt
+        f["ms"] += ms
+        f["kernels"].append(demangle(name))
+    timed_ms = sum(f["ms"] for f in fams.values()) or 1.0
+    dom = max(fams, key=lambda f: fams[f]["ms"]) if fams else "other"
+    work = RL.family_work(cfg, dom, N, args.method, exhaustive)
+    dom_ms = fams[dom]["ms"] if fams else launch_ms
+    dom_launches = fams[dom]["launches"] if fams else 1
+    avg_s = dom_ms / dom_launches / 1e3
+    if work["bound"] == "hbm":
+        achieved = work["bytes"] / dom_launches / avg_s / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None}
     else:
-        bf16 = float(peaks.get("bf16_tflops", 1590.0))
-        achieved = rm["flops_per_patch"] * N / (launch_ms / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                "frac": achieved / bf16, "traffic": None,
-                # the path computes fp32-accurate scores as 3xTF32 (three tf32 products per
-                # k-step); against that arithmetic's peak (dense TF32 = bf16 / 2):
-                "peak_3xtf32": bf16 / 6.0, "frac_3xtf32": achieved / (bf16 / 6.0)}
+        achieved = work["flops"] / dom_launches / avg_s / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s", "frac": achieved / bf16,
+                "traffic": None,
+                # the scores are fp32-accurate 3xTF32 (three tf32 products per k-step): against the
+                # dense TF32 rate measured live in this run, divided by 3
+                "peak_3xtf32": tf32 / 3, "frac_3xtf32": achieved / (tf32 / 3) if tf32 else None}
     roof.update({
-        "peak_source": "MEASURED_PEAKS.json" if peaks else "B200_PROFILING.md fallback",
-        "model": "SURVEY §8d per-patch algorithmic bytes/FLOPs x patches per launch / mean launch time",
-        "bytes_per_patch": rm["bytes_per_patch"], "flops_per_patch": rm["flops_per_patch"],
-        "launch_ms": launch_ms,
-        "fp32_simt_frac": rm["flops_per_patch"] * N / (launch_ms / 1e3) / 1e12 / RL.FP32_SIMT_TFLOPS,
-        "kernel": kernel_desc,
+        "kernel": f"{dom}: {', '.join(sorted(set(fams[dom]['kernels'])))}" if fams else "?",
+        "launches_per_step": dom_launches, "avg_launch_ms": dom_ms / dom_launches,
+        "share_of_step": dom_ms / timed_ms,
+        "peak_source": ("MEASURED_PEAKS.json" if peaks else "B200_PROFILING.md fallback") +
+                       (f"; TF32 {tf32:.0f} TFLOP/s measured live (cuBLAS 8192^3)" if tf32 else ""),
+        "model": "SURVEY §8d algorithmic bytes/FLOPs of the dominant kernel family (roofline.family_work) per "
+                 "launch / its mean launch time (CUDA events on the encode stream, one instrumented encode)",
+        "families": {f: {"launches": v["launches"], "ms": round(v["ms"], 4), "share": round(v["ms"] / timed_ms, 4)}
+                     for f, v in sorted(fams.items(), key=lambda kv: -kv[1]["ms"])},
+        # the whole staged step against the §8d per-patch model (the pipeline as one unit)
+        "step": {"bound": rm["bound"], "bytes_per_patch": rm["bytes_per_patch"],
+                 "flops_per_patch": rm["flops_per_patch"], "launch_ms": launch_ms,
+                 "launches": per_step, "model_patches_per_s": rm["patches_per_s_roof"],
+                 "frac": rm["patches_per_s_roof"] and (N / (launch_ms / 1e3)) / rm["patches_per_s_roof"]},
     })
-    traffic_file = os.path.join(ROOT, "profiles", f"traffic_c{cfg.cid}.json")
+    traffic_file = os.path.join(ROOT, "profiles", f"r02_traffic_c{cfg.cid}.json")
     if os.path.exists(traffic_file):
         tr = json.load(open(traffic_file))
-        if tr.get("patches") == N and tr.get("method") == args.method and tr.get("selector") == args.selector:
-            roof["traffic"] = tr.get("bytes_per_launch")
+        key = f"{'exact' if exhaustive else 'tree'}-{args.method}-{N}"
+        if key in tr and dom in tr[key]:
+            roof["traffic"] = tr[key][dom]   # ncu dram bytes per launch of this family
 
     cpu = None
     parity = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and not args.profile_run and world == 1:
         from oracle import stmp_oracle as O
         from oracle.parity import compare
         oracle_res = []
@@ -404,6 +469,7 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
         "roofline_model_patches_per_s": rm["patches_per_s_roof"],
+        "peaks": {"tf32_tflops_live": tf32},
     }
     print(json.dumps(line), flush=True)
     if dist:

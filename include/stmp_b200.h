@@ -171,17 +171,26 @@ int stmp_apply_operator(int32_t kind, const float* X, int64_t N, int32_t n_in, c
 /* Process-wide tuning knobs (no reference counterpart):
  *   "path": 0 auto (default), 1 fused warp-per-patch kernel, 2 staged tensor-core pipeline;
  *   "staged_min_batch": batch size from which `auto` picks the staged pipeline;
- *   "score_kernel": staged score pass 0 single-role, 1 warp-specialised, 2 TMEM A operand (default),
- *                   3 streamed table (always used for nodes whose table exceeds shared memory);
- *   "update_kernel": staged update 0 generic, 1 lockstep OMP (default), 2 tile + fused root;
- *   "gram": 1 lockstep update reads the atom Gram table (m <= 32768, K <= 8), 0 support-row dots (default);
+ *   "score_kernel": staged score pass 2 node table in shared memory where it fits (default),
+ *                   3 streamed table at every level (always used where the table does not fit);
+ *   "update_kernel": staged OMP update 0 generic, 1 lockstep / wide-row (default);
  *   "pdl": 1 (default) launch the staged kernels with programmatic dependent launch, 0 plain;
- *   "score_tma": 1 gather the score pass's rows with TMA tile::gather4, 0 per-thread cp.async (default);
  *   "graphs": 1 (default) replay repeated staged encodes (same buffers, sizes, stream) as CUDA graphs. */
 int stmp_set_option(const char* key, int64_t value);
 
 /* Instrumentation: cumulative number of CUDA kernels this library has launched. */
 int stmp_kernel_launches(int64_t* out);
+
+/* Instrumentation: per-kernel device time.  stmp_kernel_timing(1) clears the
+ * record and brackets every later kernel launch with CUDA events on its stream
+ * (encodes run eagerly, without graph replay, while on); stmp_kernel_timing(0)
+ * stops recording.  stmp_kernel_times synchronises the recorded events and
+ * returns, per kernel (up to max_entries, names truncated to name_len bytes,
+ * NUL-terminated, in names[i * name_len]), the launch count and the summed
+ * duration in ms; *n_entries is the number of distinct kernels.             */
+int stmp_kernel_timing(int32_t enable);
+int stmp_kernel_times(int32_t max_entries, char* names, int32_t name_len, int64_t* launches, double* total_ms,
+                      int32_t* n_entries);
 
 /* Device synchronisation helper for hosts without a CUDA runtime binding. */
 int stmp_stream_sync(void* stream);

@@ -44,6 +44,8 @@ EXPORTS = {
     "stmp_stream_sync": (C.c_int, [C.c_void_p]),
     "stmp_set_option": (C.c_int, [C.c_char_p, C.c_int64]),
     "stmp_kernel_launches": (C.c_int, [C.c_void_p]),
+    "stmp_kernel_timing": (C.c_int, [C.c_int32]),
+    "stmp_kernel_times": (C.c_int, [C.c_int32, C.c_char_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "stmp_dc_split": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.c_double,
                                 C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "stmp_reconstruct": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
@@ -70,6 +72,31 @@ def kernel_launches() -> int:
     v = C.c_int64(0)
     check(load().stmp_kernel_launches(C.byref(v)))
     return int(v.value)
+
+
+def kernel_timing(enable: bool) -> None:
+    """Start (clearing the record) or stop per-kernel CUDA-event timing."""
+    check(load().stmp_kernel_timing(1 if enable else 0))
+
+
+def kernel_times(max_entries: int = 64) -> dict:
+    """{kernel name: (launches, total ms)} of the launches recorded since
+    kernel_timing(True) (synchronises the recorded events)."""
+    import numpy as np
+    name_len = 256
+    names = C.create_string_buffer(max_entries * name_len)
+    launches = np.zeros(max_entries, dtype=np.int64)
+    ms = np.zeros(max_entries, dtype=np.float64)
+    n = C.c_int32(0)
+    check(load().stmp_kernel_times(max_entries, names, name_len, launches.ctypes.data, ms.ctypes.data,
+                                   C.byref(n)))
+    raw = names.raw
+    out = {}
+    for i in range(min(n.value, max_entries)):
+        nm = raw[i * name_len:(i + 1) * name_len].split(b"\0", 1)[0].decode(errors="replace")
+        out[nm] = (int(launches[i]), float(ms[i]))
+    return out
+
 
 _lib = None
 

@@ -166,6 +166,54 @@ int stmp_kernel_launches(int64_t* out) {
   return STMP_OK;
 }
 
+int stmp_kernel_timing(int32_t enable) {
+  g_err.clear();
+  stmp::KernelTimer& kt = stmp::kernel_timer();
+  for (auto& r : kt.recs) {
+    kt.pool.push_back(r.e0);
+    kt.pool.push_back(r.e1);
+  }
+  kt.recs.clear();
+  kt.on = enable != 0;
+  return STMP_OK;
+}
+
+int stmp_kernel_times(int32_t max_entries, char* names, int32_t name_len, int64_t* launches, double* total_ms,
+                      int32_t* n_entries) {
+  g_err.clear();
+  if (n_entries == nullptr || (max_entries > 0 && (names == nullptr || launches == nullptr || total_ms == nullptr)) ||
+      name_len < 2)
+    return fail(STMP_EINVAL, "NULL output or name_len < 2");
+  stmp::KernelTimer& kt = stmp::kernel_timer();
+  std::vector<const void*> fns;
+  std::vector<int64_t> cnt;
+  std::vector<double> ms;
+  for (auto& r : kt.recs) {
+    cudaError_t e = cudaEventSynchronize(r.e1);
+    float t = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.e0, r.e1);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel timing");
+    size_t i = 0;
+    while (i < fns.size() && fns[i] != r.fn) ++i;
+    if (i == fns.size()) {
+      fns.push_back(r.fn);
+      cnt.push_back(0);
+      ms.push_back(0.0);
+    }
+    cnt[i] += 1;
+    ms[i] += t;
+  }
+  *n_entries = (int32_t)fns.size();
+  for (size_t i = 0; i < fns.size() && (int32_t)i < max_entries; ++i) {
+    const char* nm = nullptr;
+    if (cudaFuncGetName(&nm, fns[i]) != cudaSuccess || nm == nullptr) nm = "?";
+    snprintf(names + i * name_len, (size_t)name_len, "%s", nm);
+    launches[i] = cnt[i];
+    total_ms[i] = ms[i];
+  }
+  return STMP_OK;
+}
+
 int stmp_stream_sync(void* stream) {
   STMP_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "cudaStreamSynchronize");
   return STMP_OK;
@@ -420,8 +468,8 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
       return stmp::run_staged(d, t, X, N, ldx, K, method, tol, idx, coef, count, resnorm, path, ip, workspace,
                               workspace_bytes, st);
     };
-    // the legacy default stream cannot be captured
-    if (!g_graphs || st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread) {
+    // the legacy default stream cannot be captured; timed encodes run eagerly
+    if (!g_graphs || stmp::kernel_timer().on || st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread) {
       cudaError_t e = run();
       if (e != cudaSuccess) return cuda_fail(e, "staged encode");
       return STMP_OK;

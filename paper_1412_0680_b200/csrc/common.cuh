@@ -17,6 +17,34 @@ inline std::atomic<int64_t>& launch_counter() {
 }
 inline void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
 
+// Optional per-launch timing (stmp_kernel_timing / stmp_kernel_times): CUDA
+// events recorded on the launch stream right before and after every kernel
+// launched through launch_kernel, aggregated per kernel name on request.
+// Encodes run eagerly (no graph replay) while it is on.
+struct KernelTimer {
+  struct Rec {
+    const void* fn;
+    cudaEvent_t e0, e1;
+  };
+  bool on = false;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t take() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+inline KernelTimer& kernel_timer() {
+  static KernelTimer t;
+  return t;
+}
+
 // Programmatic dependent launch between the kernels of one encode: a kernel
 // launched with `pdl` is set up while its predecessor's last CTAs drain (the
 // trigger is the implicit one at CTA exit -- an early explicit trigger let
@@ -42,7 +70,14 @@ inline cudaError_t launch_kernel(void (*k)(KArgs...), dim3 grid, dim3 block, siz
   cfg.attrs = attr;
   cfg.numAttrs = (pdl && g_pdl) ? 1 : 0;
   note_launch();
-  return cudaLaunchKernelEx(&cfg, k, args...);
+  KernelTimer& kt = kernel_timer();
+  if (!kt.on) return cudaLaunchKernelEx(&cfg, k, args...);
+  KernelTimer::Rec r{reinterpret_cast<const void*>(k), kt.take(), kt.take()};
+  cudaEventRecord(r.e0, st);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
+  cudaEventRecord(r.e1, st);
+  kt.recs.push_back(r);
+  return e;
 }
 
 constexpr unsigned kFull = 0xffffffffu;

@@ -24,7 +24,6 @@ import math
 
 L2_BYTES = 126 * 1024 * 1024
 FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: FFMA peak at max clock
-TF32_DENSE_TFLOPS_EST = 1686.0 / 2                  # half the measured bf16 rate (estimate)
 
 
 def ip_per_selection(branching, m: int, exhaustive: bool) -> int:
@@ -54,8 +53,10 @@ def bytes_per_patch(n: int, K: int, branching, m: int, N: int, method: str = "om
 
 
 def model(cfg, N: int | None = None, method: str = "omp", exhaustive: bool = False,
-          hbm_gbs: float = 6548.2, tensor_tflops: float | None = None) -> dict:
-    """Roofline numbers for a workload config (see workloads.CONFIGS)."""
+          hbm_gbs: float = 6548.2, tensor_tflops: float = 300.0) -> dict:
+    """Roofline numbers for a workload config (see workloads.CONFIGS).
+    ``tensor_tflops`` is the fp32-accurate tensor rate: the MEASURED dense TF32
+    GEMM rate / 3 (3xTF32, three tf32 products per k-step)."""
     N = cfg.N if N is None else N
     L = len(cfg.branching)
     # centroid tables of depths 1..L (excluding single-atom depth L, which is the dictionary)
@@ -63,8 +64,65 @@ def model(cfg, N: int | None = None, method: str = "omp", exhaustive: bool = Fal
     table_bytes = sum(4 * cfg.n * v for v in nodes if 4 * cfg.n * v > L2_BYTES)
     F = flops_per_patch(cfg.n, cfg.K, cfg.branching, cfg.m, method, exhaustive)
     B = bytes_per_patch(cfg.n, cfg.K, cfg.branching, cfg.m, N, method, exhaustive, table_bytes)
-    P = (tensor_tflops or TF32_DENSE_TFLOPS_EST / 3) * 1e12
+    P = tensor_tflops * 1e12
     t_hbm = B / (hbm_gbs * 1e9)
     t_fl = F / P
     return dict(flops_per_patch=F, bytes_per_patch=B, bound="hbm" if t_hbm >= t_fl else "tensor",
                 t_roof_per_patch=max(t_hbm, t_fl), patches_per_s_roof=1.0 / max(t_hbm, t_fl))
+
+
+# ---------------------------------------------------------------- per kernel family
+# Kernel families of one staged encode, by (mangled) kernel name.
+FAMILIES = (("score", ("score_ts_kernel", "score_st_kernel")),
+            ("exact_scan", ("exact_scan_kernel",)),
+            ("update", ("update_omp8_kernel", "update_wide_kernel", "update_kernel")),
+            ("scatter", ("scatter_scan_kernel", "scatter_kernel", "scatter_root_kernel", "scan_kernel")),
+            ("init", ("init_kernel",)))
+
+
+def family_of(name: str) -> str:
+    for fam, keys in FAMILIES:
+        if any(k in name for k in keys):
+            return fam
+    return "other"
+
+
+def family_work(cfg, family: str, N: int, method: str = "omp", exhaustive: bool = False) -> dict:
+    """Algorithmic work of one kernel family over a whole encode of N patches,
+    assuming every patch runs all K iterations (the noisy BASELINE inputs never
+    reach the 1e-6 tolerance early).  Returns {"bytes": B, "flops": F, "bound"}.
+
+    * score (tree): every level pass reads each residual row (4n B) and the
+      patch's node id (8 B); centroid tables count only when the level's table
+      exceeds L2 (config 4's last level: each visited node table once per
+      iteration).  FLOPs 2n per scored child.
+    * exact_scan: FLOPs 2nm per patch per iteration (tensor-bound).
+    * update (OMP, iteration T): x read, new atom read, r written (3 x 4n B),
+      plus the T support rows when the dictionary exceeds L2; MP: r read, atom
+      read, r written.
+    * scatter: active flag, node id and permutation slot (12 B per patch and level).
+    """
+    n, K, m = cfg.n, cfg.K, cfg.m
+    L = len(cfg.branching)
+    big = 4 * n * m > L2_BYTES
+    if family == "exact_scan":
+        return {"bytes": float(N * K * 4 * n + K * 4 * n * m), "flops": float(N * K * 2 * n * m), "bound": "tensor"}
+    if family == "score":
+        nodes = [math.prod(cfg.branching[:d]) for d in range(L)]          # nodes per level (parents)
+        kids = [math.prod(cfg.branching[:d + 1]) for d in range(L)]
+        tables = sum(4 * n * k for k in kids if 4 * n * k > L2_BYTES)
+        del nodes
+        return {"bytes": float(N * K * L * (4 * n + 8) + K * tables),
+                "flops": float(N * K * 2 * n * sum(cfg.branching)), "bound": "hbm"}
+    if family == "update":
+        if method == "omp":
+            per = sum(4 * n * (3 + (T if big else 0)) for T in range(K))
+            fl = sum(4 * n * (T + 1) for T in range(K))
+        else:
+            per, fl = K * 3 * 4 * n, K * 2 * n
+        return {"bytes": float(N * per), "flops": float(N * fl), "bound": "hbm"}
+    if family == "scatter":
+        return {"bytes": float(N * K * max(L - 1, 0) * 12), "flops": 0.0, "bound": "hbm"}
+    if family == "init":
+        return {"bytes": float(N * 4 * n * 2), "flops": 0.0, "bound": "hbm"}
+    return {"bytes": 0.0, "flops": 0.0, "bound": "hbm"}

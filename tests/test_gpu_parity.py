@@ -295,18 +295,16 @@ def oracle_config(cid, rows, method, exhaustive=False):
     return _ORACLE[key]
 
 
-def _skip_duplicate(cid, path):
+def _tree_cases():
+    cases = [(0, 10_000, "omp"), (0, 10_000, "mp"), (1, 16_384, "omp"), (1, 4096, "mp"),
+             (2, 16_384, "omp"), (3, 16_384, "omp"), (4, 512, "omp"), (4, 256, "mp")]
     # configs 2 and 4 have no node table that fits shared memory: their default
     # already streams every table, so "staged-st" would rerun the same kernels
-    if path == "staged-st" and cid in (2, 4):
-        pytest.skip("same kernels as staged-ts for this shape (score_st at every level)")
+    return [(c, r, m, p) for c, r, m in cases for p in PATHS if not (p == "staged-st" and c in (2, 4))]
 
 
-@pytest.mark.parametrize("cid,rows,method", [
-    (0, 10_000, "omp"), (0, 10_000, "mp"), (1, 16_384, "omp"), (1, 4096, "mp"),
-    (2, 16_384, "omp"), (3, 16_384, "omp"), (4, 512, "omp"), (4, 256, "mp")])
+@pytest.mark.parametrize("cid,rows,method,path", _tree_cases(), indirect=["path"])
 def test_config_tree_parity(cid, rows, method, path):
-    _skip_duplicate(cid, path)
     cfg, wl, flat = config(cid)
     X, ref = oracle_config(cid, rows, method)
     sel = P().TreeSelector(flat, wl.atoms, cfg.alpha)

@@ -22,7 +22,7 @@ def load(path):
     return list(launches.values())
 
 
-def main(path, out_json, patches, method="omp", selector="tree"):
+def main(path, out_json, patches, method="omp", selector="tree", family_json=None):
     ls = load(path)
     starts = [i for i, l in enumerate(ls) if "init_kernel" in l["name"]]
     step = ls[starts[-1]:] if starts else ls[len(ls) // 2:]   # last encode = the timed step
@@ -41,7 +41,22 @@ def main(path, out_json, patches, method="omp", selector="tree"):
                "kernels": {k: {"launches": c, "time_share": tt / t, "dram_bytes": b} for k, (c, tt, b) in per.items()}}
     json.dump(summary, open(out_json, "w"), indent=1)
     print(json.dumps(summary, indent=1))
+    if family_json:
+        # ncu DRAM bytes per launch of each kernel family (bench.py's roofline.traffic)
+        import os
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from paper_1412_0680_b200 import roofline as RL
+        fam = collections.defaultdict(lambda: [0, 0.0])
+        for l in step:
+            f = RL.family_of(l["name"])
+            fam[f][0] += 1
+            fam[f][1] += l.get("dram__bytes_read.sum", 0) + l.get("dram__bytes_write.sum", 0)
+        table = json.load(open(family_json)) if os.path.exists(family_json) else {}
+        table[f"{selector}-{method}-{patches}"] = {f: b / c for f, (c, b) in fam.items()}
+        json.dump(table, open(family_json, "w"), indent=1)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], int(sys.argv[3]))
+    a = sys.argv
+    main(a[1], a[2], int(a[3]), a[4] if len(a) > 4 else "omp", a[5] if len(a) > 5 else "tree",
+         a[6] if len(a) > 6 else None)
