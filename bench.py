@@ -318,7 +318,10 @@ def main():
     res = None
     for i in range(args.steps):
         ev[i][0].record(stream)
-        res = step()
+        if i + 1 < args.steps:
+            step()      # outputs freed at once: every step reuses the same buffers (one cached graph)
+        else:
+            res = step()
         ev[i][1].record(stream)
     e1.record(stream)
     launches = _lib.kernel_launches() - lc0   # counted by the library at each launch site

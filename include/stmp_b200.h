@@ -174,6 +174,11 @@ int stmp_apply_operator(int32_t kind, const float* X, int64_t N, int32_t n_in, c
  *   "score_kernel": staged score pass 2 node table in shared memory where it fits (default),
  *                   3 streamed table at every level (always used where the table does not fit);
  *   "update_kernel": staged OMP update 0 generic, 1 lockstep / wide-row (default);
+ *   "gram_path": tree OMP without a residual in HBM, on per-tree pair tables of
+ *                child-centroid . atom products (the Gram matrix at the last level;
+ *                needs single-atom depth-L nodes and m x nodes x 4 B of free device
+ *                memory): 0 off, 1 auto = rows >= 256 and >= 8x the widest node
+ *                (default), 2 whenever supported;
  *   "pdl": 1 (default) launch the staged kernels with programmatic dependent launch, 0 plain;
  *   "graphs": 1 (default) replay repeated staged encodes (same buffers, sizes, stream) as CUDA graphs. */
 int stmp_set_option(const char* key, int64_t value);

@@ -347,6 +347,13 @@ int stmp_tree_create(const stmp_dict* d, int32_t levels, const int32_t* branchin
     stmp_tree_free(t);
     return fail(STMP_ECUDA, "staged table upload: %s", berr.c_str());
   }
+  // Gram path (gram_path.cu): each atom must be exactly one depth-L leaf
+  if (t->max_leaf_children == 1 && num_leaves == d->m) {
+    std::vector<char> seen((size_t)d->m, 0);
+    bool unique = true;
+    for (int64_t j = 0; j < num_leaves && unique; ++j) unique = !seen[leaf_atom[j]]++;
+    if (unique && !stmp::build_leaf_pos(t, d->m, s)) cudaGetLastError();
+  }
   *out = t;
   return STMP_OK;
 }
@@ -359,6 +366,7 @@ void stmp_tree_free(stmp_tree* t) {
   cudaFree(t->leaf_atom);
   cudaFree(t->cent);
   stmp::free_staged_tables(t);
+  stmp::free_pair_tables(t);
   delete t;
 }
 
@@ -402,6 +410,11 @@ int stmp_set_option(const char* key, int64_t value) {
     if (value < 2 || value > 3)
       return fail(STMP_EINVAL, "score_kernel must be 2 (node table in shared memory) or 3 (streamed table)");
     stmp::g_score_ws = (int)value;
+    return STMP_OK;
+  }
+  if (strcmp(key, "gram_path") == 0) {
+    if (value < 0 || value > 2) return fail(STMP_EINVAL, "gram_path must be 0 (off), 1 (auto) or 2 (when supported)");
+    stmp::g_gram_path = (int)value;
     return STMP_OK;
   }
   if (strcmp(key, "staged_min_batch") == 0) {
@@ -483,7 +496,7 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
     for (int i = 0; i < 14; ++i) k.p[i] = ps[i];
     const int64_t vs[13] = {N, ldx, K, method, (int64_t)workspace_bytes, stmp::g_root_direct, stmp::g_score_ws,
                             stmp::g_update_omp8, (int64_t)d->generation, stmp::g_pdl,
-                            t ? (int64_t)t->generation : 0, 0, 0};
+                            t ? (int64_t)t->generation : 0, 0, stmp::g_gram_path};
     memcpy(k.v, vs, sizeof(vs));
     memcpy(&k.v[11], &tol, sizeof(float));
     std::lock_guard<std::mutex> lock(g_graph_mu);

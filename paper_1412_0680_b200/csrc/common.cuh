@@ -130,6 +130,13 @@ struct TreeHandle {
   uint64_t fingerprint = 0;
   uint64_t generation = 0;      // process-unique id (graph cache key)
   const DictHandle* dict = nullptr;
+  // Gram path (gram_path.cu): per level l, the [m][nodes at depth l + 1] table of
+  // child-centroid . atom products; leaf_pos[a] = column of atom a at the last level
+  int leaf_is_atom = -1;        // -1 unknown, 0/1: every depth-L node is one atom equal to its centroid
+  std::vector<float*> pair_tables;
+  std::vector<int64_t> pair_width;
+  int* leaf_pos = nullptr;
+  bool pair_tried = false;
 };
 
 // Device-side view passed to kernels by value.

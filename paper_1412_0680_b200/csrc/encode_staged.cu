@@ -262,6 +262,32 @@ __global__ void __launch_bounds__(256) scatter_root_kernel(int64_t N, const int*
   if (act) perm[offsets[0] + base + warp_off[warp] + __popc(m & ((1u << lane) - 1u))] = (int)p;
 }
 
+// Bucketing of the active patches by their level-(l-1) node for the score pass
+// of level l >= 1: the scan fused into the scatter (counters double-buffered by
+// iteration parity), or for more bins than one CTA scans, scan + scatter.
+cudaError_t launch_level_scatter(int64_t N, const int* active, const int* path_ws, int L, int l, int level_base,
+                                 int nb, int* counts_in, int* cursor_in, int* counts_next, int* cursor_next,
+                                 int* offsets, int* tile_off, int* cursor, int* perm, int4* items, int* num_items,
+                                 int sms, cudaStream_t st) {
+  cudaError_t e;
+  if (nb <= kScanRun * kScatterThreads) {
+    const int per = N >= (int64_t)sms * kScatterThreads * 8 ? 8 : N >= (int64_t)sms * kScatterThreads * 2 ? 2 : 1;
+    const int grid = (int)((N + kScatterThreads * per - 1) / (kScatterThreads * per));
+    auto k = per == 8 ? scatter_scan_kernel<8> : per == 2 ? scatter_scan_kernel<2> : scatter_scan_kernel<1>;
+    const size_t smem = (size_t)nb * 16;
+    if (smem > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+      return e;
+    return launch_kernel(k, grid, kScatterThreads, smem, st, true, N, active, path_ws, L, l, level_base, nb,
+                         (const int*)counts_in, cursor_in, counts_next, cursor_next, perm, items, num_items);
+  }
+  e = launch_kernel(scan_kernel, 1, kScanThreads, scan_smem(nb), st, true, counts_in, nb, offsets, items, num_items,
+                    tile_off, cursor, (int*)nullptr);
+  if (e != cudaSuccess) return e;
+  return launch_kernel(scatter_kernel, (int)((N + 255) / 256), 256, 0, st, true, N, active, path_ws, L, l, level_base,
+                       (const int*)offsets, cursor, perm);
+}
+
 }  // namespace
 
 size_t score_smem_bytes(int kchunks, int npad) {
@@ -372,6 +398,9 @@ struct WsLayout {
   size_t total = 0;
   size_t R, Xpad, tol, active, perm, path_ws, leaf_sel, Lf, yv, S_ws, c_ws, counts, offsets, tile_off, cursor, items,
       num_items, cursor2;
+  // Gram path only
+  bool gram = false;
+  size_t xn2 = 0, e_ws = 0, s0 = 0, bsel = 0;
 };
 
 WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method,
@@ -411,6 +440,13 @@ WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int 
   w.cursor = add((size_t)(maxbins + 1) * 4);
   w.items = add((size_t)(N / kTile + maxbins + 2) * 16);
   w.num_items = add(16);
+  if (t && gram_path_supported(d, t, K, method)) {
+    w.gram = true;
+    w.xn2 = add((size_t)N * 8);
+    w.e_ws = add((size_t)N * 8);
+    w.s0 = add((size_t)N * t->root_children * 4);
+    w.bsel = add((size_t)N * 4);
+  }
   if (bin_off_out) *bin_off_out = bin_off;
   if (maxbins_out) *maxbins_out = maxbins;
   return w;
@@ -460,6 +496,10 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   auto counts_of = [&](int it_) { return counts + (it_ & 1) * bin_off[LB]; };
   auto cursor_of = [&](int it_) { return cursor2 + (it_ & 1) * bin_off[LB]; };
 
+  // Gram path: no residual in HBM (gram_path.cu); falls back to the residual
+  // pipeline below when the pair tables cannot be built
+  const bool gram = w.gram && ensure_pair_tables(const_cast<TreeHandle*>(t), d, st);
+
   UpdateCfg uc;
   update_config(d->ld, K, uc);
   UpdateArgs u{};
@@ -501,6 +541,58 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   // exact_scan only)
   const bool root_direct = g_root_direct != 0;
   if (root_direct) u.root_count = nullptr;
+  if (gram) {
+    double* xn2 = (double*)(b + w.xn2);
+    double* e_ws = (double*)(b + w.e_ws);
+    float* s0 = (float*)(b + w.s0);
+    float* bsel = (float*)(b + w.bsel);
+    if ((e = launch_gram_init(X, ldx, d->n, N, xn2, e_ws, st)) != cudaSuccess) return e;
+    GramArgs ga{};
+    ga.N = N; ga.K = K; ga.L = L; ga.leaf_sel = leaf_sel; ga.bsel = bsel;
+    ga.gram = t->pair_tables[L - 1]; ga.gram_w = t->pair_width[L - 1]; ga.leaf_pos = t->leaf_pos;
+    ga.root_tab = t->pair_tables[0]; ga.s0 = s0; ga.root_w = t->root_children;
+    ga.root_cb = (int)t->level_offsets[1];
+    ga.path_ws = path_ws; ga.path_out = path; ga.S_ws = S_ws; ga.c_ws = c_ws; ga.yv = yv;
+    ga.Lf = Lf; ga.e_ws = e_ws; ga.xn2 = xn2; ga.tol = tol; ga.active = active; ga.idx = idx; ga.coef = coef;
+    ga.count = count; ga.resnorm = resnorm; ga.ip = ip;
+    ga.X = X; ga.ldx = ldx; ga.atoms = d->atoms; ga.ld = d->ld; ga.n = d->n; ga.rho = 1e-2f;
+    for (int it = 0; it < K; ++it) {
+      for (int l = it == 0 ? 0 : 1; l < L; ++l) {
+        const StagedLevel& lv = t->staged_levels[l];
+        const int nb = (int)(t->level_offsets[l + 1] - t->level_offsets[l]);
+        if (l > 0 &&
+            (e = launch_level_scatter(N, active, path_ws, L, l, (int)t->level_offsets[l], nb,
+                                      counts_of(it) + bin_off[l], cursor_of(it) + bin_off[l],
+                                      counts_of(it + 1) + bin_off[l], cursor_of(it + 1) + bin_off[l], offsets,
+                                      tile_off, cursor, perm, items, num_items, sms, st)) != cudaSuccess)
+          return e;
+        ScoreArgs s{};
+        s.R = R0; s.ld = d->ld; s.nrows = N; s.perm = l == 0 ? nullptr : perm; s.items = items;
+        s.num_items = num_items; s.active = active;
+        s.table = t->staged_tables[l]; s.npad = lv.npad; s.kchunks = d->ld / 32; s.tmem_cols = lv.tmem_cols;
+        s.level = l; s.level_base = (int)t->level_offsets[l]; s.child_begin = t->child_begin;
+        s.child_count = t->child_count; s.path_ws = path_ws; s.path_out = path; s.count = count;
+        s.K = K; s.L = L; s.ip = ip; s.leaf_atom = t->leaf_atom;
+        s.ks_last = (d->n - 32 * (s.kchunks - 1) + 7) / 8;
+        if (l + 1 < L) {
+          s.next_counts = counts_of(it) + bin_off[l + 1];
+          s.next_base = (int)t->level_offsets[l + 1];
+        } else {
+          s.leaf_sel = leaf_sel;
+          s.bsel = bsel;
+        }
+        // the rows are x: scores corrected by the support's pair-table products
+        s.corr = t->pair_tables[l]; s.corr_w = t->pair_width[l]; s.corr_off = (int)t->level_offsets[l + 1];
+        s.sup = S_ws; s.supc = c_ws; s.sup_t = it; s.nsup = N;
+        if (l == 0) { s.raw_out = s0; s.raw_w = t->root_children; }
+        if ((e = launch_score_st(s, sms, st)) != cudaSuccess) return e;
+      }
+      ga.iter = it;
+      ga.root_counts = counts_of(it + 1) + bin_off[1];
+      if ((e = launch_update_gram(ga, st)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   const float* xtable = t ? nullptr : ensure_xtable(const_cast<DictHandle*>(d), st);
   if (!t && xtable == nullptr) return cudaErrorMemoryAllocation;
 
@@ -528,32 +620,19 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       const StagedLevel& lv = t->staged_levels[l];
       const int nb = (int)(t->level_offsets[l + 1] - t->level_offsets[l]);
       const bool direct_pass = l == 0 && root_direct;
-      if (!direct_pass && l > 0 && nb <= kScanRun * kScatterThreads) {
-        // scan fused into the scatter; counters double-buffered by iteration parity
-        const int per = N >= (int64_t)sms * kScatterThreads * 8 ? 8 : N >= (int64_t)sms * kScatterThreads * 2 ? 2 : 1;
-        const int grid = (int)((N + kScatterThreads * per - 1) / (kScatterThreads * per));
-        auto k = per == 8 ? scatter_scan_kernel<8> : per == 2 ? scatter_scan_kernel<2> : scatter_scan_kernel<1>;
-        const size_t smem = (size_t)nb * 16;
-        if (smem > 48 * 1024 &&
-            (e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+      if (!direct_pass && l > 0) {
+        if ((e = launch_level_scatter(N, active, path_ws, L, l, (int)t->level_offsets[l], nb, counts_of(it) + bin_off[l],
+                                      cursor_of(it) + bin_off[l], counts_of(it + 1) + bin_off[l],
+                                      cursor_of(it + 1) + bin_off[l], offsets, tile_off, cursor, perm, items,
+                                      num_items, sms, st)) != cudaSuccess)
           return e;
-        e = launch_kernel(k, grid, kScatterThreads, smem, st, true, N, (const int*)active, (const int*)path_ws, L, l,
-                          (int)t->level_offsets[l], nb, (const int*)(counts_of(it) + bin_off[l]),
-                          cursor_of(it) + bin_off[l], counts_of(it + 1) + bin_off[l], cursor_of(it + 1) + bin_off[l],
-                          perm, items, num_items);
+      } else if (!direct_pass) {   // root bin compaction (root_direct off)
+        e = launch_kernel(scan_kernel, 1, kScanThreads, scan_smem(nb), st, true, counts_of(it) + bin_off[l], nb,
+                          offsets, items, num_items, tile_off, cursor, stripes);
+        if (e == cudaSuccess)
+          e = launch_kernel(scatter_root_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
+                            (const int*)offsets, cursor, perm);
         if (e != cudaSuccess) return e;
-      } else if (!direct_pass) {
-      e = launch_kernel(scan_kernel, 1, kScanThreads, scan_smem(nb), st, true, counts_of(it) + bin_off[l], nb, offsets,
-                        items, num_items, tile_off, cursor, l == 0 ? stripes : nullptr);
-      if (e != cudaSuccess) return e;
-      if (l == 0)
-        e = launch_kernel(scatter_root_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
-                          (const int*)offsets, cursor, perm);
-      else
-        e = launch_kernel(scatter_kernel, scatter_blocks, 256, 0, st, true, N, (const int*)active,
-                          (const int*)path_ws, L, l, (int)t->level_offsets[l], (const int*)offsets, cursor,
-                          perm);
-      if (e != cudaSuccess) return e;
       }
       ScoreArgs s{};
       s.R = it == 0 ? R0 : R; s.ld = d->ld; s.nrows = N; s.perm = direct_pass ? nullptr : perm; s.items = items;

@@ -1,0 +1,357 @@
+// Gram path of the staged OMP encoder: no residual in HBM.
+//
+// The residual-based pipeline reads and writes r = x - A_S c every iteration
+// and rebuilds it from the T support rows: for 1600-dim light-field atoms
+// (config 4) that is ~6.4 KB x (T + 3) per patch and iteration, 60 % of the
+// step.  With 180 GB of HBM the products every score needs can instead be
+// tabulated once per tree: for each level l, P_l[a][v] = c_v . a_a over the
+// depth-(l+1) nodes v and all atoms a (config 4: 64 + 4096 + 131072 columns,
+// 71 GB; the last level's nodes are single atoms, so P_{L-1} is the Gram matrix
+// in leaf order).  Then
+//   * a child's score is c_v . r = c_v . x - sum_k c_k P_l[S_k][v]: the score
+//     passes multiply the patches x (not r) on the tensor cores and subtract the
+//     support's contribution in the epilogue (score_st.cu);
+//   * the root scores c_v . x never change: iteration 0 stores them, later
+//     iterations only subtract the correction (this file, fused into the update);
+//   * the OMP refit needs the Gram column g_k = a . a_{S_k} = P_{L-1}[S_k][pos(a)]
+//     and b = a . x (the winner's raw score from the last pass); the inverse
+//     Cholesky factor update is the one of the lockstep kernel (encode_update.cu);
+//   * ||r||^2 = ||x||^2 - sum_j y_j^2 (y = M A_S^T x), accumulated in f64.  When
+//     it falls below rho ||x||^2 the cancellation is large, so the update
+//     computes the residual norm explicitly from x and the support rows.
+// Semantics are the OMP restatement of SURVEY §8c over pursuit.py:112-162 and
+// omp_refit (pursuit.py:235-250); scores differ from the residual form only by
+// rounding (c . x and the table products are fp32-accurate), so decisions can
+// differ only at near ties.
+#include <cublas_v2.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "sm100.cuh"
+#include "staged.cuh"
+
+namespace stmp {
+
+int g_gram_path = 1;
+
+namespace {
+
+constexpr int kMaxGramK = 16;
+
+// every depth-L node has one leaf whose atom equals the node's centroid bitwise
+__global__ void leaf_atom_check_kernel(const float* __restrict__ cent, const float* __restrict__ atoms, int ld,
+                                       const int* child_begin, const int* leaf_atom, int64_t v0, int64_t nv,
+                                       int* ok) {
+  const int64_t v = v0 + blockIdx.x;
+  if (blockIdx.x >= nv) return;
+  const int a = leaf_atom[child_begin[v]];
+  const float* c = cent + v * (int64_t)ld;
+  const float* r = atoms + (int64_t)a * ld;
+  for (int i = threadIdx.x; i < ld; i += blockDim.x)
+    if (__float_as_uint(c[i]) != __float_as_uint(r[i])) atomicExch(ok, 0);
+}
+
+__global__ void leaf_pos_kernel(const int* child_begin, const int* leaf_atom, int64_t v0, int64_t nv, int* pos) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nv) pos[leaf_atom[child_begin[v0 + i]]] = (int)i;
+}
+
+__global__ void __launch_bounds__(256) gram_init_kernel(const float* __restrict__ X, int64_t ldx, int n, int64_t N,
+                                                        double* xn2, double* e) {
+  pdl_enter();
+  const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= N) return;
+  const float* xp = X + p * ldx;
+  double s = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    const double v = xp[i];
+    s += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if (lane == 0) {
+    xn2[p] = s;
+    e[p] = s;
+  }
+}
+
+// Explicit ||x - sum_k c_k a_{S_k}||^2 (f64 accumulation of f32 terms), one thread.
+template <int T>
+__device__ double explicit_resnorm2(const GramArgs& a, int64_t p, const int (&S)[T + 1], const float (&c)[T + 1]) {
+  const float* xp = a.X + p * a.ldx;
+  double s = 0.0;
+  for (int i = 0; i < a.n; ++i) {
+    float r = __ldg(xp + i);
+#pragma unroll
+    for (int k = 0; k <= T; ++k) r = fmaf(-c[k], __ldg(a.atoms + (int64_t)S[k] * a.ld + i), r);
+    s += (double)r * r;
+  }
+  return s;
+}
+
+// One thread per patch.  Iteration T (= support size): refit with the winner of
+// the last score pass, then (if the patch goes on) the next iteration's root
+// choice from the cached root scores.
+template <int T>
+__global__ void __launch_bounds__(128) update_gram_kernel(GramArgs a) {
+  pdl_enter();
+  __shared__ int hist[256];
+  for (int i = threadIdx.x; i < a.root_w; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const int64_t N = a.N;
+  const int K = a.K;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool inb = p < N;
+  const int64_t pc = inb ? p : 0;
+  const bool act = inb && a.active[pc] != 0;
+  bool act_next = false;
+  int S[T + 1];
+  float c[T + 1];
+  if (act) {
+    float y[T + 1], g[T + 1], w[T + 1];
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      S[k] = a.S_ws[k * N + p];
+      c[k] = a.c_ws[k * N + p];
+      y[k] = a.yv[k * N + p];
+    }
+    const int atom = a.leaf_sel[p];
+    const float bt = a.bsel[p];
+    const int pa = __ldg(a.leaf_pos + atom);
+    bool dup = false;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      dup |= S[k] == atom;
+      g[k] = __ldg(a.gram + (int64_t)S[k] * a.gram_w + pa);   // a . a_{S_k}
+    }
+    const float gtt = __ldg(a.gram + (int64_t)atom * a.gram_w + pa);
+    // w = M g, with M = L^{-1} packed by rows in [entry][patch] order
+    float gc = 0.f, wsum = 0.f, wy = 0.f;
+#pragma unroll
+    for (int j = 0; j < T; ++j) {
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k <= j; ++k) s = fmaf(a.Lf[(int64_t)(j * (j + 1) / 2 + k) * N + p], g[k], s);
+      w[j] = s;
+      gc = fmaf(g[j], c[j], gc);
+      wsum = fmaf(s, s, wsum);
+      wy = fmaf(s, y[j], wy);
+    }
+    const float score = bt - gc;   // a . r (pursuit.py:217 zero-score stop)
+    const bool ok = !dup && score != 0.f;
+    const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
+    const float inv_d = 1.f / dg;
+    const float yy = (bt - wy) * inv_d;
+    // new row T of M: -(1/d) w^T M and 1/d;  c_new = c_prev + m_T y_T
+    float mt[T + 1], cn[T + 1];
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      float s = 0.f;
+#pragma unroll
+      for (int j = k; j < T; ++j) s = fmaf(w[j], a.Lf[(int64_t)(j * (j + 1) / 2 + k) * N + p], s);
+      mt[k] = -inv_d * s;
+      cn[k] = fmaf(mt[k], yy, c[k]);
+    }
+    mt[T] = inv_d;
+    cn[T] = inv_d * yy;
+    S[T] = atom;
+    if (ok) {
+      double e = a.e_ws[p] - (double)yy * yy;
+      const double xn2 = a.xn2[p];
+      if (e < (double)a.rho * xn2) e = explicit_resnorm2<T>(a, p, S, cn);
+      const float rn = (float)sqrt(fmax(e, 0.0));
+      act_next = (T + 1 < K) && rn > a.tol[p];
+      a.count[p] = T + 1;
+      a.resnorm[p] = rn;
+      if (act_next) {
+#pragma unroll
+        for (int k = 0; k <= T; ++k) {
+          a.Lf[(int64_t)(T * (T + 1) / 2 + k) * N + p] = mt[k];
+          a.c_ws[k * N + p] = cn[k];
+        }
+        a.yv[T * N + p] = yy;
+        a.S_ws[T * N + p] = atom;
+        a.e_ws[p] = e;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k <= T; ++k) c[k] = ok || k == T ? cn[k] : c[k];
+    if (!act_next) {
+      // final rows of the caller's idx / coef (T or T + 1 entries; the rest stay -1 / 0 from init)
+      const int n_out = ok ? T + 1 : T;
+#pragma unroll
+      for (int k = 0; k <= T; ++k)
+        if (k < n_out) {
+          a.idx[p * K + k] = S[k];
+          a.coef[p * K + k] = c[k];
+        }
+    }
+    a.active[p] = act_next ? 1 : 0;
+  }
+  // next iteration's root choice: s_v = (c_v . x) - sum_k c_k P_0[S_k][v],
+  // first max of |s| in child order (pursuit.py:151)
+  int best = -1;
+  if (act_next) {
+    const float* s0 = a.s0 + p * a.root_w;
+    float bestv = -1.f;
+    for (int c0 = 0; c0 < a.root_w; c0 += 32) {
+      float v[32];
+      const int nc = min(32, a.root_w - c0);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = j < nc ? __ldg(s0 + c0 + j) : 0.f;
+#pragma unroll
+      for (int k = 0; k <= T; ++k) {
+        const float* row = a.root_tab + (int64_t)S[k] * a.root_w + c0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nc) v[j] = fmaf(-c[k], __ldg(row + j), v[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nc && fabsf(v[j]) > bestv) {
+          bestv = fabsf(v[j]);
+          best = c0 + j;
+        }
+    }
+    const int child = a.root_cb + best;
+    a.path_ws[p * a.L] = child;
+    if (a.path_out) a.path_out[(p * K + (T + 1)) * a.L] = child;
+    if (a.ip) add_ip(a.ip, p, a.root_w, a.root_w);
+    atomicAdd(&hist[best], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.root_w; i += blockDim.x)
+    if (hist[i]) atomicAdd(&a.root_counts[i], hist[i]);
+}
+
+cublasHandle_t blas_handle() {
+  static cublasHandle_t h = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) h = nullptr;
+    // plain fp32 FFMA GEMMs: the tables must be fp32-accurate (no TF32)
+    if (h) cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);
+  });
+  return h;
+}
+
+}  // namespace
+
+bool gram_path_supported(const DictHandle* d, const TreeHandle* t, int K, int method) {
+  if (t == nullptr || method != kMethodOMP || K > kMaxGramK || g_gram_path == 0 || t->levels < 2) return false;
+  if (t->max_leaf_children != 1 || t->num_leaves != d->m || t->leaf_pos == nullptr) return false;
+  if (t->root_children > 256) return false;
+  if (g_gram_path == 2) return true;
+  // auto: rows much wider than the nodes, where the residual traffic dominates
+  int maxk = 0;
+  for (int k : t->branching) maxk = std::max(maxk, k);
+  return d->n >= 256 && d->n >= 8 * maxk;
+}
+
+bool ensure_pair_tables(TreeHandle* t, const DictHandle* d, cudaStream_t st) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (t->pair_tried) return !t->pair_tables.empty();
+  t->pair_tried = true;
+  const int L = t->levels;
+  const int64_t m = d->m;
+  // the last level's centroids must be the atoms themselves
+  {
+    int* ok = nullptr;
+    if (cudaMalloc(&ok, sizeof(int)) != cudaSuccess) return false;
+    const int one = 1;
+    cudaMemcpyAsync(ok, &one, sizeof(int), cudaMemcpyHostToDevice, st);
+    const int64_t v0 = t->level_offsets[L], nv = t->level_offsets[L + 1] - v0;
+    leaf_atom_check_kernel<<<(unsigned)nv, 128, 0, st>>>(t->cent, d->atoms, d->ld, t->child_begin, t->leaf_atom, v0,
+                                                         nv, ok);
+    note_launch();
+    int h = 0;
+    cudaMemcpyAsync(&h, ok, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(ok);
+    t->leaf_is_atom = (e == cudaSuccess && h) ? 1 : 0;
+    if (!t->leaf_is_atom) return false;
+  }
+  std::vector<int64_t> width(L);
+  size_t total = 0;
+  for (int l = 0; l < L; ++l) {
+    width[l] = t->level_offsets[l + 2] - t->level_offsets[l + 1];
+    total += (size_t)m * width[l] * sizeof(float);
+  }
+  size_t free_b = 0, tot_b = 0;
+  if (cudaMemGetInfo(&free_b, &tot_b) != cudaSuccess || total + (4ull << 30) > free_b) return false;
+  cublasHandle_t h = blas_handle();
+  if (h == nullptr || cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) return false;
+  std::vector<float*> tabs(L, nullptr);
+  bool good = true;
+  for (int l = 0; l < L && good; ++l) {
+    if (cudaMalloc(&tabs[l], (size_t)m * width[l] * sizeof(float)) != cudaSuccess) {
+      good = false;
+      break;
+    }
+    // P_l [m][W] row-major = (C_l A^T) column-major W x m: cent rows of depth l + 1
+    const float* cent = t->cent + t->level_offsets[l + 1] * (int64_t)d->ld;
+    const float one = 1.f, zero = 0.f;
+    const int64_t blk = 8192;
+    for (int64_t a0 = 0; a0 < m && good; a0 += blk) {
+      const int mb = (int)std::min(blk, m - a0);
+      good = cublasSgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)width[l], mb, d->n, &one, cent, d->ld,
+                         d->atoms + a0 * d->ld, d->ld, &zero, tabs[l] + a0 * width[l], (int)width[l]) ==
+             CUBLAS_STATUS_SUCCESS;
+    }
+  }
+  if (good) good = cudaStreamSynchronize(st) == cudaSuccess;
+  if (!good) {
+    for (float* p : tabs) cudaFree(p);
+    cudaGetLastError();
+    return false;
+  }
+  t->pair_tables = tabs;
+  t->pair_width = width;
+  return true;
+}
+
+// leaf_pos (host-side at tree creation would need the leaf order; done here on the device)
+bool build_leaf_pos(TreeHandle* t, int64_t m, cudaStream_t st) {
+  const int L = t->levels;
+  const int64_t v0 = t->level_offsets[L], nv = t->level_offsets[L + 1] - v0;
+  if (t->max_leaf_children != 1 || nv != m || t->num_leaves != m) return false;
+  if (cudaMalloc(&t->leaf_pos, m * sizeof(int)) != cudaSuccess) {
+    t->leaf_pos = nullptr;
+    return false;
+  }
+  leaf_pos_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(t->child_begin, t->leaf_atom, v0, nv, t->leaf_pos);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess;
+}
+
+void free_pair_tables(TreeHandle* t) {
+  for (float* p : t->pair_tables) cudaFree(p);
+  t->pair_tables.clear();
+  cudaFree(t->leaf_pos);
+  t->leaf_pos = nullptr;
+}
+
+cudaError_t launch_gram_init(const float* X, int64_t ldx, int n, int64_t N, double* xn2, double* e_ws,
+                             cudaStream_t st) {
+  return launch_kernel(gram_init_kernel, (unsigned)((N + 7) / 8), 256, 0, st, true, X, ldx, n, N, xn2, e_ws);
+}
+
+cudaError_t launch_update_gram(const GramArgs& a, cudaStream_t st) {
+  const unsigned blocks = (unsigned)((a.N + 127) / 128);
+  switch (a.iter) {
+#define STMP_GRAM_CASE(t) \
+  case t: return launch_kernel(update_gram_kernel<t>, blocks, 128, 0, st, true, a);
+    STMP_GRAM_CASE(0) STMP_GRAM_CASE(1) STMP_GRAM_CASE(2) STMP_GRAM_CASE(3) STMP_GRAM_CASE(4) STMP_GRAM_CASE(5)
+    STMP_GRAM_CASE(6) STMP_GRAM_CASE(7) STMP_GRAM_CASE(8) STMP_GRAM_CASE(9) STMP_GRAM_CASE(10) STMP_GRAM_CASE(11)
+    STMP_GRAM_CASE(12) STMP_GRAM_CASE(13) STMP_GRAM_CASE(14) STMP_GRAM_CASE(15)
+#undef STMP_GRAM_CASE
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace stmp

@@ -63,6 +63,60 @@ __host__ __device__ inline StLayout st_layout(int npad, bool last, int na, int n
   return L;
 }
 
+// Epilogue of the Gram path (gram_path.cu): the accumulator holds c_v . x for
+// the node's cc children; subtract the support's contribution
+// sum_k c_k P[S_k][colbase + v] (the patch's current OMP support and
+// coefficients), then the first max of |score| in child order
+// (pursuit.py:151).  `rawbest` is the winner's uncorrected c . x (for the last
+// level: a . x, the OMP right-hand side); iteration 0's root pass also stores
+// every raw score (raw_out) for the later root choices.  p < 0: no patch row.
+__device__ __forceinline__ void corr_abs_argmax(uint32_t taddr, int cc, const ScoreArgs& a, int p, int colbase,
+                                                float& bestv, int& best, float& rawbest) {
+  const int T = p >= 0 && a.corr ? a.sup_t : 0;
+  const bool vec = ((colbase | (int)a.corr_w) & 3) == 0;
+  for (int c0 = 0; c0 < cc; c0 += 32) {
+    float v[32];
+    tmem_ld32(taddr + (uint32_t)c0, v);   // every lane of the warp takes part
+    if (p < 0) continue;
+    const int nc = min(32, cc - c0);
+    float raw[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) raw[j] = v[j];
+    if (a.raw_out) {
+      float* dst = a.raw_out + (int64_t)p * a.raw_w + c0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nc && c0 + j < a.raw_w) dst[j] = v[j];
+    }
+    for (int k = 0; k < T; ++k) {
+      const int sk = __ldg(a.sup + (int64_t)k * a.nsup + p);
+      const float ck = __ldg(a.supc + (int64_t)k * a.nsup + p);
+      const float* row = a.corr + (int64_t)sk * a.corr_w + colbase + c0;
+      if (vec && nc == 32) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 t4 = __ldg(reinterpret_cast<const float4*>(row) + q);
+          v[4 * q] = fmaf(-ck, t4.x, v[4 * q]);
+          v[4 * q + 1] = fmaf(-ck, t4.y, v[4 * q + 1]);
+          v[4 * q + 2] = fmaf(-ck, t4.z, v[4 * q + 2]);
+          v[4 * q + 3] = fmaf(-ck, t4.w, v[4 * q + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nc) v[j] = fmaf(-ck, __ldg(row + j), v[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nc && fabsf(v[j]) > bestv) {
+        bestv = fabsf(v[j]);
+        best = c0 + j;
+        rawbest = raw[j];
+      }
+  }
+}
+
 template <int NA, int NB>
 __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int nacc) {
   pdl_enter();
@@ -242,12 +296,18 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       const int cb = __ldg(a.child_begin + gnode);
       const int cc = __ldg(a.child_count + gnode);
       int best = 0;
-      float bestv = -1.f;
-      tmem_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * accw, (int)accw, npad, bestv, best);
-      tc_fence_before();
-      mbar_arrive(&accempty[acc]);
+      float bestv = -1.f, rawbest = 0.f;
       const bool valid = tid < cur_rows && cur_p >= 0;
       const int p = cur_p;
+      if (a.corr != nullptr || a.raw_out != nullptr) {
+        // Gram path: rows are x; score = c . x - sum_k c_k P[S_k][child] (gram_path.cu)
+        corr_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * accw, cc, a, valid ? p : -1,
+                        cb - a.corr_off, bestv, best, rawbest);
+      } else {
+        tmem_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * accw, (int)accw, npad, bestv, best);
+      }
+      tc_fence_before();
+      mbar_arrive(&accempty[acc]);
       int leaf_info = 0, leaf_cnt = 0;
       if (last && valid) {   // the winner's leaf record, straight from the (L2-resident) table block
         const int* info = reinterpret_cast<const int*>(reinterpret_cast<const uint8_t*>(a.table) +
@@ -261,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
         if (a.path_out) a.path_out[((int64_t)p * a.K + a.count[p]) * a.L + a.level] = child;
         if (a.next_counts) atomicAdd(&s_hist[best], 1);
         if (last) a.leaf_sel[p] = leaf_info;
+        if (last && a.bsel) a.bsel[p] = rawbest;
         if (a.ip) add_ip(a.ip, p, cc + leaf_cnt, cc);
       }
       if (a.next_counts) {

@@ -35,6 +35,19 @@ struct ScoreArgs {
   const int* active;     // root pass in patch order (perm == nullptr): skip inactive rows
   int ks_last;           // 8-column k-steps holding data in the last 32-column chunk (1..4): the
                          // rest are zero padding on both operands and their MMAs are skipped
+
+  // ---- Gram path (gram_path.cu): the rows are the patches x, not residuals, and
+  // a child's score is corrected to c . r = c . x - sum_k c_k (c . a_{S_k})
+  const float* corr;     // pair table of this level: [m][corr_w], row = atom, column = child node
+  int64_t corr_w;        // columns per row (nodes at depth level + 1)
+  int corr_off;          // global id of the first depth-(level + 1) node (column 0)
+  const int* sup;        // support atoms [K][N] (S_ws), the first `sup_t` entries valid
+  const float* supc;     // current coefficients [K][N] (c_ws)
+  int sup_t;             // support size of every active patch (the iteration index)
+  int64_t nsup;          // N: stride of sup / supc
+  float* raw_out;        // root pass of iteration 0: raw scores c . x of all children -> [N][raw_w]
+  int raw_w;
+  float* bsel;           // last level: raw score a . x of the winning leaf atom -> [N]
 };
 
 // Work items of a score pass: (bin, first slot in perm, rows) from the scan, or
@@ -92,6 +105,55 @@ struct UpdateArgs {
   float* c_ws;           // coefficients [K][N]
   int iter;              // iteration index = support size of every active patch
 };
+
+// Gram path (gram_path.cu, OMP on trees whose depth-L nodes are single atoms):
+// no residual is kept; every score is c . x minus the support's contribution
+// read from per-level pair tables, and the OMP update works on Gram entries.
+struct GramArgs {
+  int64_t N;
+  int K, L, iter;
+  const int* leaf_sel;     // atom chosen by the last score pass
+  const float* bsel;       // its raw score a . x
+  const float* gram;       // pair table of the last level = the Gram matrix in leaf order [m][m]
+  int64_t gram_w;
+  const int* leaf_pos;     // [m] column of each atom in the last-level table
+  const float* root_tab;   // pair table of level 0 [m][root_w]
+  const float* s0;         // cached root scores c . x [N][root_w]
+  int root_w, root_cb;     // root children: count, first global id
+  int* root_counts;        // level-1 bin counters of the next iteration
+  int* path_ws;
+  int32_t* path_out;
+  int* S_ws;
+  float* c_ws;
+  float* yv;
+  float* Lf;
+  double* e_ws;            // ||r||^2 = ||x||^2 - sum_j y_j^2 (f64)
+  const double* xn2;       // ||x||^2
+  const float* tol;
+  int* active;
+  int32_t* idx;
+  float* coef;
+  int32_t* count;
+  float* resnorm;
+  int32_t* ip;
+  // explicit residual norm for patches whose ||r||^2 estimate falls below
+  // rho ||x||^2 (cancellation): x and the support rows
+  const float* X;
+  int64_t ldx;
+  const float* atoms;
+  int ld, n;
+  float rho;
+};
+bool gram_path_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
+// builds the pair tables on first use; false if they cannot be allocated
+bool ensure_pair_tables(TreeHandle* t, const DictHandle* d, cudaStream_t st);
+cudaError_t launch_update_gram(const GramArgs& a, cudaStream_t st);
+// leaf_pos of a tree whose depth-L nodes are single atoms covering the dictionary
+bool build_leaf_pos(TreeHandle* t, int64_t m, cudaStream_t st);
+void free_pair_tables(TreeHandle* t);
+cudaError_t launch_gram_init(const float* X, int64_t ldx, int n, int64_t N, double* xn2, double* e_ws,
+                             cudaStream_t st);
+extern int g_gram_path;   // 0 off, 1 auto (wide rows), 2 whenever supported
 
 struct UpdateCfg {
   int G = 0;   // lanes per patch

@@ -28,11 +28,13 @@ def P():
     return pkg
 
 
-# (score_kernel, update_kernel) per staged variant; library defaults are (2, 1).
-# Every id runs a distinct kernel set: the whole-table score pass (score_ts) or
-# the streamed one (score_st) at every level, the lockstep / wide-row OMP update
-# or the generic one.
-STAGED_KERNELS = {"staged-ts": (2, 1), "staged-st": (3, 1), "staged-generic": (2, 0)}
+# (score_kernel, update_kernel, gram_path) per staged variant; library defaults
+# are (2, 1, 1).  Every id runs a distinct kernel set: the whole-table score pass
+# (score_ts) or the streamed one (score_st) at every level; the lockstep /
+# wide-row OMP update or the generic one; the Gram path (no residual, pair
+# tables; auto = config 4) forced on, or off.
+STAGED_KERNELS = {"staged-ts": (2, 1, 1), "staged-st": (3, 1, 1), "staged-generic": (2, 0, 0),
+                  "staged-resid": (2, 1, 0), "staged-gram": (2, 1, 2)}
 PATHS = ["fused", *STAGED_KERNELS]
 
 
@@ -40,6 +42,7 @@ def restore_defaults(_lib):
     _lib.set_option("path", _lib.PATH_AUTO)
     _lib.set_option("score_kernel", 2)
     _lib.set_option("update_kernel", 1)
+    _lib.set_option("gram_path", 1)
 
 
 @pytest.fixture(params=PATHS)
@@ -49,14 +52,15 @@ def path(request):
     from paper_1412_0680_b200 import _lib
     mode = request.param
     _lib.set_option("path", _lib.PATH_FUSED if mode == "fused" else _lib.PATH_STAGED)
-    sk, uk = STAGED_KERNELS.get(mode, (2, 1))
+    sk, uk, gp = STAGED_KERNELS.get(mode, (2, 1, 1))
     _lib.set_option("score_kernel", sk)
     _lib.set_option("update_kernel", uk)
+    _lib.set_option("gram_path", gp)
     yield mode
     restore_defaults(_lib)
 
 
-@pytest.mark.parametrize("kernels", sorted(set(STAGED_KERNELS.values())))
+@pytest.mark.parametrize("kernels", sorted(set(STAGED_KERNELS.values()) - {(2, 1, 0)}))
 def test_staged_is_deterministic_and_batch_invariant(kernels):
     """262,144 config-1 patches: two runs and a run in 8192-patch batches must agree
     bitwise (each patch's arithmetic is independent of bucketing order)."""
@@ -68,6 +72,7 @@ def test_staged_is_deterministic_and_batch_invariant(kernels):
     _lib.set_option("path", _lib.PATH_STAGED)
     _lib.set_option("score_kernel", kernels[0])
     _lib.set_option("update_kernel", kernels[1])
+    _lib.set_option("gram_path", kernels[2])
     try:
         a = P().encode(sel, X, cfg.K, method="omp")
         b = P().encode(sel, X, cfg.K, method="omp")
@@ -298,9 +303,33 @@ def oracle_config(cid, rows, method, exhaustive=False):
 def _tree_cases():
     cases = [(0, 10_000, "omp"), (0, 10_000, "mp"), (1, 16_384, "omp"), (1, 4096, "mp"),
              (2, 16_384, "omp"), (3, 16_384, "omp"), (4, 512, "omp"), (4, 256, "mp")]
-    # configs 2 and 4 have no node table that fits shared memory: their default
-    # already streams every table, so "staged-st" would rerun the same kernels
-    return [(c, r, m, p) for c, r, m in cases for p in PATHS if not (p == "staged-st" and c in (2, 4))]
+    # ids that would rerun the default kernels of a config are left out:
+    # configs 2 and 4 already stream every node table ("staged-st"); only config 4
+    # takes the Gram path by default ("staged-resid" elsewhere = "staged-ts"); config
+    # 3's ragged last level has a centroid that is not its atom and config 4 is on
+    # the Gram path already ("staged-gram"); the Gram path is OMP only.
+    skip = {("staged-st", 2), ("staged-st", 4), ("staged-resid", 0), ("staged-resid", 1), ("staged-resid", 2),
+            ("staged-resid", 3), ("staged-gram", 3), ("staged-gram", 4)}
+    return [(c, r, m, p) for c, r, m in cases for p in PATHS
+            if (p, c) not in skip and not (m == "mp" and p in ("staged-gram", "staged-resid"))]
+
+
+def launched(fn):
+    """Run fn() and return (its result, the set of library kernel names it launched)."""
+    from paper_1412_0680_b200 import _lib
+    _lib.kernel_timing(True)
+    try:
+        res = fn()
+        torch.cuda.synchronize()
+        names = set(_lib.kernel_times())
+    finally:
+        _lib.kernel_timing(False)
+    return res, names
+
+
+def expects_gram(cid, method, path):
+    return method == "omp" and ((path in ("staged-ts", "staged-st") and cid == 4) or
+                                (path == "staged-gram" and cid in (0, 1, 2)))
 
 
 @pytest.mark.parametrize("cid,rows,method,path", _tree_cases(), indirect=["path"])
@@ -308,7 +337,9 @@ def test_config_tree_parity(cid, rows, method, path):
     cfg, wl, flat = config(cid)
     X, ref = oracle_config(cid, rows, method)
     sel = P().TreeSelector(flat, wl.atoms, cfg.alpha)
-    out = run(sel, X, cfg.K, method)
+    out, names = launched(lambda: run(sel, X, cfg.K, method))
+    gram = any("update_gram_kernel" in k for k in names)
+    assert gram == expects_gram(cid, method, path), sorted(names)
     rep = compare(out, ref, X)
     print(f"c{cid} {method} {path}: {rep.summary()}")
     assert rep.ok, rep.summary()
@@ -452,4 +483,53 @@ def test_update_variants_match_oracle(shape):
     rows = slice(0, 512)   # the oracle on a prefix keeps the test short; the GPU encoded all N
     ref = oracle_pack(O.tree_selector(O.OracleTree.from_flat(flat), a64, 1 / 8), a64, X[rows], K, "omp")
     rep = compare({k: v[rows] for k, v in out.items()}, ref, X[rows], check_path=True)
+    assert rep.ok, rep.summary()
+
+
+@pytest.mark.parametrize("tol_tag,tol", [("deftol", None), ("tol0", 0.0)])
+def test_gram_path_exact_sparse_and_tolerance(tol_tag, tol):
+    """Gram path (no residual) on exactly sparse patches: the ||r||^2 estimate
+    ||x||^2 - sum y^2 cancels, so the update must fall back to the explicit
+    residual norm for the stopping rule (pursuit.py:214) and the reported norm.
+    256-dim rows (auto-enabled), single-atom leaves equal to their centroids."""
+    from paper_1412_0680_b200 import _lib
+    from paper_1412_0680_b200 import tree as T
+    rng = np.random.default_rng(21)
+    m, n, br = 1024, 256, (8, 8, 16)
+    atoms = rng.standard_normal((m, n))
+    atoms = (atoms / np.linalg.norm(atoms, axis=1, keepdims=True)).astype(np.float32)
+    cbd = [[8], [8] * 8, [16] * 64, [1] * 1024]
+    leaf = rng.permutation(m)
+    ni = sum(len(c) for c in cbd)
+    flat = T._from_counts(br, n, P().fingerprint_atoms(atoms), cbd, np.zeros((ni, n), np.float32), leaf)
+    off = flat.level_offsets
+    sums = np.zeros((ni, n))
+    for v in range(off[3], off[4]):
+        sums[v] = atoms[leaf[flat.child_begin[v]]]
+    for d in (2, 1, 0):
+        for v in range(off[d], off[d + 1]):
+            sums[v] = sums[flat.child_begin[v]:flat.child_begin[v] + flat.child_count[v]].sum(0)
+    cent = (sums / np.linalg.norm(sums, axis=1, keepdims=True)).astype(np.float32)
+    cent[off[3]:off[4]] = atoms[leaf]          # depth-L centroids are the atoms themselves
+    flat = T._from_counts(br, n, P().fingerprint_atoms(atoms), cbd, cent, leaf)
+    N, K = 4096, 8
+    X = np.zeros((N, n))
+    for p in range(N):
+        sup = rng.choice(m, 3, replace=False)
+        X[p] = rng.standard_normal(3) @ atoms[sup].astype(np.float64)
+        if p % 2:
+            X[p] += 0.05 * rng.standard_normal(n)   # half the patches noisy
+    X = X.astype(np.float32)
+    sel = P().TreeSelector(flat, atoms, 1 / 16)
+    _lib.set_option("path", _lib.PATH_STAGED)
+    try:
+        out, names = launched(lambda: run(sel, X, K, "omp", tol))
+    finally:
+        restore_defaults(_lib)
+    assert any("update_gram_kernel" in k for k in names), sorted(names)
+    a64 = atoms.astype(np.float64)
+    rows = slice(0, 1024)
+    ref = oracle_pack(O.tree_selector(O.OracleTree.from_flat(flat), a64, 1 / 16), a64, X[rows], K, "omp", tol)
+    rep = compare({k: v[rows] for k, v in out.items()}, ref, X[rows], check_path=True)
+    print(f"gram exact-sparse {tol_tag}: {rep.summary()}")
     assert rep.ok, rep.summary()
