@@ -33,6 +33,7 @@ class ParityReport:
     excused_by_reason: dict = field(default_factory=lambda: {"near_tie": 0, "noise_residual": 0,
                                                              "noise_stop_ip": 0})
     failures: list = field(default_factory=list)
+    failures_by_kind: dict = field(default_factory=lambda: {"idx": 0, "coef": 0, "resnorm": 0, "ip": 0, "path": 0})
     max_coef_rel: float = 0.0
     max_res_rel: float = 0.0
 
@@ -42,13 +43,14 @@ class ParityReport:
 
     def summary(self) -> str:
         head = (f"{self.patches} patches, {self.excused} excused {self.excused_by_reason}, "
-                f"{len(self.failures)} failures, max coef rel err {self.max_coef_rel:.2e}, "
+                f"{len(self.failures)} failures {self.failures_by_kind}, max coef rel err {self.max_coef_rel:.2e}, "
                 f"max resnorm rel err {self.max_res_rel:.2e}")
         return head + ("" if self.ok else "\n  " + "\n  ".join(self.failures[:10]))
 
     def as_dict(self) -> dict:
         return {"patches": self.patches, "excused_near_ties": self.excused_by_reason["near_tie"],
                 "excused_by_reason": dict(self.excused_by_reason), "failures": len(self.failures),
+                "failures_by_kind": dict(self.failures_by_kind),
                 "max_coef_rel": self.max_coef_rel, "max_resnorm_rel": self.max_res_rel}
 
 
@@ -80,6 +82,7 @@ def compare(gpu: dict, ref: dict, X: np.ndarray, check_ip: bool = True, check_pa
                 rep.excused += 1
                 rep.excused_by_reason["near_tie" if g < near_tie else "noise_residual"] += 1
                 continue
+            rep.failures_by_kind["idx"] += 1
             rep.failures.append(f"patch {p}: iteration {diff_at} gpu {gi[p, :gc[p]].tolist()} "
                                 f"ref {ri[p, :rc[p]].tolist()} (gap {g:.2e})")
             continue
@@ -92,11 +95,13 @@ def compare(gpu: dict, ref: dict, X: np.ndarray, check_ip: bool = True, check_pa
             rel = float(np.max(err / np.maximum(np.abs(rcoef), atol / RTOL + 1e-300)))
             rep.max_coef_rel = max(rep.max_coef_rel, rel)
             if np.any(err > RTOL * np.abs(rcoef) + atol):
+                rep.failures_by_kind["coef"] += 1
                 rep.failures.append(f"patch {p}: coef gpu {gcoef} ref {rcoef}")
                 continue
         gr, rr = float(gpu["resnorm"][p]), float(ref["resnorm"][p])
         rep.max_res_rel = max(rep.max_res_rel, abs(gr - rr) / max(rr, atol / RTOL, 1e-300))
         if abs(gr - rr) > RTOL * rr + atol:
+            rep.failures_by_kind["resnorm"] += 1
             rep.failures.append(f"patch {p}: resnorm gpu {gr} ref {rr}")
             continue
         noisy = rnorm_rel is not None and bool(np.any(rnorm_rel[p] < NOISE_RESIDUAL))
@@ -108,11 +113,13 @@ def compare(gpu: dict, ref: dict, X: np.ndarray, check_ip: bool = True, check_pa
             continue
         if check_ip and "ip" in gpu and "ip" in ref and gpu["ip"] is not None:
             if not np.array_equal(np.asarray(gpu["ip"][p], dtype=np.int64), np.asarray(ref["ip"][p], dtype=np.int64)):
+                rep.failures_by_kind["ip"] += 1
                 rep.failures.append(f"patch {p}: ip gpu {gpu['ip'][p]} ref {ref['ip'][p]}")
                 continue
         if check_path and gpu.get("path") is not None and ref.get("path") is not None:
             gp = np.asarray(gpu["path"][p, :c])
             rp = np.asarray(ref["path"][p, :c])
             if not np.array_equal(gp, rp):
+                rep.failures_by_kind["path"] += 1
                 rep.failures.append(f"patch {p}: path gpu {gp.tolist()} ref {rp.tolist()}")
     return rep

@@ -555,7 +555,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
     ga.path_ws = path_ws; ga.path_out = path; ga.S_ws = S_ws; ga.c_ws = c_ws; ga.yv = yv;
     ga.Lf = Lf; ga.e_ws = e_ws; ga.xn2 = xn2; ga.tol = tol; ga.active = active; ga.idx = idx; ga.coef = coef;
     ga.count = count; ga.resnorm = resnorm; ga.ip = ip;
-    ga.X = X; ga.ldx = ldx; ga.atoms = d->atoms; ga.ld = d->ld; ga.n = d->n; ga.rho = 1e-2f;
+    ga.xr = R0; ga.atoms = d->atoms; ga.cent = t->cent; ga.ld = d->ld; ga.rho = 1e-2f; ga.recheck_rel = 1e-5f;
     for (int it = 0; it < K; ++it) {
       for (int l = it == 0 ? 0 : 1; l < L; ++l) {
         const StagedLevel& lv = t->staged_levels[l];
@@ -583,8 +583,9 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
         }
         // the rows are x: scores corrected by the support's pair-table products
         s.corr = t->pair_tables[l]; s.corr_w = t->pair_width[l]; s.corr_off = (int)t->level_offsets[l + 1];
-        s.sup = S_ws; s.supc = c_ws; s.sup_t = it; s.nsup = N;
-        if (l == 0) { s.raw_out = s0; s.raw_w = t->root_children; }
+        s.sup = S_ws; s.supc = c_ws; s.sup_t = it; s.sup_ld = K;
+        s.cent = t->cent; s.xn2 = xn2; s.recheck_rel = 1e-5f;
+        if (l == 0) { s.raw_out = s0; s.raw_w = t->root_children; }   // iteration 0: cache c_v . x of the root
         if ((e = launch_score_st(s, sms, st)) != cudaSuccess) return e;
       }
       ga.iter = it;

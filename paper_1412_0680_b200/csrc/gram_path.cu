@@ -79,149 +79,217 @@ __global__ void __launch_bounds__(256) gram_init_kernel(const float* __restrict_
   }
 }
 
-// Explicit ||x - sum_k c_k a_{S_k}||^2 (f64 accumulation of f32 terms), one thread.
-template <int T>
-__device__ double explicit_resnorm2(const GramArgs& a, int64_t p, const int (&S)[T + 1], const float (&c)[T + 1]) {
-  const float* xp = a.X + p * a.ldx;
-  double s = 0.0;
-  for (int i = 0; i < a.n; ++i) {
-    float r = __ldg(xp + i);
-#pragma unroll
-    for (int k = 0; k <= T; ++k) r = fmaf(-c[k], __ldg(a.atoms + (int64_t)S[k] * a.ld + i), r);
-    s += (double)r * r;
+// Exact FFMA dot of two zero-padded rows of ld floats (16-byte aligned), one warp.
+__device__ __forceinline__ float warp_dot_rows(const float* __restrict__ x, const float* __restrict__ c, int ld) {
+  float s = 0.f;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const float4* c4 = reinterpret_cast<const float4*>(c);
+  for (int i = (int)(threadIdx.x & 31); i < ld / 4; i += 32) {
+    const float4 u = __ldg(x4 + i), v = __ldg(c4 + i);
+    s = fmaf(u.x, v.x, s);
+    s = fmaf(u.y, v.y, s);
+    s = fmaf(u.z, v.z, s);
+    s = fmaf(u.w, v.w, s);
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
   return s;
 }
 
-// One thread per patch.  Iteration T (= support size): refit with the winner of
-// the last score pass, then (if the patch goes on) the next iteration's root
-// choice from the cached root scores.
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// One warp per patch.  Iteration T (= support size of every active patch):
+//   * b = a . x of the atom the last score pass chose, as an exact FFMA dot (the
+//     tensor cores' truncating fp32 accumulation leaves ~1e-5 relative error on a
+//     1600-term dot: enough for the argmax with the near-tie re-check, not for
+//     the refit's right-hand side);
+//   * refit on Gram entries: g_k = P_{L-1}[S_k][pos(a)], lane j owning row j of
+//     the inverse Cholesky factor M = L^{-1} (as the lockstep kernel in
+//     encode_update.cu); ||r||^2 = ||x||^2 - sum_j y_j^2, or the explicit norm
+//     when that falls below rho ||x||^2;
+//   * if the patch goes on, the next iteration's root choice from the cached
+//     root scores s0, with the near-tie re-check (exact dots; the re-scored s0
+//     entries are written back).
+// Solver state is laid out per patch: S, c, y [N][K], M [N][K(K+1)/2].
 template <int T>
-__global__ void __launch_bounds__(128) update_gram_kernel(GramArgs a) {
+__global__ void __launch_bounds__(256) update_gram_kernel(GramArgs a) {
   pdl_enter();
   __shared__ int hist[256];
   for (int i = threadIdx.x; i < a.root_w; i += blockDim.x) hist[i] = 0;
   __syncthreads();
-  const int64_t N = a.N;
-  const int K = a.K;
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool inb = p < N;
-  const int64_t pc = inb ? p : 0;
-  const bool act = inb && a.active[pc] != 0;
-  bool act_next = false;
-  int S[T + 1];
-  float c[T + 1];
+  const int lane = threadIdx.x & 31;
+  const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const bool act = p < a.N && a.active[p] != 0;   // warp-uniform
   if (act) {
-    float y[T + 1], g[T + 1], w[T + 1];
-#pragma unroll
-    for (int k = 0; k < T; ++k) {
-      S[k] = a.S_ws[k * N + p];
-      c[k] = a.c_ws[k * N + p];
-      y[k] = a.yv[k * N + p];
-    }
+    const int K = a.K;
+    const int64_t KM = (int64_t)K * (K + 1) / 2;
+    const float* xr = a.xr + p * a.ld;
     const int atom = a.leaf_sel[p];
-    const float bt = a.bsel[p];
+    const float b = warp_dot_rows(xr, a.atoms + (int64_t)atom * a.ld, a.ld);
     const int pa = __ldg(a.leaf_pos + atom);
-    bool dup = false;
-#pragma unroll
-    for (int k = 0; k < T; ++k) {
-      dup |= S[k] == atom;
-      g[k] = __ldg(a.gram + (int64_t)S[k] * a.gram_w + pa);   // a . a_{S_k}
+    int Sk = 0;
+    float ck = 0.f, yk = 0.f, gk = 0.f;
+    if (lane < T) {
+      Sk = a.S_ws[p * K + lane];
+      ck = a.c_ws[p * K + lane];
+      yk = a.yv[p * K + lane];
+      gk = __ldg(a.gram + (int64_t)Sk * a.gram_w + pa);   // a . a_{S_k}
     }
     const float gtt = __ldg(a.gram + (int64_t)atom * a.gram_w + pa);
-    // w = M g, with M = L^{-1} packed by rows in [entry][patch] order
-    float gc = 0.f, wsum = 0.f, wy = 0.f;
+    const bool dup = __any_sync(kFull, lane < T && Sk == atom);
+    float mrow[T + 1];
 #pragma unroll
-    for (int j = 0; j < T; ++j) {
-      float s = 0.f;
+    for (int k = 0; k < T; ++k) mrow[k] = (lane < T && k <= lane) ? a.Lf[p * KM + lane * (lane + 1) / 2 + k] : 0.f;
+    float w = 0.f;
 #pragma unroll
-      for (int k = 0; k <= j; ++k) s = fmaf(a.Lf[(int64_t)(j * (j + 1) / 2 + k) * N + p], g[k], s);
-      w[j] = s;
-      gc = fmaf(g[j], c[j], gc);
-      wsum = fmaf(s, s, wsum);
-      wy = fmaf(s, y[j], wy);
-    }
-    const float score = bt - gc;   // a . r (pursuit.py:217 zero-score stop)
+    for (int k = 0; k < T; ++k) w = fmaf(mrow[k], __shfl_sync(kFull, gk, k), w);
+    const float gc = warp_sum_f(gk * ck);
+    const float wsum = warp_sum_f(w * w);
+    const float wy = warp_sum_f(w * yk);
+    const float score = b - gc;   // a . r (pursuit.py:217 zero-score stop)
     const bool ok = !dup && score != 0.f;
     const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
     const float inv_d = 1.f / dg;
-    const float yy = (bt - wy) * inv_d;
-    // new row T of M: -(1/d) w^T M and 1/d;  c_new = c_prev + m_T y_T
-    float mt[T + 1], cn[T + 1];
+    const float yy = (b - wy) * inv_d;
+    // column sums colw_k = sum_j w_j M[j][k] -> lane k; new row T of M and c_new
+    float colw = 0.f;
 #pragma unroll
     for (int k = 0; k < T; ++k) {
-      float s = 0.f;
-#pragma unroll
-      for (int j = k; j < T; ++j) s = fmaf(w[j], a.Lf[(int64_t)(j * (j + 1) / 2 + k) * N + p], s);
-      mt[k] = -inv_d * s;
-      cn[k] = fmaf(mt[k], yy, c[k]);
+      const float v = warp_sum_f(w * mrow[k]);
+      if (lane == k) colw = v;
     }
-    mt[T] = inv_d;
-    cn[T] = inv_d * yy;
-    S[T] = atom;
+    const float mt = lane < T ? -inv_d * colw : (lane == T ? inv_d : 0.f);
+    const float cn = lane < T ? fmaf(mt, yy, ck) : (lane == T ? inv_d * yy : 0.f);
+    const int Sn = lane < T ? Sk : (lane == T ? atom : 0);
+    bool act_next = false;
     if (ok) {
       double e = a.e_ws[p] - (double)yy * yy;
       const double xn2 = a.xn2[p];
-      if (e < (double)a.rho * xn2) e = explicit_resnorm2<T>(a, p, S, cn);
+      if (e < (double)a.rho * xn2) {
+        // cancellation: the explicit residual norm, lanes over the row
+        double s2 = 0.0;
+        for (int i = lane; i < a.ld; i += 32) {
+          float r = xr[i];
+#pragma unroll
+          for (int k = 0; k <= T; ++k)
+            r = fmaf(-__shfl_sync(kFull, cn, k), __ldg(a.atoms + (int64_t)__shfl_sync(kFull, Sn, k) * a.ld + i), r);
+          s2 += (double)r * r;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(kFull, s2, o);
+        e = s2;
+      }
       const float rn = (float)sqrt(fmax(e, 0.0));
       act_next = (T + 1 < K) && rn > a.tol[p];
-      a.count[p] = T + 1;
-      a.resnorm[p] = rn;
+      if (lane == 0) {
+        a.count[p] = T + 1;
+        a.resnorm[p] = rn;
+      }
       if (act_next) {
-#pragma unroll
-        for (int k = 0; k <= T; ++k) {
-          a.Lf[(int64_t)(T * (T + 1) / 2 + k) * N + p] = mt[k];
-          a.c_ws[k * N + p] = cn[k];
+        if (lane <= T) {
+          a.Lf[p * KM + T * (T + 1) / 2 + lane] = mt;
+          a.c_ws[p * K + lane] = cn;
         }
-        a.yv[T * N + p] = yy;
-        a.S_ws[T * N + p] = atom;
-        a.e_ws[p] = e;
+        if (lane == 0) {
+          a.yv[p * K + T] = yy;
+          a.S_ws[p * K + T] = atom;
+          a.e_ws[p] = e;
+        }
       }
     }
-#pragma unroll
-    for (int k = 0; k <= T; ++k) c[k] = ok || k == T ? cn[k] : c[k];
+    const float cf = ok ? cn : ck;
     if (!act_next) {
       // final rows of the caller's idx / coef (T or T + 1 entries; the rest stay -1 / 0 from init)
-      const int n_out = ok ? T + 1 : T;
-#pragma unroll
-      for (int k = 0; k <= T; ++k)
-        if (k < n_out) {
-          a.idx[p * K + k] = S[k];
-          a.coef[p * K + k] = c[k];
-        }
+      if (lane < (ok ? T + 1 : T)) {
+        a.idx[p * K + lane] = Sn;
+        a.coef[p * K + lane] = cf;
+      }
     }
-    a.active[p] = act_next ? 1 : 0;
-  }
-  // next iteration's root choice: s_v = (c_v . x) - sum_k c_k P_0[S_k][v],
-  // first max of |s| in child order (pursuit.py:151)
-  int best = -1;
-  if (act_next) {
-    const float* s0 = a.s0 + p * a.root_w;
-    float bestv = -1.f;
-    for (int c0 = 0; c0 < a.root_w; c0 += 32) {
-      float v[32];
-      const int nc = min(32, a.root_w - c0);
+    if (lane == 0) a.active[p] = act_next ? 1 : 0;
+    if (act_next) {
+      // next iteration's root choice: s_j = (c_j . x) - sum_k c_k P_0[S_k][j],
+      // first max of |s| in child order (pursuit.py:151)
+      constexpr int kMaxPer = 8;   // root_w <= 256
+      float sv[kMaxPer], corr[kMaxPer];
+      float* s0 = a.s0 + p * a.root_w;
+      float bestv = -1.f;
+      int best = 0;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = j < nc ? __ldg(s0 + c0 + j) : 0.f;
+      for (int q = 0; q < kMaxPer; ++q) {
+        const int j = lane + 32 * q;
+        corr[q] = 0.f;
+        sv[q] = 0.f;
+        if (32 * q < a.root_w) {
 #pragma unroll
-      for (int k = 0; k <= T; ++k) {
-        const float* row = a.root_tab + (int64_t)S[k] * a.root_w + c0;
+          for (int k = 0; k <= T; ++k) {
+            const float c_k = __shfl_sync(kFull, cn, k);
+            const int s_k = __shfl_sync(kFull, Sn, k);
+            if (j < a.root_w) corr[q] = fmaf(c_k, __ldg(a.root_tab + (int64_t)s_k * a.root_w + j), corr[q]);
+          }
+          if (j < a.root_w) {
+            sv[q] = s0[j] - corr[q];
+            if (fabsf(sv[q]) > bestv) {
+              bestv = fabsf(sv[q]);
+              best = j;
+            }
+          }
+        }
+      }
+      // warp argmax, ties to the lowest child index
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < nc) v[j] = fmaf(-c[k], __ldg(row + j), v[j]);
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(kFull, bestv, o);
+        const int oj = __shfl_xor_sync(kFull, best, o);
+        if (ov > bestv || (ov == bestv && oj < best)) {
+          bestv = ov;
+          best = oj;
+        }
+      }
+      float second = -1.f;
+#pragma unroll
+      for (int q = 0; q < kMaxPer; ++q) {
+        const int j = lane + 32 * q;
+        if (j < a.root_w && j != best) second = fmaxf(second, fabsf(sv[q]));
       }
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < nc && fabsf(v[j]) > bestv) {
-          bestv = fabsf(v[j]);
-          best = c0 + j;
+      for (int o = 16; o; o >>= 1) second = fmaxf(second, __shfl_xor_sync(kFull, second, o));
+      const float delta = a.recheck_rel * (float)sqrt(a.xn2[p]);
+      if (bestv - second < delta) {
+        // near tie: exact c_j . x for every child within 2 delta of the best
+        const float lo = bestv - 2.f * delta;
+        float nbv = -1.f;
+        int nbest = 0;
+#pragma unroll
+        for (int q = 0; q < kMaxPer; ++q) {
+          const int j = lane + 32 * q;
+          unsigned cand = __ballot_sync(kFull, j < a.root_w && fabsf(sv[q]) >= lo);
+          while (cand) {
+            const int l = __ffs(cand) - 1;
+            cand &= cand - 1;
+            const int jj = l + 32 * q;
+            const float raw = warp_dot_rows(xr, a.cent + (int64_t)(a.root_cb + jj) * a.ld, a.ld);
+            const float sj = fabsf(raw - __shfl_sync(kFull, corr[q], l));
+            if (lane == 0) s0[jj] = raw;   // the cache keeps the exact value
+            if (sj > nbv) {
+              nbv = sj;
+              nbest = jj;
+            }
+          }
         }
+        best = nbest;
+      }
+      if (lane == 0) {
+        const int child = a.root_cb + best;
+        a.path_ws[p * a.L] = child;
+        if (a.path_out) a.path_out[(p * K + (T + 1)) * a.L] = child;
+        if (a.ip) add_ip(a.ip, p, a.root_w, a.root_w);
+        atomicAdd(&hist[best], 1);
+      }
     }
-    const int child = a.root_cb + best;
-    a.path_ws[p * a.L] = child;
-    if (a.path_out) a.path_out[(p * K + (T + 1)) * a.L] = child;
-    if (a.ip) add_ip(a.ip, p, a.root_w, a.root_w);
-    atomicAdd(&hist[best], 1);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < a.root_w; i += blockDim.x)
@@ -342,10 +410,10 @@ cudaError_t launch_gram_init(const float* X, int64_t ldx, int n, int64_t N, doub
 }
 
 cudaError_t launch_update_gram(const GramArgs& a, cudaStream_t st) {
-  const unsigned blocks = (unsigned)((a.N + 127) / 128);
+  const unsigned blocks = (unsigned)((a.N + 7) / 8);
   switch (a.iter) {
 #define STMP_GRAM_CASE(t) \
-  case t: return launch_kernel(update_gram_kernel<t>, blocks, 128, 0, st, true, a);
+  case t: return launch_kernel(update_gram_kernel<t>, blocks, 256, 0, st, true, a);
     STMP_GRAM_CASE(0) STMP_GRAM_CASE(1) STMP_GRAM_CASE(2) STMP_GRAM_CASE(3) STMP_GRAM_CASE(4) STMP_GRAM_CASE(5)
     STMP_GRAM_CASE(6) STMP_GRAM_CASE(7) STMP_GRAM_CASE(8) STMP_GRAM_CASE(9) STMP_GRAM_CASE(10) STMP_GRAM_CASE(11)
     STMP_GRAM_CASE(12) STMP_GRAM_CASE(13) STMP_GRAM_CASE(14) STMP_GRAM_CASE(15)

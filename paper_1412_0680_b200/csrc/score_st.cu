@@ -71,7 +71,7 @@ __host__ __device__ inline StLayout st_layout(int npad, bool last, int na, int n
 // level: a . x, the OMP right-hand side); iteration 0's root pass also stores
 // every raw score (raw_out) for the later root choices.  p < 0: no patch row.
 __device__ __forceinline__ void corr_abs_argmax(uint32_t taddr, int cc, const ScoreArgs& a, int p, int colbase,
-                                                float& bestv, int& best, float& rawbest) {
+                                                float& bestv, int& best, float& rawbest, float& second) {
   const int T = p >= 0 && a.corr ? a.sup_t : 0;
   const bool vec = ((colbase | (int)a.corr_w) & 3) == 0;
   for (int c0 = 0; c0 < cc; c0 += 32) {
@@ -89,8 +89,8 @@ __device__ __forceinline__ void corr_abs_argmax(uint32_t taddr, int cc, const Sc
         if (j < nc && c0 + j < a.raw_w) dst[j] = v[j];
     }
     for (int k = 0; k < T; ++k) {
-      const int sk = __ldg(a.sup + (int64_t)k * a.nsup + p);
-      const float ck = __ldg(a.supc + (int64_t)k * a.nsup + p);
+      const int sk = __ldg(a.sup + (int64_t)p * a.sup_ld + k);
+      const float ck = __ldg(a.supc + (int64_t)p * a.sup_ld + k);
       const float* row = a.corr + (int64_t)sk * a.corr_w + colbase + c0;
       if (vec && nc == 32) {
 #pragma unroll
@@ -109,11 +109,91 @@ __device__ __forceinline__ void corr_abs_argmax(uint32_t taddr, int cc, const Sc
     }
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      if (j < nc && fabsf(v[j]) > bestv) {
-        bestv = fabsf(v[j]);
-        best = c0 + j;
-        rawbest = raw[j];
+      if (j < nc) {
+        const float m = fabsf(v[j]);
+        if (m > bestv) {
+          second = bestv;
+          bestv = m;
+          best = c0 + j;
+          rawbest = raw[j];
+        } else {
+          second = fmaxf(second, m);
+        }
       }
+  }
+}
+
+// Exact FFMA dot of patch row x (ld floats, the padding is zero) with centroid row c, by one warp.
+__device__ __forceinline__ float warp_dot(const float* __restrict__ x, const float* __restrict__ c, int ld) {
+  float s = 0.f;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const float4* c4 = reinterpret_cast<const float4*>(c);
+  for (int i = (int)(threadIdx.x & 31); i < ld / 4; i += 32) {
+    const float4 u = __ldg(x4 + i), v = __ldg(c4 + i);
+    s = fmaf(u.x, v.x, s);
+    s = fmaf(u.y, v.y, s);
+    s = fmaf(u.z, v.z, s);
+    s = fmaf(u.w, v.w, s);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  return s;
+}
+
+// Gram-path near-tie re-check, warp-cooperative (all 32 lanes of a stager warp
+// call it).  The tensor cores' fp32 accumulation truncates, leaving ~1e-6 ||x||
+// of error on c . x; a row whose two best corrected scores are closer than
+// delta = recheck_rel * ||x|| is re-scored exactly (FFMA dots) for every child
+// whose approximate score lies within 2 delta of the best -- the others cannot
+// win -- and the first maximum in child order is kept (pursuit.py:151).
+__device__ void recheck_near_ties(uint32_t taddr, int cc, int cb, const ScoreArgs& a, int p, float second,
+                                  float& bestv, int& best, float& rawbest) {
+  const int lane = (int)(threadIdx.x & 31);
+  const float delta = p >= 0 ? a.recheck_rel * (float)sqrt(a.xn2[p]) : 0.f;
+  unsigned todo = __ballot_sync(kFull, p >= 0 && bestv - second < delta);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int q = __shfl_sync(kFull, p, src);
+    const float lo = __shfl_sync(kFull, bestv, src) - 2.f * __shfl_sync(kFull, delta, src);
+    const float* xrow = a.R + (int64_t)q * a.ld;
+    float nbv = -1.f, nraw = 0.f;
+    int nbest = 0;
+    for (int c0 = 0; c0 < cc; c0 += 32) {
+      float v[32];
+      tmem_ld32(taddr + (uint32_t)c0, v);
+      float mine = 0.f;   // row q's raw score of child c0 + lane
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float t = __shfl_sync(kFull, v[j], src);
+        if (j == lane) mine = t;
+      }
+      const int col = c0 + lane;
+      float corr = 0.f;
+      if (col < cc)
+        for (int k = 0; k < a.sup_t; ++k) {
+          const int sk = __ldg(a.sup + (int64_t)q * a.sup_ld + k);
+          corr = fmaf(__ldg(a.supc + (int64_t)q * a.sup_ld + k),
+                      __ldg(a.corr + (int64_t)sk * a.corr_w + (cb - a.corr_off) + col), corr);
+        }
+      unsigned cand = __ballot_sync(kFull, col < cc && fabsf(mine - corr) >= lo);
+      while (cand) {
+        const int j = __ffs(cand) - 1;
+        cand &= cand - 1;
+        const float raw = warp_dot(xrow, a.cent + (int64_t)(cb + c0 + j) * a.ld, a.ld);
+        const float sj = fabsf(raw - __shfl_sync(kFull, corr, j));
+        if (sj > nbv) {   // columns visited in increasing order: strict > keeps the first max
+          nbv = sj;
+          nbest = c0 + j;
+          nraw = raw;
+        }
+      }
+    }
+    if (lane == src) {
+      bestv = nbv;
+      best = nbest;
+      rawbest = nraw;
+    }
   }
 }
 
@@ -301,8 +381,12 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       const int p = cur_p;
       if (a.corr != nullptr || a.raw_out != nullptr) {
         // Gram path: rows are x; score = c . x - sum_k c_k P[S_k][child] (gram_path.cu)
+        float second = -1.f;
         corr_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * accw, cc, a, valid ? p : -1,
-                        cb - a.corr_off, bestv, best, rawbest);
+                        cb - a.corr_off, bestv, best, rawbest, second);
+        if (a.cent != nullptr)
+          recheck_near_ties(tmem + lane_base + kColAcc + (uint32_t)acc * accw, cc, cb, a, valid ? p : -1, second,
+                            bestv, best, rawbest);
       } else {
         tmem_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * accw, (int)accw, npad, bestv, best);
       }

@@ -41,13 +41,19 @@ struct ScoreArgs {
   const float* corr;     // pair table of this level: [m][corr_w], row = atom, column = child node
   int64_t corr_w;        // columns per row (nodes at depth level + 1)
   int corr_off;          // global id of the first depth-(level + 1) node (column 0)
-  const int* sup;        // support atoms [K][N] (S_ws), the first `sup_t` entries valid
-  const float* supc;     // current coefficients [K][N] (c_ws)
+  const int* sup;        // support atoms [N][sup_ld] (S_ws), the first `sup_t` entries valid
+  const float* supc;     // current coefficients [N][sup_ld] (c_ws)
   int sup_t;             // support size of every active patch (the iteration index)
-  int64_t nsup;          // N: stride of sup / supc
+  int64_t sup_ld;        // K
   float* raw_out;        // root pass of iteration 0: raw scores c . x of all children -> [N][raw_w]
   int raw_w;
   float* bsel;           // last level: raw score a . x of the winning leaf atom -> [N]
+  // exact re-check of near ties: the tensor cores' truncating fp32 accumulation
+  // leaves ~1e-6 ||x|| of error on c . x, so decisions whose top-2 corrected
+  // scores are closer than recheck_rel * ||x|| are re-scored with FFMA dots
+  const float* cent;     // centroid rows [nodes][ld] (global ids)
+  const double* xn2;     // ||x||^2 per patch
+  float recheck_rel;
 };
 
 // Work items of a score pass: (bin, first slot in perm, rows) from the scan, or
@@ -118,7 +124,7 @@ struct GramArgs {
   int64_t gram_w;
   const int* leaf_pos;     // [m] column of each atom in the last-level table
   const float* root_tab;   // pair table of level 0 [m][root_w]
-  const float* s0;         // cached root scores c . x [N][root_w]
+  float* s0;               // cached root scores c . x [N][root_w] (near-tie re-checks write exact values back)
   int root_w, root_cb;     // root children: count, first global id
   int* root_counts;        // level-1 bin counters of the next iteration
   int* path_ws;
@@ -136,13 +142,14 @@ struct GramArgs {
   int32_t* count;
   float* resnorm;
   int32_t* ip;
-  // explicit residual norm for patches whose ||r||^2 estimate falls below
-  // rho ||x||^2 (cancellation): x and the support rows
-  const float* X;
-  int64_t ldx;
+  // exact dots (b = a . x, root near ties) and the explicit residual norm for
+  // patches whose ||r||^2 estimate falls below rho ||x||^2 (cancellation)
+  const float* xr;         // patch rows x, zero-padded [N][ld]
   const float* atoms;
-  int ld, n;
+  const float* cent;       // centroid rows [nodes][ld] (root children: root_cb ..)
+  int ld;
   float rho;
+  float recheck_rel;       // near-tie window: recheck_rel * ||x||
 };
 bool gram_path_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
 // builds the pair tables on first use; false if they cannot be allocated

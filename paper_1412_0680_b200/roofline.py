@@ -75,9 +75,10 @@ def model(cfg, N: int | None = None, method: str = "omp", exhaustive: bool = Fal
 # Kernel families of one staged encode, by (mangled) kernel name.
 FAMILIES = (("score", ("score_ts_kernel", "score_st_kernel")),
             ("exact_scan", ("exact_scan_kernel",)),
-            ("update", ("update_omp8_kernel", "update_wide_kernel", "update_kernel")),
+            ("update", ("update_omp8_kernel", "update_wide_kernel", "update_gram_kernel", "gram_bdot_kernel",
+                        "update_kernel")),
             ("scatter", ("scatter_scan_kernel", "scatter_kernel", "scatter_root_kernel", "scan_kernel")),
-            ("init", ("init_kernel",)))
+            ("init", ("init_kernel", "gram_init_kernel")))
 
 
 def family_of(name: str) -> str:
