@@ -66,6 +66,8 @@ def parse():
                     help="programmatic dependent launch between the staged kernels")
     ap.add_argument("--path", type=int, default=0, choices=[0, 1, 2],
                     help="encoder: 0 auto, 1 fused warp-per-patch, 2 staged tensor-core pipeline")
+    ap.add_argument("--gram", type=int, default=1, choices=[0, 1, 2],
+                    help="Gram path (tree OMP without a residual): 0 off, 1 auto, 2 whenever supported")
     ap.add_argument("--graphs", type=int, default=1, choices=[0, 1],
                     help="replay repeated staged encodes as CUDA graphs")
     return ap.parse_args()
@@ -279,6 +281,7 @@ def main():
     _lib.set_option("pdl", args.pdl)
     _lib.set_option("graphs", args.graphs)
     _lib.set_option("path", args.path)
+    _lib.set_option("gram_path", args.gram)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:

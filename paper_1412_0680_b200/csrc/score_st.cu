@@ -9,9 +9,12 @@
 //     chunk c of its 32 rows (cp.async, four whole 128-byte lines per
 //     instruction) into a ring of NA swizzled landing slots, NA chunks ahead --
 //     a warp only reads the rows it copied, so the landing ring needs no CTA
-//     barrier -- then each thread splits its row into tf32 hi / lo and stores both into one of
-//     two TMEM A buffers (tcgen05.st); after a tile's last chunk they read the
-//     accumulator back and reduce it to the argmax child (the epilogue);
+//     barrier -- then each thread splits its row into tf32 hi / lo and stores
+//     both into one of NAB TMEM A buffers (tcgen05.st);
+//   * warps 6-9, epilogue (TMEM lane quarter = warp % 4): after a tile's last
+//     chunk they read the accumulator back and reduce it to the argmax child
+//     (Gram path: with the support correction and the near-tie re-check) while
+//     the stagers already stage the next tile;
 //   * warp 4, MMA issuer: per chunk, 3xTF32 tcgen05.mma (M = 128 patches,
 //     N = npad <= 256 children, A from TMEM, B = the table chunk in shared
 //     memory), commits that free the table slot and the A buffer, and at a
@@ -37,10 +40,11 @@ namespace {
 
 constexpr int kT = 128;
 constexpr int kStagers = 128;
-constexpr int kThreads = kStagers + 64;   // + MMA warp + producer warp
+constexpr int kEpi = 128;                 // epilogue warps 6-9 (TMEM lane quarter = warp % 4)
+constexpr int kThreads = kStagers + 64 + kEpi;   // stagers, MMA warp, producer warp, epilogue
 constexpr uint32_t kSlot = kT * 128u;     // one landing slot: 128 rows x 32 floats
-constexpr int kNAB = 4;                   // TMEM A buffers (64 columns each: hi | lo of one K chunk)
-constexpr uint32_t kColAcc = 64u * kNAB;  // TMEM: A buffers at [0, 256), accumulators from 256
+// NAB TMEM A buffers (64 columns each: hi | lo of one K chunk) at [0, 64 NAB),
+// accumulators from 64 NAB
 
 struct StLayout {
   uint32_t land, btab, hist, bars, slot, total;
@@ -50,14 +54,14 @@ __host__ __device__ inline uint32_t st_align(uint32_t v, uint32_t a) { return (v
 
 __host__ __device__ inline uint32_t st_bslot(int npad) { return st_align((uint32_t)npad * 256u, 1024u); }
 
-__host__ __device__ inline StLayout st_layout(int npad, bool last, int na, int nb) {
+__host__ __device__ inline StLayout st_layout(int npad, bool last, int na, int nb, int nab) {
   StLayout L{};
   uint32_t o = 0;
   L.land = o; o += (uint32_t)na * kSlot;
   L.btab = o; o += (uint32_t)nb * st_bslot(npad);
   o = st_align(o, 16);
   L.hist = o; o += 256 * 4;
-  L.bars = st_align(o, 8); o = L.bars + (uint32_t)(2 * nb + 2 * kNAB + 4) * 8;
+  L.bars = st_align(o, 8); o = L.bars + (uint32_t)(2 * nb + 2 * nab + 4) * 8;
   L.slot = o; o += 16;
   L.total = o + 1024;
   return L;
@@ -197,8 +201,10 @@ __device__ void recheck_near_ties(uint32_t taddr, int cc, int cb, const ScoreArg
   }
 }
 
-template <int NA, int NB>
+template <int NA, int NB, int NAB>
 __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int nacc) {
+  constexpr int kNAB = NAB;
+  constexpr uint32_t kColAcc = 64u * NAB;
   pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
   const int npad = a.npad;
   const int kch = a.kchunks;
   const bool last = a.leaf_sel != nullptr;
-  const StLayout Ly = st_layout(npad, last, NA, NB);
+  const StLayout Ly = st_layout(npad, last, NA, NB, NAB);
   const uint32_t bslot = st_bslot(npad);
   int* s_hist = reinterpret_cast<int*>(base + Ly.hist);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + Ly.bars);   // [NB] table chunk landed (tx)
@@ -217,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
   uint64_t* astaged = done + NB;       // [kNAB] A buffer written by the 128 stagers
   uint64_t* aempty = astaged + kNAB;   // [kNAB] MMAs reading the A buffer retired (commit)
   uint64_t* accfull = aempty + kNAB;   // [2] accumulator complete (commit)
-  uint64_t* accempty = accfull + 2;    // [2] accumulator read back by the 128 stagers
+  uint64_t* accempty = accfull + 2;    // [2] accumulator read back by the 128 epilogue threads
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + Ly.slot);
 
   if (warp == 0) tmem_alloc(tmem_slot, a.tmem_cols);
@@ -232,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accfull[b], 1);
-      mbar_init(&accempty[b], kStagers);
+      mbar_init(&accempty[b], kEpi);
     }
     fence_mbar_init();
   }
@@ -288,17 +294,22 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
           const uint32_t al = ah + 32;
           const uint32_t o = ks * 32u;
           if (c == kch - 1 && ks >= a.ks_last) break;   // zero padding on both operands
-          mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bh + o), idesc, (c | ks) ? 1u : 0u);
-          mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bl + o), idesc, 1u);
-          mma_tf32_ts(dcol, al, sw128_kmajor_desc(bh + o), idesc, 1u);
+#ifndef STMP_ST_MMAS   // timing experiments only: 0 = no MMAs, 1 = hi.hi only, 3 = 3xTF32 (default)
+#define STMP_ST_MMAS 3
+#endif
+          if (STMP_ST_MMAS >= 1) mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bh + o), idesc, (c | ks) ? 1u : 0u);
+          if (STMP_ST_MMAS >= 3) {
+            mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bl + o), idesc, 1u);
+            mma_tf32_ts(dcol, al, sw128_kmajor_desc(bh + o), idesc, 1u);
+          }
         }
         mma_commit(&done[s]);
         mma_commit(&aempty[ab]);
         if (c == kch - 1) mma_commit(&accfull[acc]);
       }
     }
-  } else {
-    // ------------------------------------------------ stagers + epilogue (warps 0-3)
+  } else if (warp < 4) {
+    // ------------------------------------------------ stagers (warps 0-3)
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     const uint32_t land_s = smem_u32(base + Ly.land);
     // row ids of this warp's 32 rows for the item being gathered (lane l: row 32w + l)
@@ -331,16 +342,8 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
     for (int g = 0; g < NA; ++g) issue_a(g);
-    int cur_p = -1, cur_rows = 0, cur_bin = 0;
     for (int g = 0; g < total; ++g) {
-      const int seq = g / kch, c = g - seq * kch;
       const int ab = g % kNAB;
-      if (c == 0) {
-        const int4 it = item_at(a, i0 + seq);
-        cur_bin = it.x;
-        cur_rows = it.z;
-        cur_p = tid < it.z ? row_at(a, it, tid) : -1;
-      }
       asm volatile("cp.async.wait_group %0;" ::"n"(NA - 1) : "memory");
       __syncwarp();   // the warp's rows were copied by all of its lanes
       float hi[32], lo[32];
@@ -366,9 +369,18 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&astaged[ab]);
-      if (c != kch - 1) continue;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  } else {
+    // ------------------------------------------------ epilogue (warps 6-9): TMEM lane quarter warp % 4
+    const int et = (warp & 3) * 32 + lane;          // tile row = TMEM lane
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    for (int seq = 0; seq < i1 - i0; ++seq) {
+      const int4 it = item_at(a, i0 + seq);
+      const int cur_bin = it.x, cur_rows = it.z;
+      const int cur_p = et < it.z ? row_at(a, it, et) : -1;
+      const int tid = et;
 
-      // ---- tile epilogue
       const int acc = nacc == 2 ? (seq & 1) : 0;
       mbar_wait(&accfull[acc], (uint32_t)(seq / nacc) & 1u);
       tc_fence_after();
@@ -409,16 +421,15 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
         if (a.ip) add_ip(a.ip, p, cc + leaf_cnt, cc);
       }
       if (a.next_counts) {
-        named_sync(1, kStagers);
-        for (int j = tid; j < cc; j += kStagers) {
+        named_sync(1, kEpi);
+        for (int j = tid; j < cc; j += kEpi) {
           const int h = s_hist[j];
           if (h) atomicAdd(&a.next_counts[cb + j - a.next_base], h);
           s_hist[j] = 0;
         }
-        named_sync(1, kStagers);
+        named_sync(1, kEpi);
       }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
   }
   __syncwarp();   // reconverge the single-lane roles before the CTA barrier
   tc_fence_before();
@@ -428,27 +439,35 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
 }
 
 struct StCfg {
-  int na, nb;
+  int na, nb, nab;
 };
 
 // ring depths: wide nodes (c2: 64 KB table chunks) get three table slots and a
 // two-deep landing ring (the table refill latency is the one to hide); narrow
 // ones (c4: 8-16 KB) a deep ring on both sides
-inline StCfg st_cfg(int npad) { return npad > 128 ? StCfg{2, 3} : (npad > 64 ? StCfg{4, 4} : StCfg{6, 6}); }
+#ifndef STMP_ST_NAB_NARROW
+#define STMP_ST_NAB_NARROW 6
+#endif
+// four A buffers leave room for a double-buffered accumulator up to npad 128;
+// narrow nodes (c4: 32-64 children) get NAB A buffers, as many as TMEM holds
+inline StCfg st_cfg(int npad) {
+  return npad > 128 ? StCfg{2, 3, 4} : (npad > 64 ? StCfg{4, 4, 4} : StCfg{6, 6, STMP_ST_NAB_NARROW});
+}
 
-template <int NA, int NB>
+template <int NA, int NB, int NAB>
 cudaError_t launch_st(ScoreArgs s, int sms, cudaStream_t st) {
+  constexpr uint32_t kColAcc = 64u * NAB;
   const bool last = s.leaf_sel != nullptr;
-  const uint32_t smem = st_layout(s.npad, last, NA, NB).total;
+  const uint32_t smem = st_layout(s.npad, last, NA, NB, NAB).total;
   const int accw = (s.npad + 31) / 32 * 32;
   const int nacc = (int)kColAcc + 2 * accw <= 512 ? 2 : 1;
   int cols = 32;
   while (cols < (int)kColAcc + nacc * accw) cols <<= 1;
   s.tmem_cols = cols;
-  cudaError_t e = cudaFuncSetAttribute(score_st_kernel<NA, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(score_st_kernel<NA, NB, NAB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_kernel(score_st_kernel<NA, NB>, sms, kThreads, (size_t)smem, st, true, s, nacc);
+  return launch_kernel(score_st_kernel<NA, NB, NAB>, sms, kThreads, (size_t)smem, st, true, s, nacc);
 }
 
 }  // namespace
@@ -456,15 +475,15 @@ cudaError_t launch_st(ScoreArgs s, int sms, cudaStream_t st) {
 bool score_st_fits(int kchunks, int npad, bool last) {
   if (kchunks < 1 || npad < 16 || npad > 256) return false;
   const StCfg c = st_cfg(npad);
-  return st_layout(npad, last, c.na, c.nb).total <= 227 * 1024;
+  return st_layout(npad, last, c.na, c.nb, c.nab).total <= 227 * 1024;
 }
 
 cudaError_t launch_score_st(const ScoreArgs& s, int sms, cudaStream_t st) {
   if (!score_st_fits(s.kchunks, s.npad, s.leaf_sel != nullptr)) return cudaErrorNotSupported;
   const StCfg c = st_cfg(s.npad);
-  if (c.nb == 3) return launch_st<2, 3>(s, sms, st);
-  if (c.nb == 4) return launch_st<4, 4>(s, sms, st);
-  return launch_st<6, 6>(s, sms, st);
+  if (c.nb == 3) return launch_st<2, 3, 4>(s, sms, st);
+  if (c.nb == 4) return launch_st<4, 4, 4>(s, sms, st);
+  return launch_st<6, 6, STMP_ST_NAB_NARROW>(s, sms, st);
 }
 
 }  // namespace stmp
