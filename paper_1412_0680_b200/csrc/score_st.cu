@@ -67,6 +67,57 @@ __host__ __device__ inline StLayout st_layout(int npad, bool last, int na, int n
   return L;
 }
 
+// Accumulator read-back: with two MMA chains (hi.hi in one accumulator, the
+// small hi.lo + lo.hi in a second one `off2` columns further) the two are summed.
+__device__ __forceinline__ void acc_ld32(uint32_t taddr, uint32_t off2, float (&v)[32]) {
+  tmem_ld32(taddr, v);
+  if (off2) {
+    float w[32];
+    tmem_ld32(taddr + off2, w);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] += w[j];
+  }
+}
+
+// first max of |score| over the node's children (ties to the lowest child
+// position, pursuit.py:151), two passes as tmem_abs_argmax (sm100.cuh)
+__device__ __forceinline__ void acc_abs_argmax(uint32_t taddr, uint32_t off2, int ncols, int nvalid, float& bestv,
+                                               int& best) {
+  float m = -1.f;
+  int bc = 0;
+  for (int c0 = 0; c0 < ncols; c0 += 32) {
+    float v[32];
+    acc_ld32(taddr + (uint32_t)c0, off2, v);
+    if (c0 + 32 > nvalid) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = c0 + j < nvalid ? v[j] : 0.f;
+    }
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+      for (int j = 0; j < w; ++j) v[j] = fmaxf(fabsf(v[j]), fabsf(v[j + w]));
+    const float t = fabsf(v[0]);
+    if (t > m) {
+      m = t;
+      bc = c0;
+    }
+  }
+  // the TMEM address of tcgen05.ld must be warp-uniform: every lane walks every
+  // chunk and resolves the column inside its own winning chunk
+  int idx = 0;
+  for (int c0 = 0; c0 < ncols; c0 += 32) {
+    float v[32];
+    acc_ld32(taddr + (uint32_t)c0, off2, v);
+    if (c0 == bc) {
+      idx = 31;
+#pragma unroll
+      for (int j = 31; j >= 0; --j) idx = (c0 + j < nvalid && fabsf(v[j]) == m) ? j : idx;
+    }
+  }
+  bestv = m;
+  best = bc + idx;
+}
+
 // Epilogue of the Gram path (gram_path.cu): the accumulator holds c_v . x for
 // the node's cc children; subtract the support's contribution
 // sum_k c_k P[S_k][colbase + v] (the patch's current OMP support and
@@ -74,13 +125,14 @@ __host__ __device__ inline StLayout st_layout(int npad, bool last, int na, int n
 // (pursuit.py:151).  `rawbest` is the winner's uncorrected c . x (for the last
 // level: a . x, the OMP right-hand side); iteration 0's root pass also stores
 // every raw score (raw_out) for the later root choices.  p < 0: no patch row.
-__device__ __forceinline__ void corr_abs_argmax(uint32_t taddr, int cc, const ScoreArgs& a, int p, int colbase,
-                                                float& bestv, int& best, float& rawbest, float& second) {
+__device__ __forceinline__ void corr_abs_argmax(uint32_t taddr, uint32_t off2, int cc, const ScoreArgs& a, int p,
+                                                int colbase, float& bestv, int& best, float& rawbest,
+                                                float& second) {
   const int T = p >= 0 && a.corr ? a.sup_t : 0;
   const bool vec = ((colbase | (int)a.corr_w) & 3) == 0;
   for (int c0 = 0; c0 < cc; c0 += 32) {
     float v[32];
-    tmem_ld32(taddr + (uint32_t)c0, v);   // every lane of the warp takes part
+    acc_ld32(taddr + (uint32_t)c0, off2, v);   // every lane of the warp takes part
     if (p < 0) continue;
     const int nc = min(32, cc - c0);
     float raw[32];
@@ -150,8 +202,8 @@ __device__ __forceinline__ float warp_dot(const float* __restrict__ x, const flo
 // delta = recheck_rel * ||x|| is re-scored exactly (FFMA dots) for every child
 // whose approximate score lies within 2 delta of the best -- the others cannot
 // win -- and the first maximum in child order is kept (pursuit.py:151).
-__device__ void recheck_near_ties(uint32_t taddr, int cc, int cb, const ScoreArgs& a, int p, float second,
-                                  float& bestv, int& best, float& rawbest) {
+__device__ void recheck_near_ties(uint32_t taddr, uint32_t off2, int cc, int cb, const ScoreArgs& a, int p,
+                                  float second, float& bestv, int& best, float& rawbest) {
   const int lane = (int)(threadIdx.x & 31);
   const float delta = p >= 0 ? a.recheck_rel * (float)sqrt(a.xn2[p]) : 0.f;
   unsigned todo = __ballot_sync(kFull, p >= 0 && bestv - second < delta);
@@ -165,7 +217,7 @@ __device__ void recheck_near_ties(uint32_t taddr, int cc, int cb, const ScoreArg
     int nbest = 0;
     for (int c0 = 0; c0 < cc; c0 += 32) {
       float v[32];
-      tmem_ld32(taddr + (uint32_t)c0, v);
+      acc_ld32(taddr + (uint32_t)c0, off2, v);
       float mine = 0.f;   // row q's raw score of child c0 + lane
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -202,7 +254,7 @@ __device__ void recheck_near_ties(uint32_t taddr, int cc, int cb, const ScoreArg
 }
 
 template <int NA, int NB, int NAB>
-__global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int nacc) {
+__global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int nacc, int chains) {
   constexpr int kNAB = NAB;
   constexpr uint32_t kColAcc = 64u * NAB;
   pdl_enter();
@@ -256,6 +308,13 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
   const uint32_t tb = table_bytes(kch, npad, last);
   const uint32_t chunk_bytes = (uint32_t)npad * 256u;
   const uint32_t accw = (uint32_t)(npad + 31) / 32 * 32;
+  // wide-N mode (chains == 2, npad % 32 == 0): an accumulator buffer holds
+  // [hi.hi | hi.lo + lo.hi]; one MMA with N = 2 npad multiplies x_hi by the
+  // table's hi and lo planes at once (they are adjacent row blocks of the chunk),
+  // a second adds x_lo . b_hi into the upper half -- two tensor instructions per
+  // k-step instead of three; the epilogue sums the halves
+  const uint32_t off2 = chains == 2 ? accw : 0u;
+  const uint32_t accs = accw * (uint32_t)chains;   // stride of the accumulator buffers
 
   if (warp == 5) {
     // ------------------------------------------------ table producer
@@ -276,12 +335,14 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = idesc_tf32(kT, npad);
+      const uint32_t idesc2 = idesc_tf32(kT, 2 * npad);
       const uint32_t b_s = smem_u32(base + Ly.btab);
       for (int g = 0; g < total; ++g) {
         const int seq = g / kch, c = g - seq * kch;
         const int ab = g % kNAB, s = g % NB;
         const int acc = nacc == 2 ? (seq & 1) : 0;
-        const uint32_t dcol = tmem + kColAcc + (uint32_t)acc * accw;
+        const uint32_t dcol = tmem + kColAcc + (uint32_t)acc * accs;
+        const uint32_t dlo = dcol + off2;
         if (c == 0 && seq >= nacc) mbar_wait(&accempty[acc], (uint32_t)(seq / nacc - 1) & 1u);
         mbar_wait(&astaged[ab], (uint32_t)(g / kNAB) & 1u);
         mbar_wait(&full[s], (uint32_t)(g / NB) & 1u);
@@ -297,10 +358,15 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
 #ifndef STMP_ST_MMAS   // timing experiments only: 0 = no MMAs, 1 = hi.hi only, 3 = 3xTF32 (default)
 #define STMP_ST_MMAS 3
 #endif
-          if (STMP_ST_MMAS >= 1) mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bh + o), idesc, (c | ks) ? 1u : 0u);
-          if (STMP_ST_MMAS >= 3) {
-            mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bl + o), idesc, 1u);
-            mma_tf32_ts(dcol, al, sw128_kmajor_desc(bh + o), idesc, 1u);
+          if (off2) {
+            mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bh + o), idesc2, (c | ks) ? 1u : 0u);   // [hi.hi | hi.lo]
+            if (STMP_ST_MMAS >= 3) mma_tf32_ts(dlo, al, sw128_kmajor_desc(bh + o), idesc, 1u);   // += lo.hi
+          } else {
+            if (STMP_ST_MMAS >= 1) mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bh + o), idesc, (c | ks) ? 1u : 0u);
+            if (STMP_ST_MMAS >= 3) {
+              mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bl + o), idesc, 1u);
+              mma_tf32_ts(dcol, al, sw128_kmajor_desc(bh + o), idesc, 1u);
+            }
           }
         }
         mma_commit(&done[s]);
@@ -394,13 +460,13 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
       if (a.corr != nullptr || a.raw_out != nullptr) {
         // Gram path: rows are x; score = c . x - sum_k c_k P[S_k][child] (gram_path.cu)
         float second = -1.f;
-        corr_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * accw, cc, a, valid ? p : -1,
+        corr_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * accs, off2, cc, a, valid ? p : -1,
                         cb - a.corr_off, bestv, best, rawbest, second);
         if (a.cent != nullptr)
-          recheck_near_ties(tmem + lane_base + kColAcc + (uint32_t)acc * accw, cc, cb, a, valid ? p : -1, second,
-                            bestv, best, rawbest);
+          recheck_near_ties(tmem + lane_base + kColAcc + (uint32_t)acc * accs, off2, cc, cb, a, valid ? p : -1,
+                            second, bestv, best, rawbest);
       } else {
-        tmem_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * accw, (int)accw, npad, bestv, best);
+        acc_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * accs, off2, (int)accw, npad, bestv, best);
       }
       tc_fence_before();
       mbar_arrive(&accempty[acc]);
@@ -446,7 +512,7 @@ struct StCfg {
 // two-deep landing ring (the table refill latency is the one to hide); narrow
 // ones (c4: 8-16 KB) a deep ring on both sides
 #ifndef STMP_ST_NAB_NARROW
-#define STMP_ST_NAB_NARROW 6
+#define STMP_ST_NAB_NARROW 4
 #endif
 // four A buffers leave room for a double-buffered accumulator up to npad 128;
 // narrow nodes (c4: 32-64 children) get NAB A buffers, as many as TMEM holds
@@ -460,14 +526,19 @@ cudaError_t launch_st(ScoreArgs s, int sms, cudaStream_t st) {
   const bool last = s.leaf_sel != nullptr;
   const uint32_t smem = st_layout(s.npad, last, NA, NB, NAB).total;
   const int accw = (s.npad + 31) / 32 * 32;
-  const int nacc = (int)kColAcc + 2 * accw <= 512 ? 2 : 1;
+#ifndef STMP_ST_CHAINS
+#define STMP_ST_CHAINS 2
+#endif
+  // wide-N MMAs (two accumulator halves) and two accumulator buffers when TMEM holds them
+  const int chains = (int)kColAcc + 2 * 2 * accw <= 512 && s.npad % 32 == 0 ? STMP_ST_CHAINS : 1;
+  const int nacc = (int)kColAcc + 2 * chains * accw <= 512 ? 2 : 1;
   int cols = 32;
-  while (cols < (int)kColAcc + nacc * accw) cols <<= 1;
+  while (cols < (int)kColAcc + nacc * chains * accw) cols <<= 1;
   s.tmem_cols = cols;
   cudaError_t e = cudaFuncSetAttribute(score_st_kernel<NA, NB, NAB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_kernel(score_st_kernel<NA, NB, NAB>, sms, kThreads, (size_t)smem, st, true, s, nacc);
+  return launch_kernel(score_st_kernel<NA, NB, NAB>, sms, kThreads, (size_t)smem, st, true, s, nacc, chains);
 }
 
 }  // namespace
