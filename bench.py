@@ -403,7 +403,10 @@ def main():
         f["kernels"].append(demangle(name))
     timed_ms = sum(f["ms"] for f in fams.values()) or 1.0
     dom = max(fams, key=lambda f: fams[f]["ms"]) if fams else "other"
-    work = RL.family_work(cfg, dom, N, args.method, exhaustive)
+    gram = any("update_gram_kernel" in k for k in ktimes)
+    work = RL.gram_family_work(cfg, dom, N) if gram else RL.family_work(cfg, dom, N, args.method, exhaustive)
+    if gram:   # the step model of the path that ran (Gram path: no residual traffic)
+        rm = RL.gram_model(cfg, N, hbm_gbs=hbm)
     dom_ms = fams[dom]["ms"] if fams else launch_ms
     dom_launches = fams[dom]["launches"] if fams else 1
     avg_s = dom_ms / dom_launches / 1e3
@@ -424,12 +427,14 @@ def main():
         "share_of_step": dom_ms / timed_ms,
         "peak_source": ("MEASURED_PEAKS.json" if peaks else "B200_PROFILING.md fallback") +
                        (f"; TF32 {tf32:.0f} TFLOP/s measured live (cuBLAS 8192^3)" if tf32 else ""),
-        "model": "SURVEY §8d algorithmic bytes/FLOPs of the dominant kernel family (roofline.family_work) per "
-                 "launch / its mean launch time (CUDA events on the encode stream, one instrumented encode)",
+        "model": ("algorithmic bytes/FLOPs of the dominant kernel family (roofline." +
+                  ("gram_family_work, Gram path" if gram else "family_work, SURVEY §8d") +
+                  ") per launch / its mean launch time (CUDA events on the encode stream, one instrumented encode)"),
         "families": {f: {"launches": v["launches"], "ms": round(v["ms"], 4), "share": round(v["ms"] / timed_ms, 4)}
                      for f, v in sorted(fams.items(), key=lambda kv: -kv[1]["ms"])},
         # the whole staged step against the §8d per-patch model (the pipeline as one unit)
-        "step": {"bound": rm["bound"], "bytes_per_patch": rm["bytes_per_patch"],
+        "step": {"path": "gram (no residual; pair tables)" if gram else "residual (SURVEY §8d staged design)",
+                 "bound": rm["bound"], "bytes_per_patch": rm["bytes_per_patch"],
                  "flops_per_patch": rm["flops_per_patch"], "launch_ms": launch_ms,
                  "launches": per_step, "model_patches_per_s": rm["patches_per_s_roof"],
                  "frac": rm["patches_per_s_roof"] and (N / (launch_ms / 1e3)) / rm["patches_per_s_roof"]},

@@ -525,6 +525,11 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   {
     UpdateArgs ui = u;
     if (direct) { ui.R = nullptr; ui.X2 = nullptr; }
+    if (gram) {   // ||x||^2 for the Gram path's residual norms; no OMP rebuild copy
+      ui.xn2 = (double*)(b + w.xn2);
+      ui.e_ws = (double*)(b + w.e_ws);
+      ui.X2 = nullptr;
+    }
     if ((e = launch_init(uc, ui, ublocks, st)) != cudaSuccess) return e;
   }
   if (direct && method == kMethodOMP) u.X2 = X;
@@ -546,7 +551,6 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
     double* e_ws = (double*)(b + w.e_ws);
     float* s0 = (float*)(b + w.s0);
     float* bsel = (float*)(b + w.bsel);
-    if ((e = launch_gram_init(X, ldx, d->n, N, xn2, e_ws, st)) != cudaSuccess) return e;
     GramArgs ga{};
     ga.N = N; ga.K = K; ga.L = L; ga.leaf_sel = leaf_sel; ga.bsel = bsel;
     ga.gram = t->pair_tables[L - 1]; ga.gram_w = t->pair_width[L - 1]; ga.leaf_pos = t->leaf_pos;

@@ -102,6 +102,17 @@ __global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
     }
 #pragma unroll
     for (int i = 0; i < CPL * 4; ++i) ss = fmaf(x.v[i], x.v[i], ss);
+    if (a.xn2) {   // Gram path: ||x||^2 in f64 (gram_path.cu)
+      double ds = 0.0;
+#pragma unroll
+      for (int i = 0; i < CPL * 4; ++i) ds += (double)x.v[i] * x.v[i];
+#pragma unroll
+      for (int o = G >> 1; o; o >>= 1) ds += __shfl_xor_sync(group_mask<G>(), ds, o);
+      if (gl == 0) {
+        a.xn2[p] = ds;
+        a.e_ws[p] = ds;
+      }
+    }
     if (a.R) x.store(a.R + p * a.ld, gl, F);
     if (a.X2) x.store(const_cast<float*>(a.X2) + p * a.ld2, gl, F);
   }

@@ -59,26 +59,6 @@ __global__ void leaf_pos_kernel(const int* child_begin, const int* leaf_atom, in
   if (i < nv) pos[leaf_atom[child_begin[v0 + i]]] = (int)i;
 }
 
-__global__ void __launch_bounds__(256) gram_init_kernel(const float* __restrict__ X, int64_t ldx, int n, int64_t N,
-                                                        double* xn2, double* e) {
-  pdl_enter();
-  const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (p >= N) return;
-  const float* xp = X + p * ldx;
-  double s = 0.0;
-  for (int i = lane; i < n; i += 32) {
-    const double v = xp[i];
-    s += v * v;
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-  if (lane == 0) {
-    xn2[p] = s;
-    e[p] = s;
-  }
-}
-
 // Exact FFMA dot of two zero-padded rows of ld floats (16-byte aligned), one warp.
 __device__ __forceinline__ float warp_dot_rows(const float* __restrict__ x, const float* __restrict__ c, int ld) {
   float s = 0.f;
@@ -402,11 +382,6 @@ void free_pair_tables(TreeHandle* t) {
   t->pair_tables.clear();
   cudaFree(t->leaf_pos);
   t->leaf_pos = nullptr;
-}
-
-cudaError_t launch_gram_init(const float* X, int64_t ldx, int n, int64_t N, double* xn2, double* e_ws,
-                             cudaStream_t st) {
-  return launch_kernel(gram_init_kernel, (unsigned)((N + 7) / 8), 256, 0, st, true, X, ldx, n, N, xn2, e_ws);
 }
 
 cudaError_t launch_update_gram(const GramArgs& a, cudaStream_t st) {

@@ -110,6 +110,8 @@ struct UpdateArgs {
   int* S_ws;             // support atoms [K][N]
   float* c_ws;           // coefficients [K][N]
   int iter;              // iteration index = support size of every active patch
+  double* xn2;           // Gram path: ||x||^2 per patch (init), and the running ||r||^2
+  double* e_ws;
 };
 
 // Gram path (gram_path.cu, OMP on trees whose depth-L nodes are single atoms):
@@ -158,8 +160,6 @@ cudaError_t launch_update_gram(const GramArgs& a, cudaStream_t st);
 // leaf_pos of a tree whose depth-L nodes are single atoms covering the dictionary
 bool build_leaf_pos(TreeHandle* t, int64_t m, cudaStream_t st);
 void free_pair_tables(TreeHandle* t);
-cudaError_t launch_gram_init(const float* X, int64_t ldx, int n, int64_t N, double* xn2, double* e_ws,
-                             cudaStream_t st);
 extern int g_gram_path;   // 0 off, 1 auto (wide rows), 2 whenever supported
 
 struct UpdateCfg {
