@@ -408,12 +408,16 @@ def _encode_on_stream(selector, X, K, method, tol, paths, stream) -> EncodeResul
 
 
 def encode_host(selector, X: np.ndarray, K: int, method: str = "omp", tol: float | None = None,
-                chunk: int = 1 << 17, out: dict | None = None) -> EncodeResult:
-    """End-to-end encode from host memory (``stmp_encode_host``): chunked H2D
-    (ramped chunk sizes; 2^17 measured best on config 1: 178 M patches/s with
-    pinned buffers against a 55 GB/s H2D copy floor of 217 M/s),
+                chunk: int | None = None, out: dict | None = None) -> EncodeResult:
+    """End-to-end encode from host memory (``stmp_encode_host``): chunked H2D,
     encode and D2H overlapped on three streams.  Pass pinned buffers (e.g. torch
-    ``pin_memory()`` tensors' numpy views) for full copy bandwidth."""
+    ``pin_memory()`` tensors' numpy views) for full copy bandwidth.
+
+    ``chunk`` (rows per encode) defaults to 2^17 for narrow rows (config 1: 178 M
+    patches/s against a 55 GB/s pinned-copy floor of 217 M/s) and to half the
+    batch for rows of >= 256 floats: there every encode also streams the deepest
+    level's node tables once per iteration whatever its size (config 4: 94 ms
+    for 2^19 patches in two chunks, 129 ms in four, 459 ms in 32)."""
     if method not in ("mp", "omp"):
         raise ValueError(f"unknown method {method!r}")
     X = np.asarray(X)
@@ -423,6 +427,8 @@ def encode_host(selector, X: np.ndarray, K: int, method: str = "omp", tol: float
     if X.shape[1] != g.n:
         raise ValueError(f"patches have dimension {X.shape[1]}, dictionary atoms have {g.n}")
     N = X.shape[0]
+    if chunk is None:
+        chunk = 1 << 17 if g.n < 256 else max(4096, -(-N // 2))
     if out is None:
         out = dict(idx=np.empty((N, K), np.int32), coef=np.empty((N, K), np.float32),
                    count=np.empty(N, np.int32), resnorm=np.empty(N, np.float32),
