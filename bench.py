@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--method", default="omp", choices=["omp", "mp"])
     ap.add_argument("--selector", default="tree", choices=["tree", "exact"])
     ap.add_argument("--patches", type=int, default=0, help="override N per GPU")
+    ap.add_argument("--alpha", type=float, default=0.0,
+                    help="tree descent alpha (default 1/max(branching): greedy); larger = beam descent")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -152,7 +154,7 @@ def _cpu_worker(args):
     return out
 
 
-def cpu_rate(wl, flat, X, K, method, selector, seconds, cores=None, results=None):
+def cpu_rate(wl, flat, X, K, method, selector, seconds, cores=None, results=None, alpha=None):
     """Time the reference CPU algorithm (oracle port, f64 NumPy, per-patch loop as
     in pkg/src/stmp/pipelines.py:199-206) on a fork pool of all host cores.
     The per-patch results (rows [0, done) of X) are appended to ``results``."""
@@ -160,7 +162,7 @@ def cpu_rate(wl, flat, X, K, method, selector, seconds, cores=None, results=None
     cores = cores or len(os.sched_getaffinity(0))
     a64 = wl.atoms.astype(np.float64)
     otree = O.OracleTree.from_flat(flat) if selector == "tree" else None
-    _POOL_STATE.update(a64=a64, otree=otree, alpha=wl.cfg.alpha, K=K, method=method, X=X)
+    _POOL_STATE.update(a64=a64, otree=otree, alpha=alpha or wl.cfg.alpha, K=K, method=method, X=X)
     # calibrate on one core
     t0 = time.perf_counter()
     probe = 16 if selector == "tree" else 2
@@ -234,7 +236,10 @@ def main():
     cfg = W.CONFIGS[args.config]
     exhaustive = args.selector == "exact"
     N = args.patches or cfg.N
+    alpha = args.alpha or cfg.alpha
     workload = f"{cfg.name}/{'tree' if not exhaustive else 'exhaustive'}-{args.method.upper()}"
+    if args.alpha and not exhaustive:
+        workload += f"-alpha{args.alpha:g}"
 
     if args.impl == "reference":
         if rank != 0:
@@ -244,12 +249,12 @@ def main():
         sample_rows = min(N, 65536)
         X = W.make_patches(wl, sample_rows)
         # size each step to ~3 s of the whole CPU so the run ends within minutes
-        rate0, cores, _, _ = cpu_rate(wl, flat, X, cfg.K, args.method, args.selector, 3.0)
+        rate0, cores, _, _ = cpu_rate(wl, flat, X, cfg.K, args.method, args.selector, 3.0, alpha=alpha)
         per_step = int(max(cores, min(len(X), rate0 * 3.0)))
         times = []
         for step in range(args.warmup + args.steps):
             r, cores, done, wall = cpu_rate(wl, flat, X[:per_step], cfg.K, args.method,
-                                            args.selector, 1e9)
+                                            args.selector, 1e9, alpha=alpha)
             if step >= args.warmup:
                 times.append((done, wall))
         done = sum(d for d, _ in times)
@@ -292,7 +297,7 @@ def main():
     flat = T.load_structure(tree_path(cfg.cid), wl.atoms) if not exhaustive else None
     chunk_start = rank * (-(-N // cfg.chunk) * cfg.chunk)  # distinct patch shard per rank
     X_host = W.make_patches(wl, N, start=chunk_start)
-    sel = P.ExactSelector(wl.atoms) if exhaustive else P.TreeSelector(flat, wl.atoms, cfg.alpha)
+    sel = P.ExactSelector(wl.atoms) if exhaustive else P.TreeSelector(flat, wl.atoms, alpha)
     Xd = torch.as_tensor(X_host).cuda()
     # a dedicated stream: the library replays repeated encodes on it as CUDA graphs
     # (the legacy default stream cannot be captured)
@@ -404,13 +409,22 @@ def main():
     timed_ms = sum(f["ms"] for f in fams.values()) or 1.0
     dom = max(fams, key=lambda f: fams[f]["ms"]) if fams else "other"
     gram = any("update_gram_kernel" in k for k in ktimes)
-    work = RL.gram_family_work(cfg, dom, N) if gram else RL.family_work(cfg, dom, N, args.method, exhaustive)
+    if dom == "fused":
+        work = RL.fused_work(cfg, N, alpha, args.method)
+    elif gram:
+        work = RL.gram_family_work(cfg, dom, N)
+    else:
+        work = RL.family_work(cfg, dom, N, args.method, exhaustive)
     if gram:   # the step model of the path that ran (Gram path: no residual traffic)
         rm = RL.gram_model(cfg, N, hbm_gbs=hbm)
     dom_ms = fams[dom]["ms"] if fams else launch_ms
     dom_launches = fams[dom]["launches"] if fams else 1
     avg_s = dom_ms / dom_launches / 1e3
-    if work["bound"] == "hbm":
+    if work["bound"] == "fp32":
+        achieved = work["flops"] / dom_launches / avg_s / 1e12
+        roof = {"bound": "fp32 (SIMT FFMA)", "achieved": achieved, "peak": RL.FP32_SIMT_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / RL.FP32_SIMT_TFLOPS, "traffic": None}
+    elif work["bound"] == "hbm":
         achieved = work["bytes"] / dom_launches / avg_s / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": None}
@@ -453,7 +467,7 @@ def main():
         from oracle.parity import compare
         oracle_res = []
         rate, cores, done, wall = cpu_rate(wl, flat, X_host[:65536], cfg.K, args.method, args.selector,
-                                           args.cpu_seconds, results=oracle_res)
+                                           args.cpu_seconds, results=oracle_res, alpha=alpha)
         cpu = {"value": rate, "unit": "patches/s", "cores": cores, "kind": "port",
                "sample": f"{done} patches (prefix of the batch) in {wall:.1f}s, oracle port of the "
                          f"reference (f64 NumPy per-patch loop), {cores}-process pool on {cpu_model()}"}

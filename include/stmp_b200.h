@@ -81,9 +81,11 @@ void stmp_tree_free(stmp_tree* t);
 
 /* Batch encode N patches X[N x ldx] (f32, device).
  *   tree == NULL selects exhaustively (ExactSelector, pursuit.py:165-172),
- *   otherwise greedy tree descent (TreeSelector, pursuit.py:175-191); the
- *   GPU supports greedy alpha only (retained_count(alpha, k_i) == 1 at every
- *   level), anything else is STMP_EINVAL.
+ *   otherwise tree descent (TreeSelector, pursuit.py:175-191) with
+ *   retained_count(alpha, k_l) children kept per node at level l: greedy
+ *   (one child per level, alpha <= 1/max(branching)) runs on the
+ *   staged tensor-core pipeline for large batches; non-greedy alpha (beam
+ *   descent, pursuit.py:134-162) on the warp-per-patch kernel (<= 8 levels).
  *   method: STMP_METHOD_MP / STMP_METHOD_OMP / STMP_METHOD_SELECT.
  *   tol_abs < 0 means the reference default 1e-6 * ||x|| (pursuit.py:207-209).
  * Outputs (device; idx, coef, count and resnorm are required, path and ip
@@ -97,9 +99,10 @@ void stmp_tree_free(stmp_tree* t);
  *   (ScoreCounter, pkg/src/stmp/dictionary.py:40-65) (optional; 8-byte aligned).
  * Replaces `matching_pursuit` (pursuit.py:194-221) driven by the batch loop
  * of `_code_patches` (pkg/src/stmp/pipelines.py:180-217).
- * Workspace: stmp_encode_workspace() bytes of device memory, caller-owned.   */
+ * Workspace: stmp_encode_workspace() bytes of device memory, caller-owned
+ * (the same alpha as the encode: beam descent needs frontier scratch).      */
 size_t stmp_encode_workspace(const stmp_dict* d, const stmp_tree* t, int64_t N, int32_t K,
-                             int32_t method);
+                             int32_t method, double alpha);
 int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t N, int64_t ldx,
                 int32_t K, int32_t method, double alpha, double tol_abs, int32_t* idx,
                 float* coef, int32_t* count, float* resnorm, int32_t* path, int32_t* ip,

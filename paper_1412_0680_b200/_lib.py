@@ -33,7 +33,7 @@ EXPORTS = {
                                    C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_uint64,
                                    C.c_void_p, C.POINTER(C.c_void_p)]),
     "stmp_tree_free": (None, [C.c_void_p]),
-    "stmp_encode_workspace": (C.c_size_t, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32]),
+    "stmp_encode_workspace": (C.c_size_t, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_double]),
     "stmp_encode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int32,
                               C.c_int32, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

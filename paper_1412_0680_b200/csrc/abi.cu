@@ -370,8 +370,30 @@ void stmp_tree_free(stmp_tree* t) {
   delete t;
 }
 
-static bool use_staged(const stmp_dict* d, const stmp_tree* t, int64_t N, int32_t K, int32_t method) {
+// Beam descent (retained_count(alpha, k_l) > 1 at some level, pursuit.py:141-153):
+// children kept per level and a bound on the frontier size.  Returns false for
+// greedy alpha (one child per level).
+static bool beam_plan(const stmp_tree* t, double alpha, int* keep, int* max_frontier) {
+  if (t == nullptr || !(alpha > 0.0 && alpha <= 1.0)) return false;
+  bool beam = false;
+  int64_t f = 1, mx = 1;
+  for (int l = 0; l < t->levels; ++l) {
+    const int k = retained_count(alpha, t->branching[l]);
+    if (keep && l < stmp::kMaxBeamLevels) keep[l] = k;
+    beam |= k > 1;
+    const int64_t nodes = (l + 2 < (int)t->level_offsets.size() ? t->level_offsets[l + 2] - t->level_offsets[l + 1]
+                                                                 : t->num_leaves);
+    f = std::min<int64_t>(f * std::min(k, t->max_children), nodes);
+    mx = std::max(mx, f);
+  }
+  if (max_frontier) *max_frontier = (int)std::min<int64_t>(mx, 1 << 30);
+  return beam;
+}
+
+static bool use_staged(const stmp_dict* d, const stmp_tree* t, int64_t N, int32_t K, int32_t method,
+                       double alpha = 0.0) {
   if (g_path_mode == 1 || d == nullptr) return false;
+  if (beam_plan(t, alpha, nullptr, nullptr)) return false;   // beam descent: the fused warp-per-patch kernel
   if (!stmp::staged_supported(d, t, K, method)) return false;
   // exhaustive selection: the tensor-core scan wins as soon as one tile fills an SM
   return g_path_mode == 2 || N >= (t == nullptr ? g_exact_min : g_staged_min);
@@ -426,8 +448,12 @@ int stmp_set_option(const char* key, int64_t value) {
 }
 
 size_t stmp_encode_workspace(const stmp_dict* d, const stmp_tree* t, int64_t N, int32_t K,
-                             int32_t method) {
-  if (!use_staged(d, t, N, K, method) || N <= 0) return 0;
+                             int32_t method, double alpha) {
+  if (N <= 0 || d == nullptr) return 0;
+  int mf = 0;
+  if (beam_plan(t, alpha, nullptr, &mf))
+    return (size_t)stmp::fused_warps(N) * (size_t)stmp::beam_scratch_ints(mf) * sizeof(int);
+  if (!use_staged(d, t, N, K, method, alpha)) return 0;
   return stmp::staged_workspace_bytes(d, t, N, K, method);
 }
 
@@ -449,12 +475,9 @@ static int validate_encode(const stmp_dict* d, const stmp_tree* t, int64_t N, in
       return fail(STMP_ESTALE, "tree fingerprint %#018llx does not match dictionary fingerprint %#018llx",
                   (unsigned long long)t->fingerprint, (unsigned long long)d->fingerprint);
     if (t->dict != d && t->n != d->n) return fail(STMP_EINVAL, "tree dimension differs from dictionary");
-    for (int l = 0; l < t->levels; ++l)
-      if (retained_count(alpha, t->branching[l]) != 1)
-        return fail(STMP_EINVAL,
-                    "alpha=%g keeps %d branches at level %d; the GPU path implements greedy descent "
-                    "only (alpha <= 1/max(branching))",
-                    alpha, retained_count(alpha, t->branching[l]), l);
+    if (beam_plan(t, alpha, nullptr, nullptr) && t->levels > stmp::kMaxBeamLevels)
+      return fail(STMP_EINVAL, "beam descent supports at most %d tree levels, got %d", stmp::kMaxBeamLevels,
+                  t->levels);
   }
   return STMP_OK;
 }
@@ -470,7 +493,7 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
     return fail(STMP_EINVAL, "X, idx, coef, count and resnorm must be device pointers");
   if (reinterpret_cast<uintptr_t>(ip) % 8 != 0)
     return fail(STMP_EINVAL, "ip must be 8-byte aligned (its two counters are updated as one 64-bit word)");
-  if (use_staged(d, t, N, K, method)) {
+  if (use_staged(d, t, N, K, method, alpha)) {
     const size_t need = stmp::staged_workspace_bytes(d, t, N, K, method);
     if (workspace == nullptr || workspace_bytes < need)
       return fail(STMP_EINVAL, "workspace of %zu bytes is below the required %zu (stmp_encode_workspace)",
@@ -565,6 +588,14 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
   a.K = K;
   a.method = method;
   a.tol_abs = tol_abs < 0 ? -1.f : (float)tol_abs;
+  a.beam = beam_plan(t, alpha, a.keep, &a.max_frontier) ? 1 : 0;
+  if (a.beam) {
+    const size_t need = (size_t)stmp::fused_warps(N) * (size_t)stmp::beam_scratch_ints(a.max_frontier) * sizeof(int);
+    if (workspace == nullptr || workspace_bytes < need)
+      return fail(STMP_EINVAL, "beam descent needs a workspace of %zu bytes (stmp_encode_workspace), got %zu", need,
+                  workspace_bytes);
+    a.scratch = static_cast<int*>(workspace);
+  }
   a.idx = idx;
   a.coef = coef;
   a.count = count;
@@ -603,7 +634,7 @@ int stmp_encode_host(const stmp_dict* d, const stmp_tree* t, const float* X, int
   // Persistent staging: device buffers and streams are kept between calls
   // (allocating ~1 GB of workspace per call would dominate the host path).
   std::lock_guard<std::mutex> lock(g_host_mutex);
-  const size_t wsz = stmp_encode_workspace(d, t, chunk, K, method);
+  const size_t wsz = stmp_encode_workspace(d, t, chunk, K, method, alpha);
   for (int i = 0; i < kHostStreams; ++i)
     if (int rc = ensure_stage(g_host[i], chunk, d->n, K, wsz)) return rc;
   // Chunk schedule: ramp up (chunk/4, chunk/2) so the first encode starts

@@ -64,6 +64,93 @@ __device__ __forceinline__ int key_id(unsigned long long k) {
   return (int)(0xFFFFFFFFu - (unsigned)(k & 0xFFFFFFFFull));
 }
 
+// Beam descent (pursuit.py:134-162 for retained_count > 1): every frontier node
+// keeps its `keep` best children by |score| (a stable sort on -|score|: ties to
+// the lower position), in child order; the next frontier is the concatenation
+// over the frontier in order.  Then the leaf atoms of all surviving depth-L
+// nodes are scored, max |score|, ties to the lowest atom index.  One warp per
+// patch; frontiers and a node's child scores live in the warp's global scratch.
+// Returns the leaf winner in (bk, bs); writes the first survivor per level to
+// `path_row` (the oracle's path) when given.
+template <int VPL>
+__device__ void beam_select(const FusedArgs& a, const float (&r)[VPL], int lane, int* scr, int* path_row,
+                            unsigned long long& bk, float& bs, int& ipc, int& ipa) {
+  const int ld = a.ld;
+  const int L = a.tree.levels;
+  int* fr = scr;
+  int* fn = scr + a.max_frontier;
+  float* sc = reinterpret_cast<float*>(scr + 2 * a.max_frontier);
+  if (lane == 0) fr[0] = 0;
+  int nf = 1;
+  __syncwarp();
+  for (int lvl = 0; lvl < L; ++lvl) {
+    const int keep = a.keep[lvl];
+    int nn = 0;
+    for (int f = 0; f < nf; ++f) {
+      const int node = fr[f];
+      const int b = __ldg(a.tree.child_begin + node);
+      const int c = __ldg(a.tree.child_count + node);
+      ipc += c;
+      if (keep >= c) {
+        for (int j = lane; j < c; j += 32) fn[nn + j] = b + j;
+        nn += c;
+        continue;
+      }
+      // |score| of every child
+      for (int c0 = 0; c0 < c; c0 += 32) {
+        const int nr = min(32, c - c0);
+        float p[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) p[j] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nr) {
+            const float* rp = a.tree.cent + (int64_t)(b + c0 + j) * ld + lane;
+#pragma unroll
+            for (int i = 0; i < VPL; ++i) p[j] = fmaf(rp[32 * i], r[i], p[j]);
+          }
+        const float s = reduce_scatter32(p, lane);
+        if (lane < nr) sc[c0 + lane] = fabsf(s);
+      }
+      __syncwarp();
+      // the keep best, ties to the lower position (a stable argsort of -|s|)
+      for (int q = 0; q < keep; ++q) {
+        unsigned long long best = 0ull;
+        for (int j = lane; j < c; j += 32) {
+          const float v = sc[j];
+          const unsigned long long k = v >= 0.f ? score_key(v, (unsigned)j) : 0ull;
+          best = k > best ? k : best;
+        }
+        best = warp_max_u64(best);
+        if (lane == 0) sc[key_id(best)] = -1.f;   // taken
+        __syncwarp();
+      }
+      // survivors in child order
+      for (int c0 = 0; c0 < c; c0 += 32) {
+        const bool taken = c0 + lane < c && sc[c0 + lane] < 0.f;
+        const unsigned m = __ballot_sync(kFull, taken);
+        if (taken) fn[nn + __popc(m & ((1u << lane) - 1u))] = b + c0 + lane;
+        nn += __popc(m);
+      }
+      __syncwarp();
+    }
+    if (path_row != nullptr && lane == 0) path_row[lvl] = fn[0];
+    int* tmp = fr;
+    fr = fn;
+    fn = tmp;
+    nf = nn;
+    __syncwarp();
+  }
+  bk = 0ull;
+  for (int f = 0; f < nf; ++f) {
+    const int node = fr[f];
+    const int b = __ldg(a.tree.child_begin + node);
+    const int c = __ldg(a.tree.child_count + node);
+    score_rows<VPL, true>(a.atoms, ld, 0, a.tree.leaf_atom + b, c, r, lane, bk, bs);
+    ipa += c;
+  }
+}
+
 template <int VPL>
 __global__ void __launch_bounds__(256) encode_fused_kernel(FusedArgs a) {
   extern __shared__ __align__(16) float smem[];
@@ -112,7 +199,11 @@ __global__ void __launch_bounds__(256) encode_fused_kernel(FusedArgs a) {
       // ---------------- selection ----------------
       unsigned long long bk = 0ull;
       float bs = 0.f;
-      if (a.has_tree) {
+      if (a.has_tree && a.beam) {
+        const int64_t gw = (int64_t)blockIdx.x * wpb + warp;
+        beam_select<VPL>(a, r, lane, a.scratch + gw * beam_scratch_ints(a.max_frontier),
+                         a.path != nullptr ? a.path + (p * K + t) * L : nullptr, bk, bs, ipc, ipa);
+      } else if (a.has_tree) {
         int node = 0;
         for (int lvl = 0; lvl < L; ++lvl) {
           const int b = __ldg(a.tree.child_begin + node);
@@ -254,8 +345,7 @@ cudaError_t launch_vpl(const FusedArgs& a, size_t smem, int grid, cudaStream_t s
   auto k = encode_fused_kernel<VPL>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<grid, 256, smem, s>>>(a); note_launch();
-  return cudaGetLastError();
+  return launch_kernel(k, grid, 256, smem, s, false, a);
 }
 
 }  // namespace
@@ -268,16 +358,22 @@ int fused_vpl_for(int n) {
   return -1;
 }
 
+int64_t fused_warps(int64_t N) {
+  const int wpb = 8;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    sms = 148;
+  }
+  const int64_t want = (N + wpb - 1) / wpb;
+  const int64_t cap = (int64_t)sms * 4;
+  return (want < cap ? (want > 0 ? want : 1) : cap) * wpb;
+}
+
 cudaError_t launch_encode_fused(const FusedArgs& a, cudaStream_t stream) {
   const int wpb = 8;
   const size_t smem = sizeof(float) * ((size_t)a.root_smem_rows * a.ld + (size_t)wpb * a.warp_smem_floats);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t want = (a.N + wpb - 1) / wpb;
-  int per_sm = 4;
-  const int64_t cap = (int64_t)sms * per_sm;
-  const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+  const int grid = (int)(fused_warps(a.N) / wpb);
   switch (a.vpl) {
 #define STMP_CASE(V) \
   case V:            \

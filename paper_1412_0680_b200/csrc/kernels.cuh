@@ -33,7 +33,16 @@ struct FusedArgs {
   int root_begin;
   int cache_atoms;        // support atoms cached per warp in shared memory
   int warp_smem_floats;   // per-warp shared scratch (OMP factor + optional atom cache)
+  // non-greedy alpha (beam descent, pkg/src/stmp/pursuit.py:134-162): children kept
+  // per node at each level, and per-warp global scratch for the frontiers
+  int beam;               // 0: greedy (one child per level)
+  int keep[8];            // retained_count(alpha, k_l) per level
+  int max_frontier;       // largest frontier (nodes) over the levels
+  int* scratch;           // [warps][2 * max_frontier ints | 256 floats]
 };
+constexpr int kMaxBeamLevels = 8;
+// per-warp scratch of the beam descent (ints): two frontiers and a score row
+__host__ __device__ inline int64_t beam_scratch_ints(int max_frontier) { return 2 * (int64_t)max_frontier + 256; }
 
 int fused_vpl_for(int n);
 
@@ -56,5 +65,7 @@ cudaError_t launch_coded_exposure(const float* X, int64_t N, int n_in, const flo
 cudaError_t launch_block_average(const float* X, int64_t N, int rank, const int64_t* in_shape,
                                  const int64_t* factors, double* Y, cudaStream_t st);
 cudaError_t launch_encode_fused(const FusedArgs& a, cudaStream_t stream);
+// warps of the fused kernel's persistent grid for N patches (beam scratch sizing)
+int64_t fused_warps(int64_t N);
 
 }  // namespace stmp

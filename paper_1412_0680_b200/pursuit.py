@@ -10,8 +10,9 @@ runs the whole MP / OMP loop for millions of patches in one call.
 
 Error behaviour follows the reference: ``ValueError`` for bad alpha / K /
 tolerance / dimensions, ``StaleTreeError`` for a tree built on another
-dictionary.  The GPU path implements greedy descent (alpha <= 1/max(k),
-SURVEY F4); other alphas raise ``ValueError`` instead of silently differing.
+dictionary.  Greedy descent (alpha <= 1/max(k)) runs on the
+staged tensor-core pipeline; other alphas run the reference's beam descent on
+the warp-per-patch kernel.
 """
 
 from __future__ import annotations
@@ -323,7 +324,10 @@ class ExactSelector(_GpuSelector):
 
 
 class TreeSelector(_GpuSelector):
-    """GPU ``TreeSelector`` (pursuit.py:175-191): greedy descent only."""
+    """GPU ``TreeSelector`` (pursuit.py:175-191).  Greedy alpha (one child per
+    level) runs on the staged tensor-core pipeline for large batches; any other
+    alpha is the beam descent of stmp_select (pursuit.py:134-162) on the
+    warp-per-patch kernel."""
 
     def __init__(self, tree, dictionary, alpha: float):
         if not 0.0 < alpha <= 1.0:
@@ -335,11 +339,6 @@ class TreeSelector(_GpuSelector):
             raise StaleTreeError(
                 f"tree fingerprint {flat.fingerprint:#018x} does not match "
                 f"dictionary fingerprint {fp:#018x}")
-        for lvl, k in enumerate(flat.branching):
-            if retained_count(alpha, k) != 1:
-                raise ValueError(
-                    f"alpha={alpha} keeps {retained_count(alpha, k)} branches at level {lvl}; "
-                    "the GPU selector implements greedy descent only (alpha <= 1/max(branching))")
         self.dictionary = dictionary
         self.gdict = _gpu_dict_for(dictionary)
         self.tree = GpuTree(flat, self.gdict)
@@ -396,7 +395,7 @@ def _encode_on_stream(selector, X, K, method, tol, paths, stream) -> EncodeResul
         path = torch.empty((N, K, tree.levels), dtype=torch.int32, device=dev)
     lib = _lib.load()
     th = tree.handle if tree is not None else None
-    ws_bytes = int(lib.stmp_encode_workspace(g.handle, th, N, K, _METHODS[method]))
+    ws_bytes = int(lib.stmp_encode_workspace(g.handle, th, N, K, _METHODS[method], float(selector.alpha)))
     ws = torch.empty((max(ws_bytes, 1),), dtype=torch.uint8, device=dev)
     _lib.check(lib.stmp_encode(
         g.handle, th, X.data_ptr(), N, X.stride(0) if N > 1 else g.n, K, _METHODS[method],

@@ -77,7 +77,8 @@ FAMILIES = (("score", ("score_ts_kernel", "score_st_kernel")),
             ("exact_scan", ("exact_scan_kernel",)),
             ("update", ("update_omp8_kernel", "update_wide_kernel", "update_gram_kernel", "update_kernel")),
             ("scatter", ("scatter_scan_kernel", "scatter_kernel", "scatter_root_kernel", "scan_kernel")),
-            ("init", ("init_kernel",)))
+            ("init", ("init_kernel",)),
+            ("fused", ("encode_fused_kernel",)))
 
 
 def family_of(name: str) -> str:
@@ -85,6 +86,27 @@ def family_of(name: str) -> str:
         if any(k in name for k in keys):
             return fam
     return "other"
+
+
+def beam_ip(branching, alpha: float, m: int) -> int:
+    """Inner products of one beam selection (pursuit.py:134-162): the frontier of
+    level l holds F_l nodes, each scoring its k_l children; the survivors' leaf
+    atoms are scored at the end (balanced tree: m / prod(k) atoms per leaf node)."""
+    f, ips = 1, 0
+    for k in branching:
+        ips += f * k
+        f *= min(k, max(1, math.ceil(alpha * k - 1e-9)))
+    return ips + f * max(1, round(m / math.prod(branching)))
+
+
+def fused_work(cfg, N: int, alpha: float, method: str = "omp") -> dict:
+    """The warp-per-patch kernel (encode_fused.cu): FFMA dot products of every
+    scored centroid / atom with the residual held in registers -- SIMT-FLOP
+    bound; HBM bytes are x in and the outputs."""
+    n, K = cfg.n, cfg.K
+    ips = beam_ip(cfg.branching, alpha, cfg.m)
+    upd = 2 * n * K * (K + 1) if method == "omp" else 2 * n * K
+    return {"bytes": float(N * (4 * n + 8 * K + 16)), "flops": float(N * (K * 2 * n * ips + upd)), "bound": "fp32"}
 
 
 def gram_family_work(cfg, family: str, N: int) -> dict:

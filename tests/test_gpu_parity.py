@@ -223,7 +223,7 @@ def test_error_behaviour_matches_reference():
     z = golden("pursuit_small.npz")
     flat = flat_from_fixture(z)
     with pytest.raises(ValueError):
-        P().TreeSelector(flat, z["atoms"], 0.5)   # non-greedy: refused, not silently different
+        P().TreeSelector(flat, z["atoms"], 1.5)   # alpha outside (0, 1] (pursuit.py:179-180)
     with pytest.raises(ValueError):
         P().TreeSelector(flat, z["atoms"], 0.0)
     other = np.ascontiguousarray(z["atoms"][::-1])
@@ -533,3 +533,56 @@ def test_gram_path_exact_sparse_and_tolerance(tol_tag, tol):
     rep = compare({k: v[rows] for k, v in out.items()}, ref, X[rows], check_path=True)
     print(f"gram exact-sparse {tol_tag}: {rep.summary()}")
     assert rep.ok, rep.summary()
+
+
+# ----------------------------------------------------------------- beam (non-greedy alpha) descent
+
+@pytest.mark.parametrize("tag,alpha", [("beam", 0.3), ("full", 1.0)])
+def test_tree_select_beam_matches_reference(tag, alpha):
+    """stmp_select with retained_count > 1 (pursuit.py:134-162) against the
+    reference's own recorded selections (select_small.npz)."""
+    z = golden("select_small.npz")
+    flat = flat_from_fixture(z)
+    sel = P().TreeSelector(flat, z["atoms"], alpha)
+    out, names = launched(lambda: run(sel, z["Q"], 1, "select"))
+    assert any("encode_fused_kernel" in k for k in names)
+    t = O.OracleTree.from_flat(flat)
+    a64 = z["atoms"].astype(np.float64)
+    gaps = np.array([O.tree_select(t, a64, q.astype(np.float64), alpha)[5] for q in z["Q"]])
+    ok = (out["idx"][:, 0] == z[f"{tag}_idx"]) | (gaps < 1e-5)
+    assert ok.all()
+    same = out["idx"][:, 0] == z[f"{tag}_idx"]
+    np.testing.assert_allclose(out["coef"][same, 0], z[f"{tag}_score"][same], rtol=1e-5, atol=1e-6)
+    np.testing.assert_array_equal(out["ip"], z[f"{tag}_ip"])
+
+
+@pytest.mark.parametrize("method", ["omp", "mp"])
+def test_beam_pursuit_matches_oracle(method):
+    z = golden("pursuit_small.npz")
+    flat = flat_from_fixture(z)
+    K = int(z["K"])
+    a64 = z["atoms"].astype(np.float64)
+    sel = P().TreeSelector(flat, z["atoms"], 0.3)
+    out = run(sel, z["X"], K, method)
+    ref = oracle_pack(O.tree_selector(O.OracleTree.from_flat(flat), a64, 0.3), a64, z["X"], K, method)
+    rep = compare(out, ref, z["X"], check_path=True)
+    assert rep.ok, rep.summary()
+    assert rep.excused <= 2
+
+
+@pytest.mark.parametrize("cid,rows,alpha", [(1, 1024, 0.1), (4, 48, 0.1)])
+def test_config_beam_parity(cid, rows, alpha):
+    """The paper's alpha = 0.1 setting on config trees: frontiers
+    of ceil(0.1 k) children per node (c1: 4, 16, 32 nodes; c4: 7, 49, 196)."""
+    from paper_1412_0680_b200 import workloads as W
+    from oracle import parallel as OP
+    cfg, wl, flat = config(cid)
+    X = W.make_patches(wl, rows)
+    sel = P().TreeSelector(flat, wl.atoms, alpha)
+    out = run(sel, X, cfg.K, "omp")
+    a64 = wl.atoms.astype(np.float64)
+    ref = O.pack(OP.encode_parallel(O.OracleTree.from_flat(flat), a64, X, cfg.K, "omp", alpha=alpha), cfg.K)
+    rep = compare(out, ref, X, check_path=True)
+    print(f"c{cid} beam alpha={alpha}: {rep.summary()}")
+    assert rep.ok, rep.summary()
+    assert rep.excused <= max(2, rows // 200)

@@ -11,6 +11,8 @@ run --config 2 --steps 5 --warmup 3
 run --config 3 --steps 10 --warmup 3
 run --config 4 --steps 5 --warmup 3
 run --config 4 --selector exact --steps 1 --warmup 3 --no-e2e
+run --config 1 --alpha 0.1 --patches 131072 --steps 3 --warmup 2 --no-e2e
+run --config 4 --alpha 0.1 --patches 8192 --steps 2 --warmup 2 --no-e2e
 python - <<'PY'
 import json
 for line in open("gpurun_out/configs.jsonl"):
@@ -22,6 +24,6 @@ for line in open("gpurun_out/configs.jsonl"):
     r = d["roofline"]
     e2e = d["e2e"]["value"] if d.get("e2e") else None
     print(f'{c["workload"]:44s} N={c["patches_per_gpu"]:8d} {d["value"]:14.1f} patches/s  ms/step {d["ms_per_step"]:9.3f}  '
-          f'step frac {r["step"]["frac"]:.3f}  dominant {r["kernel"][:40]} frac {r["frac"]:.3f} '
+          f'step frac {r["step"]["frac"] or 0:.3f}  dominant {r["kernel"][:40]} frac {r["frac"]:.3f} '
           f'(3xtf32 {r.get("frac_3xtf32")})  e2e {e2e}')
 PY
