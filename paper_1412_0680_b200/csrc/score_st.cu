@@ -316,9 +316,13 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
   const uint32_t off2 = chains == 2 ? accw : 0u;
   const uint32_t accs = accw * (uint32_t)chains;   // stride of the accumulator buffers
 
+#ifndef STMP_ST_L2HINTS
+#define STMP_ST_L2HINTS 1
+#endif
   if (warp == 5) {
     // ------------------------------------------------ table producer
     if (lane == 0) {
+      const uint64_t tab_policy = STMP_ST_L2HINTS ? l2_policy_evict_last() : l2_policy_evict_first();
       int bin = 0;
       for (int g = 0; g < total; ++g) {
         const int seq = g / kch, c = g - seq * kch;
@@ -326,9 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
         const int s = g % NB;
         if (g >= NB) mbar_wait(&done[s], (uint32_t)(g / NB - 1) & 1u);
         mbar_arrive_expect_tx(&full[s], chunk_bytes);
-        bulk_g2s(base + Ly.btab + s * bslot,
-                 reinterpret_cast<const uint8_t*>(a.table) + (size_t)bin * tb + (size_t)c * chunk_bytes, chunk_bytes,
-                 &full[s]);
+        bulk_g2s_hint(base + Ly.btab + s * bslot,
+                      reinterpret_cast<const uint8_t*>(a.table) + (size_t)bin * tb + (size_t)c * chunk_bytes,
+                      chunk_bytes, &full[s], tab_policy);
       }
     }
   } else if (warp == 4) {
@@ -378,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
     // ------------------------------------------------ stagers (warps 0-3)
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     const uint32_t land_s = smem_u32(base + Ly.land);
+    const uint64_t row_policy = l2_policy_evict_first();
     // row ids of this warp's 32 rows for the item being gathered (lane l: row 32w + l)
     int r_item = -1, r_row = -1;
     auto row_of = [&](int item) {
@@ -402,7 +407,11 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
           const int rl = 4 * i + q;   // row within the warp
           const int r = __shfl_sync(kFull, rmine, rl);
           const float* src = a.R + (r >= 0 ? (int64_t)r * a.ld + 32 * c + 4 * j : 0);
-          cp_async16(dst + sw128_offset((uint32_t)(warp * 32 + rl), (uint32_t)j), src, r >= 0 ? 16u : 0u);
+          if (STMP_ST_L2HINTS)
+            cp_async16_hint(dst + sw128_offset((uint32_t)(warp * 32 + rl), (uint32_t)j), src, r >= 0 ? 16u : 0u,
+                            row_policy);
+          else
+            cp_async16(dst + sw128_offset((uint32_t)(warp * 32 + rl), (uint32_t)j), src, r >= 0 ? 16u : 0u);
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");

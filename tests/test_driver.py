@@ -87,6 +87,12 @@ def test_gpu_code_patches_matches_reference(pre):
                             _PD(z, pre), params)
     assert out_d.is_cuda and out_d.dtype == torch.float64
     np.testing.assert_array_equal(out_d.cpu().numpy(), out)
+    # on a side stream: every launch and host read on it, the caller's stream waits
+    s = torch.cuda.Stream()
+    out_s, counter_s = code_patches(torch.as_tensor(z[f"{pre}_Y"]).cuda(), z[f"{pre}_dc_meas"], _selector(z, pre),
+                                    _PD(z, pre), params, stream=s)
+    np.testing.assert_array_equal(out_s.cpu().numpy(), out)
+    assert counter_s.inner_products == counter.inner_products
 
 
 @pytest.mark.gpu

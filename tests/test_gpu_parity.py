@@ -586,3 +586,87 @@ def test_config_beam_parity(cid, rows, alpha):
     print(f"c{cid} beam alpha={alpha}: {rep.summary()}")
     assert rep.ok, rep.summary()
     assert rep.excused <= max(2, rows // 200)
+
+
+# ----------------------------------------------------------------- API robustness (round-1 advisor findings)
+
+def test_encode_on_a_side_stream_matches_default_stream():
+    """encode(stream=s) allocates its outputs and workspace on s and orders s after
+    the producer of X: results equal the default-stream run."""
+    z = golden("pursuit_small.npz")
+    sel = P().TreeSelector(flat_from_fixture(z), z["atoms"], 1 / 16)
+    X = torch.as_tensor(np.ascontiguousarray(np.tile(z["X"], (300, 1)))).cuda()   # staged pipeline
+    ref = P().encode(sel, X, int(z["K"]), "omp")
+    s = torch.cuda.Stream()
+    Y = X * 1.0                                   # produced on the current stream
+    out = P().encode(sel, Y, int(z["K"]), "omp", stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    assert torch.equal(out.idx, ref.idx) and torch.equal(out.coef, ref.coef)
+
+
+def test_encode_host_rejects_bad_output_buffers():
+    z = golden("pursuit_small.npz")
+    sel = P().TreeSelector(flat_from_fixture(z), z["atoms"], 1 / 16)
+    X = np.ascontiguousarray(z["X"])
+    N, K = X.shape[0], int(z["K"])
+    good = dict(idx=np.empty((N, K), np.int32), coef=np.empty((N, K), np.float32), count=np.empty(N, np.int32),
+                resnorm=np.empty(N, np.float32), ip=np.empty((N, 2), np.int32))
+    P().encode_host(sel, X, K, "omp", out=good)
+    for key, bad in (("idx", np.empty((N - 1, K), np.int32)), ("coef", np.empty((N, K), np.float64)),
+                     ("ip", np.empty((2, N), np.int32).T), ("count", np.empty(N, np.int64))):
+        out = dict(good)
+        out[key] = bad
+        with pytest.raises(ValueError):
+            P().encode_host(sel, X, K, "omp", out=out)
+
+
+def test_encode_requires_count_and_resnorm():
+    import ctypes as C
+    from paper_1412_0680_b200 import _lib
+    z = golden("pursuit_small.npz")
+    sel = P().TreeSelector(flat_from_fixture(z), z["atoms"], 1 / 16)
+    X = torch.as_tensor(np.ascontiguousarray(z["X"])).cuda()
+    N, K = X.shape[0], int(z["K"])
+    idx = torch.empty((N, K), dtype=torch.int32, device="cuda")
+    coef = torch.empty((N, K), dtype=torch.float32, device="cuda")
+    lib = _lib.load()
+    rc = lib.stmp_encode(sel.gdict.handle, sel.tree.handle, X.data_ptr(), N, X.shape[1], K, _lib.METHOD_OMP,
+                         1 / 16, -1.0, idx.data_ptr(), coef.data_ptr(), None, None, None, None, None, 0,
+                         C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == _lib.STMP_EINVAL
+
+
+def test_graph_cache_never_replays_a_freed_tree():
+    """A tree handle allocated where a freed one lived must not replay the freed
+    one's CUDA graph (the cache keys on handle generations, and freeing a handle
+    drops its graphs)."""
+    import gc
+    from paper_1412_0680_b200 import tree as T
+    from paper_1412_0680_b200 import workloads as W
+    cfg, wl, flat = config(0)
+    rng = np.random.default_rng(5)
+    other = T._from_counts(flat.branching, flat.n, flat.fingerprint,
+                           [flat.child_count[flat.level_offsets[d]:flat.level_offsets[d + 1]]
+                            for d in range(flat.levels + 1)],
+                           flat.centroids, rng.permutation(flat.leaf_atom))   # same dictionary, other leaves
+    X = torch.as_tensor(W.make_patches(wl, 8192)).cuda()
+    s = torch.cuda.Stream()
+
+    def three_on_side_stream(tree):
+        sel = P().TreeSelector(tree, wl.atoms, cfg.alpha)
+        with torch.cuda.stream(s):
+            for _ in range(3):     # eager, capture, replay
+                r = P().encode(sel, X, cfg.K, "omp")
+        torch.cuda.synchronize()
+        out = r.idx.clone()
+        del sel, r
+        gc.collect()
+        return out
+
+    a = three_on_side_stream(flat)
+    b = three_on_side_stream(other)
+    fresh = P().encode(P().TreeSelector(other, wl.atoms, cfg.alpha), X, cfg.K, "omp").idx
+    torch.cuda.synchronize()
+    assert not torch.equal(a, b)
+    assert torch.equal(b, fresh)
