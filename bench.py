@@ -434,7 +434,8 @@ def main():
                 "traffic": None,
                 # the scores are fp32-accurate 3xTF32 (three tf32 products per k-step): against the
                 # dense TF32 rate measured live in this run, divided by 3
-                "peak_3xtf32": tf32 / 3, "frac_3xtf32": achieved / (tf32 / 3) if tf32 else None}
+                "peak_3xtf32": tf32 / 3, "frac_3xtf32": achieved / (tf32 / 3) if tf32 else None,
+                "hbm_frac": work["bytes"] / dom_launches / avg_s / 1e9 / hbm}
     roof.update({
         "kernel": f"{dom}: {', '.join(sorted(set(fams[dom]['kernels'])))}" if fams else "?",
         "launches_per_step": dom_launches, "avg_launch_ms": dom_ms / dom_launches,

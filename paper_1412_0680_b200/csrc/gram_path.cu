@@ -64,7 +64,27 @@ __device__ __forceinline__ float warp_dot_rows(const float* __restrict__ x, cons
   float s = 0.f;
   const float4* x4 = reinterpret_cast<const float4*>(x);
   const float4* c4 = reinterpret_cast<const float4*>(c);
-  for (int i = (int)(threadIdx.x & 31); i < ld / 4; i += 32) {
+  const int lane = (int)(threadIdx.x & 31);
+  const int nq = ld / 4;
+  // eight float4 of each row in flight per lane before the first FMA (a 1600-float
+  // row is 12.5 float4 per lane): the dot is latency-bound otherwise
+  int i = lane;
+  for (; i + 7 * 32 < nq; i += 8 * 32) {
+    float4 u[8], v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      u[q] = __ldg(x4 + i + 32 * q);
+      v[q] = __ldg(c4 + i + 32 * q);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      s = fmaf(u[q].x, v[q].x, s);
+      s = fmaf(u[q].y, v[q].y, s);
+      s = fmaf(u[q].z, v[q].z, s);
+      s = fmaf(u[q].w, v[q].w, s);
+    }
+  }
+  for (; i < nq; i += 32) {
     const float4 u = __ldg(x4 + i), v = __ldg(c4 + i);
     s = fmaf(u.x, v.x, s);
     s = fmaf(u.y, v.y, s);

@@ -88,6 +88,20 @@ def family_of(name: str) -> str:
     return "other"
 
 
+# fp32-accurate tensor rate of the score passes (3xTF32: three tf32 products per
+# k-step) against HBM, to decide which roof binds a tensor-core pass; bench.py
+# passes the TF32 rate it measures live (profiles/r02_peaks_tf32.json: 776)
+HBM_GBS_DEFAULT = 6548.2
+TF32X3_TFLOPS_DEFAULT = 776.3 / 3
+
+
+def binding(work: dict, hbm_gbs: float = HBM_GBS_DEFAULT, tensor_tflops: float = TF32X3_TFLOPS_DEFAULT) -> dict:
+    """Mark a tensor-core family "tensor"- or "hbm"-bound by its roofline time."""
+    t_hbm = work["bytes"] / (hbm_gbs * 1e9)
+    t_tc = work["flops"] / (tensor_tflops * 1e12)
+    return dict(work, bound="tensor" if t_tc > t_hbm else "hbm")
+
+
 def beam_ip(branching, alpha: float, m: int) -> int:
     """Inner products of one beam selection (pursuit.py:134-162): the frontier of
     level l holds F_l nodes, each scoring its k_l children; the survivors' leaf
@@ -131,8 +145,8 @@ def gram_family_work(cfg, family: str, N: int) -> dict:
     tables = sum(4 * n * k for k in kids[1:] if 4 * n * k > L2_BYTES)
     if family == "score":
         b = 4 * n + 4 * br[0] + K * (L - 1) * (4 * n + 8) + T_sum * 4 * sum(br[1:])
-        return {"bytes": float(N * b + K * tables),
-                "flops": float(N * 2 * n * (br[0] + K * sum(br[1:]))), "bound": "hbm"}
+        return binding({"bytes": float(N * b + K * tables),
+                        "flops": float(N * 2 * n * (br[0] + K * sum(br[1:])))})
     if family == "update":
         b = sum(8 * n + 4 * T + 4 * br[0] + 4 * 3 * (T + 1) for T in range(K))
         return {"bytes": float(N * b), "flops": float(N * K * 2 * n), "bound": "hbm"}
@@ -169,12 +183,10 @@ def family_work(cfg, family: str, N: int, method: str = "omp", exhaustive: bool 
     if family == "exact_scan":
         return {"bytes": float(N * K * 4 * n + K * 4 * n * m), "flops": float(N * K * 2 * n * m), "bound": "tensor"}
     if family == "score":
-        nodes = [math.prod(cfg.branching[:d]) for d in range(L)]          # nodes per level (parents)
         kids = [math.prod(cfg.branching[:d + 1]) for d in range(L)]
         tables = sum(4 * n * k for k in kids if 4 * n * k > L2_BYTES)
-        del nodes
-        return {"bytes": float(N * K * L * (4 * n + 8) + K * tables),
-                "flops": float(N * K * 2 * n * sum(cfg.branching)), "bound": "hbm"}
+        return binding({"bytes": float(N * K * L * (4 * n + 8) + K * tables),
+                        "flops": float(N * K * 2 * n * sum(cfg.branching))})
     if family == "update":
         if method == "omp":
             per = sum(4 * n * (3 + (T if big else 0)) for T in range(K))
