@@ -253,8 +253,8 @@ __device__ void recheck_near_ties(uint32_t taddr, uint32_t off2, int cc, int cb,
   }
 }
 
-template <int NA, int NB, int NAB>
-__global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int nacc, int chains) {
+template <int NA, int NB, int NAB, int CPS>
+__global__ void __launch_bounds__(kThreads, CPS) score_st_kernel(ScoreArgs a, int nacc, int chains) {
   constexpr int kNAB = NAB;
   constexpr uint32_t kColAcc = 64u * NAB;
   pdl_enter();
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_st_kernel(ScoreArgs a, int 
 }
 
 struct StCfg {
-  int na, nb, nab;
+  int na, nb, nab, cps;   // landing slots, table slots, TMEM A buffers, CTAs per SM
 };
 
 // ring depths: wide nodes (c2: 64 KB table chunks) get three table slots and a
@@ -525,11 +525,18 @@ struct StCfg {
 #endif
 // four A buffers leave room for a double-buffered accumulator up to npad 128;
 // narrow nodes (c4: 32-64 children) get NAB A buffers, as many as TMEM holds
+#ifndef STMP_ST_CPS_NARROW
+#define STMP_ST_CPS_NARROW 2
+#endif
+// narrow nodes (<= 64 children): two CTAs per SM, each with half the rings and
+// half of TMEM, so one CTA's epilogue / refills overlap the other's MMAs
 inline StCfg st_cfg(int npad) {
-  return npad > 128 ? StCfg{2, 3, 4} : (npad > 64 ? StCfg{4, 4, 4} : StCfg{6, 6, STMP_ST_NAB_NARROW});
+  if (npad > 128) return StCfg{2, 3, 4, 1};
+  if (npad > 64) return StCfg{4, 4, 4, 1};
+  return STMP_ST_CPS_NARROW == 2 ? StCfg{3, 3, 2, 2} : StCfg{6, 6, STMP_ST_NAB_NARROW, 1};
 }
 
-template <int NA, int NB, int NAB>
+template <int NA, int NB, int NAB, int CPS>
 cudaError_t launch_st(ScoreArgs s, int sms, cudaStream_t st) {
   constexpr uint32_t kColAcc = 64u * NAB;
   const bool last = s.leaf_sel != nullptr;
@@ -539,15 +546,17 @@ cudaError_t launch_st(ScoreArgs s, int sms, cudaStream_t st) {
 #define STMP_ST_CHAINS 2
 #endif
   // wide-N MMAs (two accumulator halves) and two accumulator buffers when TMEM holds them
-  const int chains = (int)kColAcc + 2 * 2 * accw <= 512 && s.npad % 32 == 0 ? STMP_ST_CHAINS : 1;
-  const int nacc = (int)kColAcc + 2 * chains * accw <= 512 ? 2 : 1;
+  constexpr int kCols = 512 / CPS;   // TMEM columns per CTA
+  const int chains = (int)kColAcc + 2 * accw <= kCols && s.npad % 32 == 0 ? STMP_ST_CHAINS : 1;
+  const int nacc = (int)kColAcc + 2 * chains * accw <= kCols ? 2 : 1;
   int cols = 32;
   while (cols < (int)kColAcc + nacc * chains * accw) cols <<= 1;
   s.tmem_cols = cols;
-  cudaError_t e = cudaFuncSetAttribute(score_st_kernel<NA, NB, NAB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(score_st_kernel<NA, NB, NAB, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_kernel(score_st_kernel<NA, NB, NAB>, sms, kThreads, (size_t)smem, st, true, s, nacc, chains);
+  return launch_kernel(score_st_kernel<NA, NB, NAB, CPS>, sms * CPS, kThreads, (size_t)smem, st, true, s, nacc,
+                       chains);
 }
 
 }  // namespace
@@ -561,9 +570,10 @@ bool score_st_fits(int kchunks, int npad, bool last) {
 cudaError_t launch_score_st(const ScoreArgs& s, int sms, cudaStream_t st) {
   if (!score_st_fits(s.kchunks, s.npad, s.leaf_sel != nullptr)) return cudaErrorNotSupported;
   const StCfg c = st_cfg(s.npad);
-  if (c.nb == 3) return launch_st<2, 3, 4>(s, sms, st);
-  if (c.nb == 4) return launch_st<4, 4, 4>(s, sms, st);
-  return launch_st<6, 6, STMP_ST_NAB_NARROW>(s, sms, st);
+  if (c.cps == 2) return launch_st<3, 3, 2, 2>(s, sms, st);
+  if (c.nb == 3) return launch_st<2, 3, 4, 1>(s, sms, st);
+  if (c.nb == 4) return launch_st<4, 4, 4, 1>(s, sms, st);
+  return launch_st<6, 6, STMP_ST_NAB_NARROW, 1>(s, sms, st);
 }
 
 }  // namespace stmp
