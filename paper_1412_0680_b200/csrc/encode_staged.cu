@@ -400,7 +400,7 @@ struct WsLayout {
       num_items, cursor2;
   // Gram path only
   bool gram = false;
-  size_t xn2 = 0, e_ws = 0, s0 = 0, bsel = 0;
+  size_t xn2 = 0, e_ws = 0, s0 = 0, bsel = 0, corr = 0;
 };
 
 WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method,
@@ -446,6 +446,7 @@ WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int 
     w.e_ws = add((size_t)N * 8);
     w.s0 = add((size_t)N * t->root_children * 4);
     w.bsel = add((size_t)N * 4);
+    w.corr = add((size_t)N * t->max_children * 4);
   }
   if (bin_off_out) *bin_off_out = bin_off;
   if (maxbins_out) *maxbins_out = maxbins;
@@ -570,6 +571,15 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
                                       counts_of(it + 1) + bin_off[l], cursor_of(it + 1) + bin_off[l], offsets,
                                       tile_off, cursor, perm, items, num_items, sms, st)) != cudaSuccess)
           return e;
+#ifndef STMP_GRAM_CORR_PRE
+#define STMP_GRAM_CORR_PRE 1
+#endif
+        float* corr_pre = STMP_GRAM_CORR_PRE && l > 0 && it > 0 ? (float*)(b + w.corr) : nullptr;
+        if (corr_pre != nullptr &&
+            (e = launch_gram_corr(N, active, path_ws, L, l, t->child_begin, t->child_count,
+                                  (int)t->level_offsets[l + 1], t->pair_tables[l], t->pair_width[l], S_ws, c_ws, K,
+                                  it, corr_pre, t->max_children, st)) != cudaSuccess)
+          return e;
         ScoreArgs s{};
         s.R = R0; s.ld = d->ld; s.nrows = N; s.perm = l == 0 ? nullptr : perm; s.items = items;
         s.num_items = num_items; s.active = active;
@@ -589,6 +599,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
         s.corr = t->pair_tables[l]; s.corr_w = t->pair_width[l]; s.corr_off = (int)t->level_offsets[l + 1];
         s.sup = S_ws; s.supc = c_ws; s.sup_t = it; s.sup_ld = K;
         s.cent = t->cent; s.xn2 = xn2; s.recheck_rel = 1e-5f;
+        s.corr_pre = corr_pre; s.corr_pre_ld = t->max_children;
         if (l == 0) { s.raw_out = s0; s.raw_w = t->root_children; }   // iteration 0: cache c_v . x of the root
         if ((e = launch_score_st(s, sms, st)) != cudaSuccess) return e;
       }

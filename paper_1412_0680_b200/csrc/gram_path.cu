@@ -296,6 +296,44 @@ __global__ void __launch_bounds__(256) update_gram_kernel(GramArgs a) {
     if (hist[i]) atomicAdd(&a.root_counts[i], hist[i]);
 }
 
+__global__ void __launch_bounds__(256) gram_corr_kernel(int64_t N, const int* active, const int* path_ws, int L,
+                                                        int level, const int* child_begin, const int* child_count,
+                                                        int col_off, const float* __restrict__ tab, int64_t tab_w,
+                                                        const int* S_ws, const float* c_ws, int K, int T,
+                                                        float* out, int ld) {
+  pdl_enter();
+  const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= N || !active[p]) return;
+  const int node = path_ws[p * L + level - 1];
+  const int cb = __ldg(child_begin + node), cc = __ldg(child_count + node);
+  const int Sk = lane < T ? S_ws[p * K + lane] : 0;
+  const float ck = lane < T ? c_ws[p * K + lane] : 0.f;
+  const float* base = tab + (cb - col_off);
+  for (int j0 = 0; j0 < cc; j0 += 32) {
+    const int j = j0 + lane;
+    float acc = 0.f;
+    for (int k = 0; k < T; ++k) {
+      const int s_k = __shfl_sync(kFull, Sk, k);
+      const float c_k = __shfl_sync(kFull, ck, k);
+      if (j < cc) acc = fmaf(c_k, __ldg(base + (int64_t)s_k * tab_w + j), acc);
+    }
+    if (j < cc) out[p * ld + j] = acc;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_gram_corr(int64_t N, const int* active, const int* path_ws, int L, int level,
+                             const int* child_begin, const int* child_count, int col_off, const float* tab,
+                             int64_t tab_w, const int* S_ws, const float* c_ws, int K, int T, float* out, int ld,
+                             cudaStream_t st) {
+  return launch_kernel(gram_corr_kernel, (unsigned)((N + 7) / 8), 256, 0, st, true, N, active, path_ws, L, level,
+                       child_begin, child_count, col_off, tab, tab_w, S_ws, c_ws, K, T, out, ld);
+}
+
+namespace {
+
 cublasHandle_t blas_handle() {
   static cublasHandle_t h = nullptr;
   static std::once_flag once;

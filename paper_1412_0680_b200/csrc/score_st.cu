@@ -144,7 +144,24 @@ __device__ __forceinline__ void corr_abs_argmax(uint32_t taddr, uint32_t off2, i
       for (int j = 0; j < 32; ++j)
         if (j < nc && c0 + j < a.raw_w) dst[j] = v[j];
     }
-    for (int k = 0; k < T; ++k) {
+    if (a.corr_pre != nullptr && T > 0) {   // one precomputed row (gram_corr_kernel)
+      const float* row = a.corr_pre + (int64_t)p * a.corr_pre_ld + c0;
+      if (nc == 32 && (a.corr_pre_ld & 3) == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 t4 = __ldg(reinterpret_cast<const float4*>(row) + q);
+          v[4 * q] -= t4.x;
+          v[4 * q + 1] -= t4.y;
+          v[4 * q + 2] -= t4.z;
+          v[4 * q + 3] -= t4.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nc) v[j] -= __ldg(row + j);
+      }
+    }
+    for (int k = 0; k < (a.corr_pre != nullptr ? 0 : T); ++k) {
       const int sk = __ldg(a.sup + (int64_t)p * a.sup_ld + k);
       const float ck = __ldg(a.supc + (int64_t)p * a.sup_ld + k);
       const float* row = a.corr + (int64_t)sk * a.corr_w + colbase + c0;
@@ -226,7 +243,9 @@ __device__ void recheck_near_ties(uint32_t taddr, uint32_t off2, int cc, int cb,
       }
       const int col = c0 + lane;
       float corr = 0.f;
-      if (col < cc)
+      if (col < cc && a.corr_pre != nullptr)
+        corr = a.sup_t > 0 ? __ldg(a.corr_pre + (int64_t)q * a.corr_pre_ld + col) : 0.f;
+      else if (col < cc)
         for (int k = 0; k < a.sup_t; ++k) {
           const int sk = __ldg(a.sup + (int64_t)q * a.sup_ld + k);
           corr = fmaf(__ldg(a.supc + (int64_t)q * a.sup_ld + k),

@@ -54,6 +54,10 @@ struct ScoreArgs {
   const float* cent;     // centroid rows [nodes][ld] (global ids)
   const double* xn2;     // ||x||^2 per patch
   float recheck_rel;
+  // corrections precomputed by gram_corr_kernel: [N][corr_pre_ld], column j =
+  // child j of the patch's node (nullptr: gathered from the pair table here)
+  const float* corr_pre;
+  int corr_pre_ld;
 };
 
 // Work items of a score pass: (bin, first slot in perm, rows) from the scan, or
@@ -157,6 +161,13 @@ bool gram_path_supported(const DictHandle* d, const TreeHandle* t, int K, int me
 // builds the pair tables on first use; false if they cannot be allocated
 bool ensure_pair_tables(TreeHandle* t, const DictHandle* d, cudaStream_t st);
 cudaError_t launch_update_gram(const GramArgs& a, cudaStream_t st);
+// sum_k c_k P_l[S_k][children of the patch's level-l node] for every active patch,
+// written to out[N][ld] before the level-l score pass (one warp per patch: the
+// support's pair-table rows are read coalesced, the epilogue then reads one row)
+cudaError_t launch_gram_corr(int64_t N, const int* active, const int* path_ws, int L, int level,
+                             const int* child_begin, const int* child_count, int col_off, const float* tab,
+                             int64_t tab_w, const int* S_ws, const float* c_ws, int K, int T, float* out, int ld,
+                             cudaStream_t st);
 // leaf_pos of a tree whose depth-L nodes are single atoms covering the dictionary
 bool build_leaf_pos(TreeHandle* t, int64_t m, cudaStream_t st);
 void free_pair_tables(TreeHandle* t);
