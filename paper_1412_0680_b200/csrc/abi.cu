@@ -36,7 +36,7 @@ int g_graphs = 1;             // replay repeated staged encodes as CUDA graphs
 // of small batches and of the chunked host-buffer path.
 struct GraphKey {
   const void* p[14];
-  int64_t v[13];
+  int64_t v[16];
 };
 struct GraphEntry {
   GraphKey key;
@@ -439,6 +439,11 @@ int stmp_set_option(const char* key, int64_t value) {
     stmp::g_gram_path = (int)value;
     return STMP_OK;
   }
+  if (strcmp(key, "incr_update") == 0) {
+    if (value < 0 || value > 1) return fail(STMP_EINVAL, "incr_update must be 0 or 1");
+    stmp::g_incr_update = (int)value;
+    return STMP_OK;
+  }
   if (strcmp(key, "staged_min_batch") == 0) {
     if (value < 1) return fail(STMP_EINVAL, "staged_min_batch must be positive");
     g_staged_min = value;
@@ -517,9 +522,9 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
     const void* ps[14] = {nullptr, nullptr, X, idx, coef, count, resnorm, path, ip, workspace, stream, nullptr,
                           nullptr, nullptr};
     for (int i = 0; i < 14; ++i) k.p[i] = ps[i];
-    const int64_t vs[13] = {N, ldx, K, method, (int64_t)workspace_bytes, stmp::g_root_direct, stmp::g_score_ws,
+    const int64_t vs[16] = {N, ldx, K, method, (int64_t)workspace_bytes, stmp::g_root_direct, stmp::g_score_ws,
                             stmp::g_update_omp8, (int64_t)d->generation, stmp::g_pdl,
-                            t ? (int64_t)t->generation : 0, 0, stmp::g_gram_path};
+                            t ? (int64_t)t->generation : 0, 0, stmp::g_gram_path, stmp::g_incr_update, 0, 0};
     memcpy(k.v, vs, sizeof(vs));
     memcpy(&k.v[11], &tol, sizeof(float));
     std::lock_guard<std::mutex> lock(g_graph_mu);
