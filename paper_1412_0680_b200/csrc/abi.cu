@@ -439,11 +439,6 @@ int stmp_set_option(const char* key, int64_t value) {
     stmp::g_gram_path = (int)value;
     return STMP_OK;
   }
-  if (strcmp(key, "incr_update") == 0) {
-    if (value < 0 || value > 1) return fail(STMP_EINVAL, "incr_update must be 0 or 1");
-    stmp::g_incr_update = (int)value;
-    return STMP_OK;
-  }
   if (strcmp(key, "staged_min_batch") == 0) {
     if (value < 1) return fail(STMP_EINVAL, "staged_min_batch must be positive");
     g_staged_min = value;
@@ -524,7 +519,7 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
     for (int i = 0; i < 14; ++i) k.p[i] = ps[i];
     const int64_t vs[16] = {N, ldx, K, method, (int64_t)workspace_bytes, stmp::g_root_direct, stmp::g_score_ws,
                             stmp::g_update_omp8, (int64_t)d->generation, stmp::g_pdl,
-                            t ? (int64_t)t->generation : 0, 0, stmp::g_gram_path, stmp::g_incr_update, 0, 0};
+                            t ? (int64_t)t->generation : 0, 0, stmp::g_gram_path, 0, 0, 0};
     memcpy(k.v, vs, sizeof(vs));
     memcpy(&k.v[11], &tol, sizeof(float));
     std::lock_guard<std::mutex> lock(g_graph_mu);

@@ -29,7 +29,6 @@ int g_pdl = 1;          // programmatic dependent launch between staged kernels
 int g_root_direct = 1;  // root pass over the batch in patch order (no scan / scatter at level 0)
 int g_update_omp8 = 1;  // 1: lockstep OMP update (update_omp8_kernel, encode_update.cu)
 int g_update_wide = 1;  // one-CTA-per-patch OMP update for rows wider than 160 floats
-int g_incr_update = 1;   // incremental lockstep OMP update on the atom Gram table where available
 int g_score_ws = 2;  // 2: A operand in TMEM, whole node table in shared memory (default); 3: streamed table
 
 namespace {
@@ -514,14 +513,6 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   u.root_count = stripes; u.N = N; u.S_ws = S_ws; u.c_ws = c_ws; u.leaf_sel = leaf_sel;
   // lockstep OMP update (update_omp8_kernel): K <= 8 with rows of <= 160 floats or K <= 16 with <= 64
   const bool lockstep = method == kMethodOMP && lockstep_lanes(d->ld, K) != 0 && g_update_omp8;
-  // incremental lockstep update on the atom Gram table (the last level's pair
-  // table) when the tree's depth-L nodes are single atoms and the tables fit
-  if (lockstep && !gram && t != nullptr && g_incr_update && t->leaf_pos != nullptr &&
-      ensure_pair_tables(const_cast<TreeHandle*>(t), d, st)) {
-    u.gram_tab = t->pair_tables[L - 1];
-    u.gram_w = t->pair_width[L - 1];
-    u.leaf_pos = t->leaf_pos;
-  }
   u.m = d->m;
   // stage the support atoms in shared memory when the patch groups fit comfortably
   u.cache_atoms = update_smem_bytes(uc, K, d->ld, true) <= 96 * 1024 ? 1 : 0;

@@ -568,13 +568,7 @@ __device__ __forceinline__ void group_reduce_scatter_n(float (&p)[NR * G], int g
 
 // Lane gl owns rows gl + G * i (i < NR) of the inverse Cholesky factor M (and the
 // matching y_j, c_j): NR = 1 while the support fits the group, 2 up to 2G atoms.
-// INCR: the incremental form.  The Gram column comes from the tree's last-level
-// pair table (= the atom Gram matrix in leaf order, gram_path.cu) instead of T
-// dot products with the support rows, and the residual is updated in place,
-//   r_new = r - y_T (A_S m_T + m_T[T] a)   (c_new - c_prev = y_T m_T),
-// so each support row is read once (not twice) and x is not read at all; the
-// right-hand side is b = a . x = a . r + sum_k c_k g_k.
-template <int G, int CPL, int T, bool INCR>
+template <int G, int CPL, int T>
 __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T < G ? STMP_OMP8_MINB : 5))
                                                 : STMP_OMP8_MINBW)
     update_omp8_kernel(UpdateArgs a) {
@@ -599,8 +593,7 @@ __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
     const int ch = gl + G * i;
-    const float* xrow = INCR ? a.R_in + pc * a.ld : a.X2 + pc * a.ld2;   // INCR: x holds r
-    const float4 q = ch < F ? sm100::ld_now(reinterpret_cast<const float4*>(xrow) + ch)
+    const float4 q = ch < F ? sm100::ld_now(reinterpret_cast<const float4*>(a.X2 + pc * a.ld2) + ch)
                             : make_float4(0.f, 0.f, 0.f, 0.f);
     x.v[4 * i] = q.x; x.v[4 * i + 1] = q.y; x.v[4 * i + 2] = q.z; x.v[4 * i + 3] = q.w;
   }
@@ -652,20 +645,7 @@ __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T
 #pragma unroll
   for (int k = 0; k < T; ++k) dup |= S[k] == atom;
   float gtt, bt;
-  if constexpr (INCR) {
-    // g_k from the Gram table (lane-redundant loads coalesce), a . a and a . r by reduction
-    const int pa = __ldg(a.leaf_pos + atom);
-#pragma unroll
-    for (int k = 0; k < T; ++k) g[k] = __ldg(a.gram_tab + (int64_t)S[k] * a.gram_w + pa);
-    float pv2[2] = {av.dot(av), av.dot(x)};
-#pragma unroll
-    for (int o = G >> 1; o; o >>= 1) {
-      pv2[0] += __shfl_xor_sync(kFull, pv2[0], o);
-      pv2[1] += __shfl_xor_sync(kFull, pv2[1], o);
-    }
-    gtt = pv2[0];
-    bt = pv2[1];   // a . r here; a . x once gc is known (below)
-  } else {
+  {
     // value k < T: a . a_{S_k};  T: a . a;  T + 1: a . x (if it fits)
     float pv[NV];
 #pragma unroll
@@ -711,7 +691,6 @@ __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T
     wsum += __shfl_xor_sync(kFull, wsum, o);
     wy += __shfl_xor_sync(kFull, wy, o);
   }
-  if constexpr (INCR) bt += gc;   // a . x = a . r + a . (A_S c_prev)
   const float score = bt - gc;   // a . r for r = x - A_S c_prev (pursuit.py:217 check)
   const bool ok = act && !dup && score != 0.f;   // re-selection or a zero score ends the loop
   const float dg = sqrtf(fmaxf(gtt + kRidge - wsum, 1e-30f));
@@ -743,11 +722,6 @@ __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T
   float c[T + 1];
 #pragma unroll
   for (int k = 0; k <= T; ++k) c[k] = group_bcast<G>(ok ? cn[k / G] : cj[k / G], k % G);
-  if constexpr (INCR) {
-    // in-place update: subtract y_T m_T (the coefficient change) from r (held in x)
-#pragma unroll
-    for (int k = 0; k <= T; ++k) c[k] = yy * group_bcast<G>(mt[k / G], k % G);
-  }
   if (__any_sync(kFull, ok)) {
     // residual r = x - A_S c (support rows from L1 / L2 / shared memory) - c_T a
     Sl r;
@@ -826,11 +800,9 @@ cudaError_t launch_update_omp8(const UpdateArgs& a, cudaStream_t st) {
   if (G == 0 || a.method != kMethodOMP || a.S_ws == nullptr) return cudaErrorNotSupported;
   const int blocks = (int)((a.N + (128 / G) - 1) / (128 / G));
   const int cpl = (a.ld / 4 + G - 1) / G;
-  const int incr = a.gram_tab != nullptr ? 1 : 0;
-  switch (((G * 8 + cpl) * 16 + a.iter) * 2 + incr) {
-#define STMP_OMP8_CASE(g, cp, t)                                                                             \
-  case ((g * 8 + cp) * 16 + t) * 2: return launch_kernel(update_omp8_kernel<g, cp, t, false>, blocks, 128, 0, st, true, a); \
-  case ((g * 8 + cp) * 16 + t) * 2 + 1: return launch_kernel(update_omp8_kernel<g, cp, t, true>, blocks, 128, 0, st, true, a);
+  switch ((G * 8 + cpl) * 16 + a.iter) {
+#define STMP_OMP8_CASE(g, cp, t) \
+  case (g * 8 + cp) * 16 + t: return launch_kernel(update_omp8_kernel<g, cp, t>, blocks, 128, 0, st, true, a);
 #define STMP_OMP8_ITERS(g, cp)                                                                          \
   STMP_OMP8_CASE(g, cp, 0) STMP_OMP8_CASE(g, cp, 1) STMP_OMP8_CASE(g, cp, 2) STMP_OMP8_CASE(g, cp, 3) \
   STMP_OMP8_CASE(g, cp, 4) STMP_OMP8_CASE(g, cp, 5) STMP_OMP8_CASE(g, cp, 6) STMP_OMP8_CASE(g, cp, 7)

@@ -116,11 +116,6 @@ struct UpdateArgs {
   int iter;              // iteration index = support size of every active patch
   double* xn2;           // Gram path: ||x||^2 per patch (init), and the running ||r||^2
   double* e_ws;
-  // incremental lockstep update: the last-level pair table (atom Gram matrix in
-  // leaf order) and leaf_pos; nullptr = Gram column by dot products
-  const float* gram_tab;
-  int64_t gram_w;
-  const int* leaf_pos;
 };
 
 // Gram path (gram_path.cu, OMP on trees whose depth-L nodes are single atoms):
@@ -177,7 +172,6 @@ cudaError_t launch_gram_corr(int64_t N, const int* active, const int* path_ws, i
 bool build_leaf_pos(TreeHandle* t, int64_t m, cudaStream_t st);
 void free_pair_tables(TreeHandle* t);
 extern int g_gram_path;   // 0 off, 1 auto (wide rows), 2 whenever supported
-extern int g_incr_update; // 1: incremental lockstep update on the pair table's Gram matrix when available
 
 struct UpdateCfg {
   int G = 0;   // lanes per patch
