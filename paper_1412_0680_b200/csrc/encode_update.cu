@@ -589,6 +589,7 @@ __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T
   // branch, which would add a dependent round trip)
   const int act_in = inb ? sm100::ld_now(a.active + pc) : 0;
   const int lsel = sm100::ld_now(a.leaf_sel + pc);
+  const float tol_p = sm100::ld_now(a.tol + pc);   // needed last: issued with the first loads
   Sl x;
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
@@ -746,7 +747,7 @@ __global__ void __launch_bounds__(128, CPL <= 2 ? (T == 0 ? STMP_OMP8_MINB0 : (T
     const float rn = sqrtf(gsum_full<G>(s2));
     if (ok) {
       r.store(a.R + p * a.ld, gl, F);
-      act_next = (T + 1 < K) && rn > a.tol[p];
+      act_next = (T + 1 < K) && rn > tol_p;
       if (act_next) {
 #pragma unroll
         for (int i = 0; i < NR; ++i) {
