@@ -119,6 +119,12 @@ def compare(gpu: dict, ref: dict, X: np.ndarray, check_ip: bool = True, check_pa
         if check_path and gpu.get("path") is not None and ref.get("path") is not None:
             gp = np.asarray(gpu["path"][p, :c])
             rp = np.asarray(ref["path"][p, :c])
+            bad = np.flatnonzero((gp != rp).any(axis=-1)) if gp.ndim > 1 else np.flatnonzero(gp != rp)
+            if bad.size and gaps is not None and gaps[p, bad[0]] < near_tie:
+                # the path (frontier[0]) can differ alone at a near tie of a beam boundary
+                rep.excused += 1
+                rep.excused_by_reason["near_tie"] += 1
+                continue
             if not np.array_equal(gp, rp):
                 rep.failures_by_kind["path"] += 1
                 rep.failures.append(f"patch {p}: path gpu {gp.tolist()} ref {rp.tolist()}")

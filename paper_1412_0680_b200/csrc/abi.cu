@@ -390,10 +390,17 @@ static bool beam_plan(const stmp_tree* t, double alpha, int* keep, int* max_fron
   return beam;
 }
 
+int g_staged_beam = 1;   // beam descent on the staged pipeline where supported (else the fused kernel)
+
 static bool use_staged(const stmp_dict* d, const stmp_tree* t, int64_t N, int32_t K, int32_t method,
                        double alpha = 0.0) {
   if (g_path_mode == 1 || d == nullptr) return false;
-  if (beam_plan(t, alpha, nullptr, nullptr)) return false;   // beam descent: the fused warp-per-patch kernel
+  int keep[stmp::kMaxBeamLevels] = {0};
+  if (beam_plan(t, alpha, keep, nullptr)) {   // beam descent: staged entries, or the fused kernel
+    if (!g_staged_beam || t->levels > stmp::kMaxBeamLevels || !stmp::staged_beam_supported(d, t, K, method, keep))
+      return false;
+    return g_path_mode == 2 || N >= g_staged_min;
+  }
   if (!stmp::staged_supported(d, t, K, method)) return false;
   // exhaustive selection: the tensor-core scan wins as soon as one tile fills an SM
   return g_path_mode == 2 || N >= (t == nullptr ? g_exact_min : g_staged_min);
@@ -439,6 +446,11 @@ int stmp_set_option(const char* key, int64_t value) {
     stmp::g_gram_path = (int)value;
     return STMP_OK;
   }
+  if (strcmp(key, "staged_beam") == 0) {
+    if (value < 0 || value > 1) return fail(STMP_EINVAL, "staged_beam must be 0 or 1");
+    g_staged_beam = (int)value;
+    return STMP_OK;
+  }
   if (strcmp(key, "staged_min_batch") == 0) {
     if (value < 1) return fail(STMP_EINVAL, "staged_min_batch must be positive");
     g_staged_min = value;
@@ -451,8 +463,11 @@ size_t stmp_encode_workspace(const stmp_dict* d, const stmp_tree* t, int64_t N, 
                              int32_t method, double alpha) {
   if (N <= 0 || d == nullptr) return 0;
   int mf = 0;
-  if (beam_plan(t, alpha, nullptr, &mf))
+  int keep[stmp::kMaxBeamLevels] = {0};
+  if (beam_plan(t, alpha, keep, &mf)) {
+    if (use_staged(d, t, N, K, method, alpha)) return stmp::staged_beam_workspace(d, t, N, K, method, keep);
     return (size_t)stmp::fused_warps(N) * (size_t)stmp::beam_scratch_ints(mf) * sizeof(int);
+  }
   if (!use_staged(d, t, N, K, method, alpha)) return 0;
   return stmp::staged_workspace_bytes(d, t, N, K, method);
 }
@@ -494,13 +509,20 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
   if (reinterpret_cast<uintptr_t>(ip) % 8 != 0)
     return fail(STMP_EINVAL, "ip must be 8-byte aligned (its two counters are updated as one 64-bit word)");
   if (use_staged(d, t, N, K, method, alpha)) {
-    const size_t need = stmp::staged_workspace_bytes(d, t, N, K, method);
+    int keep[stmp::kMaxBeamLevels] = {0};
+    int mf = 0;
+    const bool beam = beam_plan(t, alpha, keep, &mf);
+    const size_t need = beam ? stmp::staged_beam_workspace(d, t, N, K, method, keep)
+                             : stmp::staged_workspace_bytes(d, t, N, K, method);
     if (workspace == nullptr || workspace_bytes < need)
       return fail(STMP_EINVAL, "workspace of %zu bytes is below the required %zu (stmp_encode_workspace)",
                   workspace_bytes, need);
     const float tol = tol_abs < 0 ? -1.f : (float)tol_abs;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     auto run = [&] {
+      if (beam)
+        return stmp::run_staged_beam(d, t, X, N, ldx, K, method, tol, keep, mf, idx, coef, count, resnorm, path, ip,
+                                     workspace, workspace_bytes, st);
       return stmp::run_staged(d, t, X, N, ldx, K, method, tol, idx, coef, count, resnorm, path, ip, workspace,
                               workspace_bytes, st);
     };
@@ -519,9 +541,10 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
     for (int i = 0; i < 14; ++i) k.p[i] = ps[i];
     const int64_t vs[16] = {N, ldx, K, method, (int64_t)workspace_bytes, stmp::g_root_direct, stmp::g_score_ws,
                             stmp::g_update_omp8, (int64_t)d->generation, stmp::g_pdl,
-                            t ? (int64_t)t->generation : 0, 0, stmp::g_gram_path, 0, 0, 0};
+                            t ? (int64_t)t->generation : 0, 0, stmp::g_gram_path, 0, g_staged_beam, 0};
     memcpy(k.v, vs, sizeof(vs));
     memcpy(&k.v[11], &tol, sizeof(float));
+    memcpy(&k.v[13], &alpha, sizeof(double));   // beam: the kept children per level
     std::lock_guard<std::mutex> lock(g_graph_mu);
     GraphEntry* hit = nullptr;
     GraphEntry* lru = &g_graph_cache[0];

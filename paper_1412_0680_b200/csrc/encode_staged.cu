@@ -15,6 +15,8 @@
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -672,6 +674,248 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
         e = launch_score_ts(s, sms, st);
       if (e != cudaSuccess) return e;
     }
+    u.R_in = it == 0 ? R0 : R;
+    u.iter = it;
+    if (lockstep) e = launch_update_omp8(u, st);
+    else if (wide) e = launch_update_wide(u, st);
+    else e = launch_update(uc, u, ublocks, usmem, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+
+// ======================================================================================
+// Staged beam descent (non-greedy alpha, pursuit.py:134-162).
+//
+// The greedy pipeline keeps one node per patch per level; with retained_count
+// > 1 a patch owns a frontier of nodes.  Each level pass therefore scores
+// *entries* (patch, node): the entries are bucketed by node exactly like the
+// greedy pass buckets patches, every entry's row is its patch's residual, and
+// the epilogue keeps the `keep` best children (score_st.cu: beam_epilogue) as
+// the next level's entries -- or, at the last level, folds the survivors' leaf
+// atoms into one 64-bit max per patch.  Node tables are shared by all entries
+// of a node, so the tensor-core passes stay as they are; the work grows with
+// the frontier (c4 at alpha 0.1: 1 + 7 + 49 entries per patch per iteration).
+// ======================================================================================
+namespace {
+
+__global__ void __launch_bounds__(256) scatter_entries_kernel(const int* count, const int* node, int level_base,
+                                                              const int* offsets, int* cursor, int* perm) {
+  pdl_enter();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool act = e < *count;
+  const int bin = act ? node[e] - level_base : -1;
+  const unsigned peers = __match_any_sync(kFull, bin);
+  if (act) {
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&cursor[bin], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    perm[offsets[bin] + base + __popc(peers & ((1u << lane) - 1u))] = e;
+  }
+}
+
+// the patch's pick of the last beam level -> leaf_sel; the key is reset for the next iteration
+__global__ void __launch_bounds__(256) beam_resolve_kernel(int64_t N, const int* active,
+                                                           unsigned long long* key, int* leaf_sel) {
+  pdl_enter();
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= N) return;
+  if (active[p]) leaf_sel[p] = (int)(0xFFFFFFFFu - (unsigned)(key[p] & 0xFFFFFFFFull));
+  key[p] = 0ull;
+}
+
+struct BeamLayout {
+  size_t total = 0;
+  size_t R, Xpad, tol, active, path_ws, leaf_sel, Lf, yv, S_ws, c_ws, key, perm, items, num_items, offsets, tile_off,
+      cursor, counts, ecount, epatch[2], enode[2], efirst[2];
+  int64_t maxE = 0, maxbins = 1;
+  std::vector<int64_t> frontier;   // entries per patch bound, per level
+  std::vector<int64_t> bin_off;    // counts of level l at bin_off[l]
+};
+
+BeamLayout beam_layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method, const int* keep) {
+  BeamLayout w;
+  const int L = t->levels;
+  w.frontier.assign(L, 1);
+  w.bin_off.assign(L + 1, 0);
+  for (int l = 1; l < L; ++l) {
+    const int64_t nodes = t->level_offsets[l + 1] - t->level_offsets[l];
+    w.frontier[l] = std::min<int64_t>(w.frontier[l - 1] * std::min(keep[l - 1], t->max_children), nodes);
+  }
+  for (int l = 0; l < L; ++l) {
+    const int64_t nb = t->level_offsets[l + 1] - t->level_offsets[l];
+    w.maxbins = std::max(w.maxbins, nb);
+    w.bin_off[l + 1] = w.bin_off[l] + nb;
+    w.maxE = std::max(w.maxE, N * w.frontier[l]);
+  }
+  auto add = [&](size_t bytes) {
+    const size_t at = w.total;
+    w.total += (bytes + 255) & ~(size_t)255;
+    return at;
+  };
+  w.R = add((size_t)N * d->ld * 4);
+  w.Xpad = method == kMethodOMP ? add((size_t)N * d->ld * 4) : 0;
+  w.tol = add((size_t)N * 4);
+  w.active = add((size_t)N * 4);
+  w.path_ws = add((size_t)N * L * 4);
+  w.leaf_sel = add((size_t)N * 4);
+  w.Lf = add((size_t)N * K * (K + 1) / 2 * 4);
+  w.yv = add((size_t)N * K * 4);
+  w.S_ws = add((size_t)N * K * 4);
+  w.c_ws = add((size_t)N * K * 4);
+  w.key = add((size_t)N * 8);
+  w.perm = add((size_t)w.maxE * 4);
+  w.items = add((size_t)(w.maxE / kTile + w.maxbins + 2) * 16);
+  w.num_items = add(16);
+  w.offsets = add((size_t)(w.maxbins + 1) * 4);
+  w.tile_off = add((size_t)(w.maxbins + 1) * 4);
+  w.cursor = add((size_t)(w.maxbins + 1) * 4);
+  w.counts = add((size_t)(w.bin_off[L] + 1) * 4);
+  w.ecount = add(16);
+  for (int i = 0; i < 2; ++i) {
+    w.epatch[i] = add((size_t)w.maxE * 4);
+    w.enode[i] = add((size_t)w.maxE * 4);
+    w.efirst[i] = add((size_t)w.maxE);
+  }
+  return w;
+}
+
+}  // namespace
+
+bool staged_beam_supported(const DictHandle* d, const TreeHandle* t, int K, int method, const int* keep) {
+  if (t == nullptr || t->staged_tables.empty() || (method != kMethodMP && method != kMethodOMP) || K > 64) return false;
+  if (t->max_leaf_children != 1 || t->levels > kMaxBeamLevels) return false;   // single-atom leaves
+  UpdateCfg uc;
+  if (!update_config(d->ld, K, uc)) return false;
+  for (int l = 0; l < t->levels; ++l)
+    if (keep[l] > kMaxBeamKeep || !score_st_fits(d->ld / 32, t->staged_levels[l].npad, l + 1 == t->levels))
+      return false;
+  return true;
+}
+
+size_t staged_beam_workspace(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method,
+                             const int* keep) {
+  return beam_layout(d, t, N, K, method, keep).total;
+}
+
+static bool beam_debug() {
+  static const bool on = getenv("STMP_BEAM_DEBUG") != nullptr;
+  return on;
+}
+
+cudaError_t run_staged_beam(const DictHandle* d, const TreeHandle* t, const float* X, int64_t N, int64_t ldx, int K,
+                            int method, float tol_abs, const int* keep, int max_frontier, int32_t* idx, float* coef,
+                            int32_t* count, float* resnorm, int32_t* path, int32_t* ip, void* ws, size_t ws_bytes,
+                            cudaStream_t st) {
+  (void)max_frontier;
+  const BeamLayout w = beam_layout(d, t, N, K, method, keep);
+  if (ws == nullptr || ws_bytes < w.total) return cudaErrorInvalidValue;
+  const int L = t->levels;
+  uint8_t* b = static_cast<uint8_t*>(ws);
+  float* R = (float*)(b + w.R);
+  float* Xpad = method == kMethodOMP ? (float*)(b + w.Xpad) : nullptr;
+  int* active = (int*)(b + w.active);
+  int* leaf_sel = (int*)(b + w.leaf_sel);
+  int* perm = (int*)(b + w.perm);
+  int4* items = (int4*)(b + w.items);
+  int* num_items = (int*)(b + w.num_items);
+  int* offsets = (int*)(b + w.offsets);
+  int* tile_off = (int*)(b + w.tile_off);
+  int* cursor = (int*)(b + w.cursor);
+  int* counts = (int*)(b + w.counts);
+  int* ecount = (int*)(b + w.ecount);
+  unsigned long long* key = (unsigned long long*)(b + w.key);
+  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)(w.bin_off[L] + 1) * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(key, 0, (size_t)N * 8, st);
+  if (e != cudaSuccess) return e;
+
+  UpdateCfg uc;
+  update_config(d->ld, K, uc);
+  UpdateArgs u{};
+  u.X = X; u.ldx = ldx; u.n = d->n; u.R = R; u.ld = d->ld;
+  u.X2 = Xpad; u.ld2 = d->ld;
+  u.atoms = d->atoms; u.child_begin = t->child_begin; u.child_count = t->child_count;
+  u.leaf_atom = t->leaf_atom; u.L = L; u.path_ws = (int*)(b + w.path_ws); u.K = K; u.method = method;
+  u.tol_abs = tol_abs; u.idx = idx; u.coef = coef; u.count = count; u.resnorm = resnorm;
+  u.ip = ip; u.path_out = path; u.Lf = (float*)(b + w.Lf); u.yv = (float*)(b + w.yv); u.tol = (float*)(b + w.tol);
+  u.active = active; u.root_count = nullptr; u.N = N; u.S_ws = (int*)(b + w.S_ws); u.c_ws = (float*)(b + w.c_ws);
+  u.leaf_sel = leaf_sel; u.m = d->m;
+  u.cache_atoms = update_smem_bytes(uc, K, d->ld, true) <= 96 * 1024 ? 1 : 0;
+  const bool lockstep = method == kMethodOMP && lockstep_lanes(d->ld, K) != 0 && g_update_omp8;
+  const bool wide = method == kMethodOMP && !lockstep && g_update_wide && wide_update_cpt(d->ld) != 0;
+  const int gpb = 128 / uc.G;
+  const int ublocks = (int)((N + gpb - 1) / gpb);
+  const bool direct = ldx == d->ld && d->n == d->ld;
+  {
+    UpdateArgs ui = u;
+    if (direct) { ui.R = nullptr; ui.X2 = nullptr; }
+    if ((e = launch_init(uc, ui, ublocks, st)) != cudaSuccess) return e;
+  }
+  if (direct && method == kMethodOMP) u.X2 = X;
+  const float* R0 = direct ? X : R;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t usmem = update_smem_bytes(uc, K, d->ld, u.cache_atoms != 0);
+
+  for (int it = 0; it < K; ++it) {
+    int cur = 0;
+    for (int l = 0; l < L; ++l) {
+      const StagedLevel& lv = t->staged_levels[l];
+      const int nb = (int)(t->level_offsets[l + 1] - t->level_offsets[l]);
+      const bool lastl = l + 1 == L;
+      if (l > 0) {
+        // bucket the level's entries by node
+        e = launch_kernel(scan_kernel, 1, kScanThreads, scan_smem(nb), st, true, counts + w.bin_off[l], nb, offsets,
+                          items, num_items, tile_off, cursor, (int*)nullptr);
+        if (e == cudaSuccess)
+          e = launch_kernel(scatter_entries_kernel, (int)((N * w.frontier[l] + 255) / 256), 256, 0, st, true,
+                            (const int*)(ecount + cur), (const int*)(b + w.enode[cur]), (int)t->level_offsets[l],
+                            (const int*)offsets, cursor, perm);
+        if (e != cudaSuccess) return e;
+        if (beam_debug() && (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+          fprintf(stderr, "beam: scatter level %d it %d: %s\n", l, it, cudaGetErrorString(e));
+          return e;
+        }
+      }
+      if (!lastl && (e = cudaMemsetAsync(ecount + (1 - cur), 0, 4, st)) != cudaSuccess) return e;
+      ScoreArgs s{};
+      s.R = it == 0 ? R0 : R; s.ld = d->ld; s.nrows = N; s.perm = l == 0 ? nullptr : perm; s.items = items;
+      s.num_items = num_items; s.active = active;
+      s.table = t->staged_tables[l]; s.npad = lv.npad; s.kchunks = d->ld / 32; s.tmem_cols = lv.tmem_cols;
+      s.level = l; s.level_base = (int)t->level_offsets[l]; s.child_begin = t->child_begin;
+      s.child_count = t->child_count; s.path_ws = (int*)(b + w.path_ws); s.path_out = path; s.count = count;
+      s.K = K; s.L = L; s.ip = ip; s.leaf_atom = t->leaf_atom;
+      s.ks_last = (d->n - 32 * (s.kchunks - 1) + 7) / 8;
+      s.beam_keep = keep[l];
+      if (l > 0) {
+        s.entry_patch = (const int*)(b + w.epatch[cur]);
+        s.entry_first = (const uint8_t*)(b + w.efirst[cur]);
+      }
+      if (!lastl) {
+        s.out_patch = (int*)(b + w.epatch[1 - cur]);
+        s.out_node = (int*)(b + w.enode[1 - cur]);
+        s.out_first = (uint8_t*)(b + w.efirst[1 - cur]);
+        s.out_count = ecount + (1 - cur);
+        s.next_counts = counts + w.bin_off[l + 1];
+        s.next_base = (int)t->level_offsets[l + 1];
+      } else {
+        s.leaf_sel = leaf_sel;   // marks the last level (leaf records in the table block)
+        s.leaf_key = key;
+      }
+      if ((e = launch_score_st(s, sms, st)) != cudaSuccess) return e;
+      if (beam_debug() && (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+        fprintf(stderr, "beam: score level %d it %d: %s\n", l, it, cudaGetErrorString(e));
+        return e;
+      }
+      cur = 1 - cur;   // the next level's entries are in the buffer this pass filled
+    }
+    if ((e = launch_kernel(beam_resolve_kernel, (int)((N + 255) / 256), 256, 0, st, true, N, (const int*)active,
+                           key, leaf_sel)) != cudaSuccess)
+      return e;
     u.R_in = it == 0 ? R0 : R;
     u.iter = it;
     if (lockstep) e = launch_update_omp8(u, st);

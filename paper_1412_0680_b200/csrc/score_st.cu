@@ -272,6 +272,105 @@ __device__ void recheck_near_ties(uint32_t taddr, uint32_t off2, int cc, int cb,
   }
 }
 
+// Staged beam descent (pursuit.py:134-162), one entry (patch, node) per row,
+// all 32 lanes of an epilogue warp call it (TMEM reads are warp-collective).
+// Internal levels: the node's `keep` best children by |score| -- a stable sort
+// on -|score|, i.e. the largest keys (|score| bits << 32 | ~position) -- become
+// the next level's entries, in child order; the first survivor of the patch's
+// first entry continues the reference's path (frontier[0]).  Last level: the
+// survivors' leaf atoms are candidates; the top-1 child of every entry is a
+// survivor, so the patch's pick -- max |score|, ties to the lowest atom index
+// -- is one 64-bit atomicMax of (|score| bits << 32 | ~atom) per entry.
+__device__ void beam_epilogue(uint32_t taddr, uint32_t off2, int cc, int cb, const ScoreArgs& a, bool valid, int p,
+                              int e, bool last, const int* leaf_info, int* s_hist) {
+  const int lane = (int)(threadIdx.x & 31);
+  const int keep = a.beam_keep;
+  const int npick = keep < cc ? keep : cc;
+  const bool first = valid && (a.entry_first == nullptr || a.entry_first[e] != 0);
+  auto key_at = [](float v, unsigned id) {
+    return ((unsigned long long)__float_as_uint(fabsf(v)) << 32) | (unsigned long long)(0xFFFFFFFFu - id);
+  };
+  // top-npick children by position-tie-broken keys: each round takes the largest key below the previous one
+  int pick[kMaxBeamKeep];
+  unsigned long long prev = ~0ull;
+  for (int q = 0; q < kMaxBeamKeep; ++q) {
+    if (q >= npick) break;
+    unsigned long long bk = 0ull;
+    for (int c0 = 0; c0 < cc; c0 += 32) {
+      float v[32];
+      acc_ld32(taddr + (uint32_t)c0, off2, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c0 + j < cc) {
+          const unsigned long long k = key_at(v[j], (unsigned)(c0 + j));
+          if (k < prev && k > bk) bk = k;
+        }
+    }
+    prev = bk;
+    pick[q] = (int)(0xFFFFFFFFu - (unsigned)(bk & 0xFFFFFFFFull));
+  }
+  if (!last) {
+    // survivors in child order
+    for (int i = 1; i < npick; ++i) {
+      const int v = pick[i];
+      int j = i - 1;
+      while (j >= 0 && pick[j] > v) {
+        pick[j + 1] = pick[j];
+        --j;
+      }
+      pick[j + 1] = v;
+    }
+    const int n = valid ? npick : 0;
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    int base = 0;
+    if (lane == 31 && total > 0) base = atomicAdd(a.out_count, total);
+    base = __shfl_sync(kFull, base, 31) + incl - n;
+    for (int i = 0; i < n; ++i) {
+      a.out_patch[base + i] = p;
+      a.out_node[base + i] = cb + pick[i];
+      a.out_first[base + i] = (first && i == 0) ? 1 : 0;
+      atomicAdd(&s_hist[pick[i]], 1);
+    }
+    if (valid) {
+      if (first && a.path_out) a.path_out[((int64_t)p * a.K + a.count[p]) * a.L + a.level] = cb + pick[0];
+      if (a.ip) add_ip(a.ip, p, cc, cc);
+    }
+  } else if (valid) {
+    // the reference's path continues with the first survivor (in child order) of frontier[0]
+    int minpos = pick[0];
+    for (int i = 1; i < npick; ++i) minpos = pick[i] < minpos ? pick[i] : minpos;
+    if (first && a.path_out) a.path_out[((int64_t)p * a.K + a.count[p]) * a.L + a.level] = cb + minpos;
+    if (a.ip) add_ip(a.ip, p, cc + npick, cc);   // cc centroids + the survivors' single leaf atoms
+  }
+  if (last) {
+    // candidates: the survivors' leaf atoms (pursuit.py:155-162), max |score|,
+    // ties to the lowest atom index: one pass over the chunks (warp-collective)
+    unsigned long long best = 0ull;
+    for (int c0 = 0; c0 < cc; c0 += 32) {
+      float v[32];
+      acc_ld32(taddr + (uint32_t)c0, off2, v);
+      if (!valid) continue;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        bool surv = false;
+        for (int i = 0; i < kMaxBeamKeep; ++i) surv |= (i < npick && pick[i] == c0 + j);
+        if (c0 + j < cc && surv) {
+          const int atom = __ldg(leaf_info + c0 + j);
+          const unsigned long long k = key_at(v[j], (unsigned)atom);
+          best = k > best ? k : best;
+        }
+      }
+    }
+    if (valid) atomicMax(a.leaf_key + p, best);
+  }
+}
+
 template <int NA, int NB, int NAB, int CPS>
 __global__ void __launch_bounds__(kThreads, CPS) score_st_kernel(ScoreArgs a, int nacc, int chains) {
   constexpr int kNAB = NAB;
@@ -408,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, CPS) score_st_kernel(ScoreArgs a, in
       if (item != r_item) {
         r_item = item;
         const int4 it = item_at(a, item);
-        r_row = tid < it.z ? row_at(a, it, tid) : -1;
+        r_row = tid < it.z ? patch_of(a, row_at(a, it, tid)) : -1;
       }
       return r_row;
     };
@@ -472,7 +571,8 @@ __global__ void __launch_bounds__(kThreads, CPS) score_st_kernel(ScoreArgs a, in
     for (int seq = 0; seq < i1 - i0; ++seq) {
       const int4 it = item_at(a, i0 + seq);
       const int cur_bin = it.x, cur_rows = it.z;
-      const int cur_p = et < it.z ? row_at(a, it, et) : -1;
+      const int cur_e = et < it.z ? row_at(a, it, et) : -1;   // entry id (= patch id off the beam path)
+      const int cur_p = patch_of(a, cur_e);
       const int tid = et;
 
       const int acc = nacc == 2 ? (seq & 1) : 0;
@@ -485,6 +585,26 @@ __global__ void __launch_bounds__(kThreads, CPS) score_st_kernel(ScoreArgs a, in
       float bestv = -1.f, rawbest = 0.f;
       const bool valid = tid < cur_rows && cur_p >= 0;
       const int p = cur_p;
+      if (a.beam_keep > 0) {
+        beam_epilogue(tmem + lane_base + kColAcc + (uint32_t)acc * accs, off2, cc, cb, a, valid, p, cur_e, last,
+                      a.table == nullptr ? nullptr
+                                         : reinterpret_cast<const int*>(reinterpret_cast<const uint8_t*>(a.table) +
+                                                                        (size_t)cur_bin * tb +
+                                                                        (size_t)kch * chunk_bytes),
+                      s_hist);
+        tc_fence_before();
+        mbar_arrive(&accempty[acc]);
+        if (a.out_count != nullptr) {   // next level's bin counts
+          named_sync(1, kEpi);
+          for (int j = tid; j < cc; j += kEpi) {
+            const int h = s_hist[j];
+            if (h) atomicAdd(&a.next_counts[cb + j - a.next_base], h);
+            s_hist[j] = 0;
+          }
+          named_sync(1, kEpi);
+        }
+        continue;
+      }
       if (a.corr != nullptr || a.raw_out != nullptr) {
         // Gram path: rows are x; score = c . x - sum_k c_k P[S_k][child] (gram_path.cu)
         float second = -1.f;

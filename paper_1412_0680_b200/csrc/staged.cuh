@@ -58,7 +58,19 @@ struct ScoreArgs {
   // child j of the patch's node (nullptr: gathered from the pair table here)
   const float* corr_pre;
   int corr_pre_ld;
+
+  // ---- staged beam descent (run_staged_beam): the pass scores (patch, node)
+  // entries instead of patches; perm holds entry ids
+  int beam_keep;            // > 0: retained_count(alpha, k_level) children kept per entry
+  const int* entry_patch;   // entry -> patch (nullptr: rows are patches)
+  const uint8_t* entry_first;   // the entry is frontier[0] of its patch (the reference's path)
+  int* out_patch;           // internal levels: survivors appended as the next level's entries
+  int* out_node;
+  uint8_t* out_first;
+  int* out_count;
+  unsigned long long* leaf_key;   // last level: per patch max of (|score| << 32 | ~atom)
 };
+constexpr int kMaxBeamKeep = 16;   // staged beam: children kept per node (larger: warp-per-patch kernel)
 
 // Work items of a score pass: (bin, first slot in perm, rows) from the scan, or
 // -- the root pass over the whole batch in patch order, perm == nullptr -- the
@@ -75,6 +87,10 @@ __device__ __forceinline__ int row_at(const ScoreArgs& a, int4 it, int r) {
   if (a.perm) return a.perm[it.y + r];
   const int p = it.y + r;
   return a.active[p] ? p : -1;
+}
+// patch of a row id (an entry id on the staged beam path), -1 stays -1
+__device__ __forceinline__ int patch_of(const ScoreArgs& a, int id) {
+  return (a.entry_patch != nullptr && id >= 0) ? a.entry_patch[id] : id;
 }
 
 struct UpdateArgs {
@@ -219,6 +235,15 @@ cudaError_t launch_score_st(const ScoreArgs& s, int sms, cudaStream_t st);
 cudaError_t launch_score_ts(const ScoreArgs& s, int sms, cudaStream_t st);
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
 size_t staged_workspace_bytes(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method);
+// staged beam descent (non-greedy alpha, single-atom depth-L nodes, keep <= kMaxBeamKeep):
+// keep[l] children per node at level l, max_frontier = largest entries-per-patch count
+bool staged_beam_supported(const DictHandle* d, const TreeHandle* t, int K, int method, const int* keep);
+size_t staged_beam_workspace(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method,
+                             const int* keep);
+cudaError_t run_staged_beam(const DictHandle* d, const TreeHandle* t, const float* X, int64_t N, int64_t ldx, int K,
+                            int method, float tol_abs, const int* keep, int max_frontier, int32_t* idx, float* coef,
+                            int32_t* count, float* resnorm, int32_t* path, int32_t* ip, void* ws, size_t ws_bytes,
+                            cudaStream_t st);
 cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X, int64_t N,
                        int64_t ldx, int K, int method, float tol_abs, int32_t* idx, float* coef,
                        int32_t* count, float* resnorm, int32_t* path, int32_t* ip, void* ws,

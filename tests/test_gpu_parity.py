@@ -570,16 +570,20 @@ def test_beam_pursuit_matches_oracle(method):
     assert rep.excused <= 2
 
 
-@pytest.mark.parametrize("cid,rows,alpha", [(1, 1024, 0.1), (4, 48, 0.1)])
-def test_config_beam_parity(cid, rows, alpha):
+@pytest.mark.parametrize("path", ["fused", "staged-ts"], indirect=True)
+@pytest.mark.parametrize("cid,rows,alpha", [(1, 4096, 0.1), (4, 512, 0.1), (0, 4096, 0.2)])
+def test_config_beam_parity(cid, rows, alpha, path):
     """The paper's alpha = 0.1 setting on config trees: frontiers
-    of ceil(0.1 k) children per node (c1: 4, 16, 32 nodes; c4: 7, 49, 196)."""
+    of ceil(0.1 k) children per node (c1: 4, 16, 32 nodes; c4: 7, 49, 196), on the
+    warp-per-patch kernel and on the staged pipeline (node-bucketed entries)."""
     from paper_1412_0680_b200 import workloads as W
     from oracle import parallel as OP
     cfg, wl, flat = config(cid)
     X = W.make_patches(wl, rows)
     sel = P().TreeSelector(flat, wl.atoms, alpha)
-    out = run(sel, X, cfg.K, "omp")
+    out, names = launched(lambda: run(sel, X, cfg.K, "omp"))
+    staged = any("beam_resolve_kernel" in k for k in names)
+    assert staged == (path != "fused"), sorted(names)
     a64 = wl.atoms.astype(np.float64)
     ref = O.pack(OP.encode_parallel(O.OracleTree.from_flat(flat), a64, X, cfg.K, "omp", alpha=alpha), cfg.K)
     rep = compare(out, ref, X, check_path=True)
@@ -670,3 +674,25 @@ def test_graph_cache_never_replays_a_freed_tree():
     torch.cuda.synchronize()
     assert not torch.equal(a, b)
     assert torch.equal(b, fresh)
+
+
+@pytest.mark.parametrize("method", ["omp", "mp"])
+def test_staged_beam_equals_fused_beam(method):
+    """Staged beam descent and the warp-per-patch beam give the same codes
+    (decisions; coefficients to fp32 rounding) on 8192 config-1 patches."""
+    from paper_1412_0680_b200 import _lib
+    from paper_1412_0680_b200 import workloads as W
+    cfg, wl, flat = config(1)
+    X = W.make_patches(wl, 8192)
+    sel = P().TreeSelector(flat, wl.atoms, 0.1)
+    try:
+        _lib.set_option("path", _lib.PATH_FUSED)
+        a = run(sel, X, cfg.K, method)
+        _lib.set_option("path", _lib.PATH_STAGED)
+        b = run(sel, X, cfg.K, method)
+    finally:
+        restore_defaults(_lib)
+    same = (a["idx"] == b["idx"]).all(axis=1)
+    assert same.mean() > 0.999, same.mean()
+    np.testing.assert_array_equal(a["ip"][same], b["ip"][same])
+    np.testing.assert_allclose(a["coef"][same], b["coef"][same], rtol=1e-4, atol=1e-5)
