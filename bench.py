@@ -409,8 +409,11 @@ def main():
     timed_ms = sum(f["ms"] for f in fams.values()) or 1.0
     dom = max(fams, key=lambda f: fams[f]["ms"]) if fams else "other"
     gram = any("update_gram_kernel" in k for k in ktimes)
+    staged_beam = any("beam_resolve_kernel" in k for k in ktimes)
     if dom == "fused":
         work = RL.fused_work(cfg, N, alpha, args.method)
+    elif staged_beam:
+        work = RL.family_work(cfg, dom, N, args.method, exhaustive, alpha=alpha)
     elif gram:
         work = RL.gram_family_work(cfg, dom, N)
     else:

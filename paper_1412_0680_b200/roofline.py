@@ -76,7 +76,8 @@ def model(cfg, N: int | None = None, method: str = "omp", exhaustive: bool = Fal
 FAMILIES = (("score", ("score_ts_kernel", "score_st_kernel", "gram_corr_kernel")),
             ("exact_scan", ("exact_scan_kernel",)),
             ("update", ("update_omp8_kernel", "update_wide_kernel", "update_gram_kernel", "update_kernel")),
-            ("scatter", ("scatter_scan_kernel", "scatter_kernel", "scatter_root_kernel", "scan_kernel")),
+            ("scatter", ("scatter_scan_kernel", "scatter_kernel", "scatter_root_kernel", "scan_kernel",
+                         "scatter_entries_kernel", "beam_resolve_kernel")),
             ("init", ("init_kernel",)),
             ("fused", ("encode_fused_kernel",)))
 
@@ -162,7 +163,17 @@ def gram_model(cfg, N: int, hbm_gbs: float = 6548.2) -> dict:
                 patches_per_s_roof=hbm_gbs * 1e9 / B)
 
 
-def family_work(cfg, family: str, N: int, method: str = "omp", exhaustive: bool = False) -> dict:
+def beam_frontiers(branching, alpha: float) -> list:
+    """Entries (frontier nodes) per patch at each level of a beam descent."""
+    f, out = 1, []
+    for k in branching:
+        out.append(f)
+        f *= min(k, max(1, math.ceil(alpha * k - 1e-9)))
+    return out
+
+
+def family_work(cfg, family: str, N: int, method: str = "omp", exhaustive: bool = False,
+                alpha: float | None = None) -> dict:
     """Algorithmic work of one kernel family over a whole encode of N patches,
     assuming every patch runs all K iterations (the noisy BASELINE inputs never
     reach the 1e-6 tolerance early).  Returns {"bytes": B, "flops": F, "bound"}.
@@ -185,6 +196,10 @@ def family_work(cfg, family: str, N: int, method: str = "omp", exhaustive: bool 
     if family == "score":
         kids = [math.prod(cfg.branching[:d + 1]) for d in range(L)]
         tables = sum(4 * n * k for k in kids if 4 * n * k > L2_BYTES)
+        if alpha is not None:   # staged beam: one residual row per (patch, frontier node) entry
+            fr = beam_frontiers(cfg.branching, alpha)
+            return binding({"bytes": float(N * K * sum(fr) * (4 * n + 12) + K * tables),
+                            "flops": float(N * K * 2 * n * sum(f * k for f, k in zip(fr, cfg.branching)))})
         return binding({"bytes": float(N * K * L * (4 * n + 8) + K * tables),
                         "flops": float(N * K * 2 * n * sum(cfg.branching))})
     if family == "update":

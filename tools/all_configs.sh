@@ -11,8 +11,8 @@ run --config 2 --steps 5 --warmup 3
 run --config 3 --steps 10 --warmup 3
 run --config 4 --steps 5 --warmup 3
 run --config 4 --selector exact --steps 1 --warmup 3 --no-e2e
-run --config 1 --alpha 0.1 --patches 131072 --steps 3 --warmup 2 --no-e2e
-run --config 4 --alpha 0.1 --patches 8192 --steps 2 --warmup 2 --no-e2e
+run --config 1 --alpha 0.1 --steps 5 --warmup 2 --no-e2e
+run --config 4 --alpha 0.1 --steps 2 --warmup 2 --no-e2e
 python - <<'PY'
 import json
 for line in open("gpurun_out/configs.jsonl"):
