@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--kernel-detail", action="store_true",
+                    help="add per-kernel launch counts and times of the instrumented encode (sweeps)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile-run", action="store_true",
                     help="under ncu: only the warm-up and timed encodes (no e2e, CPU leg, peak GEMM or "
@@ -457,6 +459,9 @@ def main():
                  "launches": per_step, "model_patches_per_s": rm["patches_per_s_roof"],
                  "frac": rm["patches_per_s_roof"] and (N / (launch_ms / 1e3)) / rm["patches_per_s_roof"]},
     })
+    if args.kernel_detail:
+        roof["kernel_detail"] = {demangle(k)[:70]: [c, round(ms, 4)] for k, (c, ms) in
+                                 sorted(ktimes.items(), key=lambda kv: -kv[1][1])}
     traffic_file = os.path.join(ROOT, "profiles", f"r02_traffic_c{cfg.cid}.json")
     if os.path.exists(traffic_file):
         tr = json.load(open(traffic_file))

@@ -12,7 +12,8 @@ import os
 from .errors import StaleTreeError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libstmp_b200.so")
+# STMP_LIB_PATH: a kernel-variant build for sweeps (tools/variants.sh); unset normally
+LIB_PATH = os.environ.get("STMP_LIB_PATH") or os.path.join(HERE, "_lib", "libstmp_b200.so")
 
 STMP_OK, STMP_EINVAL, STMP_ESTALE, STMP_ECUDA = 0, 1, 2, 3
 METHOD_MP, METHOD_OMP, METHOD_SELECT = 0, 1, 2
