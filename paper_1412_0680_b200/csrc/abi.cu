@@ -446,6 +446,12 @@ int stmp_set_option(const char* key, int64_t value) {
     stmp::g_gram_path = (int)value;
     return STMP_OK;
   }
+  if (strcmp(key, "half_scores") == 0) {
+    if (value < 0 || value > 1)
+      return fail(STMP_EINVAL, "half_scores must be 0 (fp32 rows) or 1 (fp16 rows on the Gram path's level passes)");
+    stmp::g_half_scores = (int)value;
+    return STMP_OK;
+  }
   if (strcmp(key, "staged_beam") == 0) {
     if (value < 0 || value > 1) return fail(STMP_EINVAL, "staged_beam must be 0 or 1");
     g_staged_beam = (int)value;
@@ -541,7 +547,7 @@ int stmp_encode(const stmp_dict* d, const stmp_tree* t, const float* X, int64_t 
     for (int i = 0; i < 14; ++i) k.p[i] = ps[i];
     const int64_t vs[16] = {N, ldx, K, method, (int64_t)workspace_bytes, stmp::g_root_direct, stmp::g_score_ws,
                             stmp::g_update_omp8, (int64_t)d->generation, stmp::g_pdl,
-                            t ? (int64_t)t->generation : 0, 0, stmp::g_gram_path, 0, g_staged_beam, 0};
+                            t ? (int64_t)t->generation : 0, 0, stmp::g_gram_path, 0, g_staged_beam, stmp::g_half_scores};
     memcpy(k.v, vs, sizeof(vs));
     memcpy(&k.v[11], &tol, sizeof(float));
     memcpy(&k.v[13], &alpha, sizeof(double));   // beam: the kept children per level

@@ -137,6 +137,7 @@ struct TreeHandle {
   std::vector<int64_t> pair_width;
   int* leaf_pos = nullptr;
   bool pair_tried = false;
+  std::vector<uint8_t*> half_tables;   // per level >= 1: fp16 piece tables (score_sh.cu), built with the pair tables
 };
 
 // Device-side view passed to kernels by value.

@@ -403,6 +403,9 @@ struct WsLayout {
   // Gram path only
   bool gram = false;
   size_t xn2 = 0, e_ws = 0, s0 = 0, bsel = 0, corr = 0;
+  // half-precision rows of the Gram path's level passes (score_sh.cu)
+  bool half = false;
+  size_t x16 = 0, inv_scale = 0, qerr = 0;
 };
 
 WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method,
@@ -449,6 +452,14 @@ WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int 
     w.s0 = add((size_t)N * t->root_children * 4);
     w.bsel = add((size_t)N * 4);
     w.corr = add((size_t)N * t->max_children * 4);
+    // reserved whenever the shapes allow it (the option is read at encode time)
+    w.half = true;
+    for (int l = 1; l < L; ++l) w.half = w.half && score_sh_fits(d->ld, t->staged_levels[l].npad);
+    if (w.half) {
+      w.x16 = add((size_t)N * d->ld * 2);
+      w.inv_scale = add((size_t)N * 4);
+      w.qerr = add((size_t)N * 4);
+    }
   }
   if (bin_off_out) *bin_off_out = bin_off;
   if (maxbins_out) *maxbins_out = maxbins;
@@ -563,6 +574,12 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
     ga.Lf = Lf; ga.e_ws = e_ws; ga.xn2 = xn2; ga.tol = tol; ga.active = active; ga.idx = idx; ga.coef = coef;
     ga.count = count; ga.resnorm = resnorm; ga.ip = ip;
     ga.xr = R0; ga.atoms = d->atoms; ga.cent = t->cent; ga.ld = d->ld; ga.rho = 1e-2f; ga.recheck_rel = 1e-5f;
+    // level passes on fp16 rows (score_sh.cu) when the tree carries the fp16 piece tables
+    const bool half = w.half && g_half_scores != 0 && (int)t->half_tables.size() == L;
+    uint16_t* x16 = half ? (uint16_t*)(b + w.x16) : nullptr;
+    float* inv_scale = half ? (float*)(b + w.inv_scale) : nullptr;
+    float* qerr = half ? (float*)(b + w.qerr) : nullptr;
+    if (half && (e = launch_half_rows(R0, N, d->ld, x16, inv_scale, qerr, st)) != cudaSuccess) return e;
     for (int it = 0; it < K; ++it) {
       for (int l = it == 0 ? 0 : 1; l < L; ++l) {
         const StagedLevel& lv = t->staged_levels[l];
@@ -603,6 +620,15 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
         s.cent = t->cent; s.xn2 = xn2; s.recheck_rel = 1e-5f;
         s.corr_pre = corr_pre; s.corr_pre_ld = t->max_children;
         if (l == 0) { s.raw_out = s0; s.raw_w = t->root_children; }   // iteration 0: cache c_v . x of the root
+        if (half && l > 0) {
+          s.R16 = x16; s.table_h = t->half_tables[l]; s.inv_scale = inv_scale; s.qerr = qerr;
+          // window += 16 sigma of the rows' quantisation noise on a unit centroid's score (||e|| / sqrt(n))
+          s.recheck_q = 16.f / sqrtf((float)d->n);
+          s.kchunks = d->ld / 64;
+          s.ks_last = (d->n - 64 * (s.kchunks - 1) + 15) / 16;
+          if ((e = launch_score_sh(s, sms, st)) != cudaSuccess) return e;
+          continue;
+        }
         if ((e = launch_score_st(s, sms, st)) != cudaSuccess) return e;
       }
       ga.iter = it;

@@ -35,6 +35,8 @@
 
 namespace stmp {
 
+using namespace sm100;
+
 int g_gram_path = 1;
 
 namespace {
@@ -115,7 +117,7 @@ __device__ __forceinline__ float warp_sum_f(float v) {
 //     root scores s0, with the near-tie re-check (exact dots; the re-scored s0
 //     entries are written back).
 // Solver state is laid out per patch: S, c, y [N][K], M [N][K(K+1)/2].
-template <int T>
+template <int T, int kMaxPer>   // kMaxPer: root children per lane (root_w <= 32 kMaxPer)
 __global__ void __launch_bounds__(256) update_gram_kernel(GramArgs a) {
   pdl_enter();
   __shared__ int hist[256];
@@ -128,22 +130,33 @@ __global__ void __launch_bounds__(256) update_gram_kernel(GramArgs a) {
     const int K = a.K;
     const int64_t KM = (int64_t)K * (K + 1) / 2;
     const float* xr = a.xr + p * a.ld;
-    const int atom = a.leaf_sel[p];
-    const float b = warp_dot_rows(xr, a.atoms + (int64_t)atom * a.ld, a.ld);
-    const int pa = __ldg(a.leaf_pos + atom);
+    // every load that does not depend on the solve is issued before the dot, so
+    // the patch pays one memory round trip for its state instead of one per use
+    // (ld_now: the compiler may not sink them below the dot)
+    const int atom = ld_now(a.leaf_sel + p);
     int Sk = 0;
-    float ck = 0.f, yk = 0.f, gk = 0.f;
+    float ck = 0.f, yk = 0.f;
     if (lane < T) {
-      Sk = a.S_ws[p * K + lane];
-      ck = a.c_ws[p * K + lane];
-      yk = a.yv[p * K + lane];
-      gk = __ldg(a.gram + (int64_t)Sk * a.gram_w + pa);   // a . a_{S_k}
+      Sk = ld_now(a.S_ws + p * K + lane);
+      ck = ld_now(a.c_ws + p * K + lane);
+      yk = ld_now(a.yv + p * K + lane);
     }
-    const float gtt = __ldg(a.gram + (int64_t)atom * a.gram_w + pa);
-    const bool dup = __any_sync(kFull, lane < T && Sk == atom);
     float mrow[T + 1];
 #pragma unroll
-    for (int k = 0; k < T; ++k) mrow[k] = (lane < T && k <= lane) ? a.Lf[p * KM + lane * (lane + 1) / 2 + k] : 0.f;
+    for (int k = 0; k < T; ++k)
+      mrow[k] = (lane < T && k <= lane) ? ld_now(a.Lf + p * KM + lane * (lane + 1) / 2 + k) : 0.f;
+    const int pa = __ldg(a.leaf_pos + atom);
+    const float gk = lane < T ? ld_now(a.gram + (int64_t)Sk * a.gram_w + pa) : 0.f;   // a . a_{S_k}
+    const float gtt = ld_now(a.gram + (int64_t)atom * a.gram_w + pa);
+    const double e_prev = ld_now(a.e_ws + p), xn2 = ld_now(a.xn2 + p);
+    const float tolp = ld_now(a.tol + p);
+    float* s0 = a.s0 + p * a.root_w;
+    float s0v[kMaxPer];
+#pragma unroll
+    for (int q = 0; q < kMaxPer; ++q)
+      s0v[q] = (T + 1 < K && lane + 32 * q < a.root_w) ? ld_now(s0 + lane + 32 * q) : 0.f;
+    const float b = warp_dot_rows(xr, a.atoms + (int64_t)atom * a.ld, a.ld);
+    const bool dup = __any_sync(kFull, lane < T && Sk == atom);
     float w = 0.f;
 #pragma unroll
     for (int k = 0; k < T; ++k) w = fmaf(mrow[k], __shfl_sync(kFull, gk, k), w);
@@ -167,8 +180,7 @@ __global__ void __launch_bounds__(256) update_gram_kernel(GramArgs a) {
     const int Sn = lane < T ? Sk : (lane == T ? atom : 0);
     bool act_next = false;
     if (ok) {
-      double e = a.e_ws[p] - (double)yy * yy;
-      const double xn2 = a.xn2[p];
+      double e = e_prev - (double)yy * yy;
       if (e < (double)a.rho * xn2) {
         // cancellation: the explicit residual norm, lanes over the row
         double s2 = 0.0;
@@ -184,7 +196,7 @@ __global__ void __launch_bounds__(256) update_gram_kernel(GramArgs a) {
         e = s2;
       }
       const float rn = (float)sqrt(fmax(e, 0.0));
-      act_next = (T + 1 < K) && rn > a.tol[p];
+      act_next = (T + 1 < K) && rn > tolp;
       if (lane == 0) {
         a.count[p] = T + 1;
         a.resnorm[p] = rn;
@@ -213,9 +225,7 @@ __global__ void __launch_bounds__(256) update_gram_kernel(GramArgs a) {
     if (act_next) {
       // next iteration's root choice: s_j = (c_j . x) - sum_k c_k P_0[S_k][j],
       // first max of |s| in child order (pursuit.py:151)
-      constexpr int kMaxPer = 8;   // root_w <= 256
       float sv[kMaxPer], corr[kMaxPer];
-      float* s0 = a.s0 + p * a.root_w;
       float bestv = -1.f;
       int best = 0;
 #pragma unroll
@@ -231,7 +241,7 @@ __global__ void __launch_bounds__(256) update_gram_kernel(GramArgs a) {
             if (j < a.root_w) corr[q] = fmaf(c_k, __ldg(a.root_tab + (int64_t)s_k * a.root_w + j), corr[q]);
           }
           if (j < a.root_w) {
-            sv[q] = s0[j] - corr[q];
+            sv[q] = s0v[q] - corr[q];
             if (fabsf(sv[q]) > bestv) {
               bestv = fabsf(sv[q]);
               best = j;
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(256) update_gram_kernel(GramArgs a) {
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) second = fmaxf(second, __shfl_xor_sync(kFull, second, o));
-      const float delta = a.recheck_rel * (float)sqrt(a.xn2[p]);
+      const float delta = a.recheck_rel * (float)sqrt(xn2);
       if (bestv - second < delta) {
         // near tie: exact c_j . x for every child within 2 delta of the best
         const float lo = bestv - 2.f * delta;
@@ -310,6 +320,9 @@ __global__ void __launch_bounds__(256) gram_corr_kernel(int64_t N, const int* ac
   const int Sk = lane < T ? S_ws[p * K + lane] : 0;
   const float ck = lane < T ? c_ws[p * K + lane] : 0.f;
   const float* base = tab + (cb - col_off);
+  // (measured: batching the k loop for more loads in flight per lane is slower --
+  // 313 -> 437 us per launch at half the occupancy; the random 128/256-byte table
+  // rows, not the load latency, bound this kernel)
   for (int j0 = 0; j0 < cc; j0 += 32) {
     const int j = j0 + lane;
     float acc = 0.f;
@@ -418,6 +431,18 @@ bool ensure_pair_tables(TreeHandle* t, const DictHandle* d, cudaStream_t st) {
   }
   t->pair_tables = tabs;
   t->pair_width = width;
+  // fp16 piece tables of the levels >= 1 for the half-precision passes (score_sh.cu);
+  // without them (shape or memory) the passes stay on fp32 rows
+  bool fits = true;
+  for (int l = 1; l < L; ++l) fits = fits && score_sh_fits(t->ld, t->staged_levels[l].npad);
+  if (fits) {
+    std::vector<uint8_t*> ht(L, nullptr);
+    for (int l = 1; l < L && fits; ++l) fits = (ht[l] = build_half_table(t, l, st)) != nullptr;
+    if (fits)
+      t->half_tables = ht;
+    else
+      for (uint8_t* p : ht) cudaFree(p);
+  }
   return true;
 }
 
@@ -438,6 +463,8 @@ bool build_leaf_pos(TreeHandle* t, int64_t m, cudaStream_t st) {
 void free_pair_tables(TreeHandle* t) {
   for (float* p : t->pair_tables) cudaFree(p);
   t->pair_tables.clear();
+  for (uint8_t* p : t->half_tables) cudaFree(p);
+  t->half_tables.clear();
   cudaFree(t->leaf_pos);
   t->leaf_pos = nullptr;
 }
@@ -445,8 +472,10 @@ void free_pair_tables(TreeHandle* t) {
 cudaError_t launch_update_gram(const GramArgs& a, cudaStream_t st) {
   const unsigned blocks = (unsigned)((a.N + 7) / 8);
   switch (a.iter) {
-#define STMP_GRAM_CASE(t) \
-  case t: return launch_kernel(update_gram_kernel<t>, blocks, 256, 0, st, true, a);
+#define STMP_GRAM_CASE(t)                                                                    \
+  case t:                                                                                    \
+    return a.root_w <= 64 ? launch_kernel(update_gram_kernel<t, 2>, blocks, 256, 0, st, true, a) \
+                          : launch_kernel(update_gram_kernel<t, 8>, blocks, 256, 0, st, true, a);
     STMP_GRAM_CASE(0) STMP_GRAM_CASE(1) STMP_GRAM_CASE(2) STMP_GRAM_CASE(3) STMP_GRAM_CASE(4) STMP_GRAM_CASE(5)
     STMP_GRAM_CASE(6) STMP_GRAM_CASE(7) STMP_GRAM_CASE(8) STMP_GRAM_CASE(9) STMP_GRAM_CASE(10) STMP_GRAM_CASE(11)
     STMP_GRAM_CASE(12) STMP_GRAM_CASE(13) STMP_GRAM_CASE(14) STMP_GRAM_CASE(15)

@@ -26,6 +26,12 @@ __device__ __forceinline__ float ld_now(const float* p) {
   return v;
 }
 
+__device__ __forceinline__ double ld_now(const double* p) {
+  double v;
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ float4 ld_now(const float4* p) {
   float4 v;
   asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"

@@ -58,6 +58,13 @@ struct ScoreArgs {
   // child j of the patch's node (nullptr: gathered from the pair table here)
   const float* corr_pre;
   int corr_pre_ld;
+  // half-precision rows (score_sh.cu, Gram path levels >= 1): x16 = fp16(s_p x)
+  // with a power-of-two scale per patch, the node tables as three fp16 pieces
+  const uint16_t* R16;      // [N][ld] halfs
+  const uint8_t* table_h;   // per node: [ld / 64][2 pieces][npad rows x 128 B] SW128
+  const float* inv_scale;   // 1 / s_p
+  const float* qerr;        // ||x - x16 / s_p|| per patch
+  float recheck_q;          // near-tie window += recheck_q * qerr
 
   // ---- staged beam descent (run_staged_beam): the pass scores (patch, node)
   // entries instead of patches; perm holds entry ids
@@ -232,6 +239,18 @@ cudaError_t launch_exact_scan(const ScoreArgs& s, int sms, cudaStream_t st);
 // streamed-table score pass (score_st.cu): any K, npad <= 256
 bool score_st_fits(int kchunks, int npad, bool last);
 cudaError_t launch_score_st(const ScoreArgs& s, int sms, cudaStream_t st);
+// half-precision streamed pass of the Gram path (score_sh.cu): s.kchunks = ld / 64,
+// s.ks_last = 16-column k-steps holding data in the last chunk
+bool score_sh_fits(int ld, int npad);
+cudaError_t launch_score_sh(const ScoreArgs& s, int sms, cudaStream_t st);
+// bytes of one node's half-precision table block
+__host__ __device__ inline uint32_t table_h_bytes(int kch64, int npad) { return (uint32_t)kch64 * 2u * npad * 128u; }
+// x16 / inv_scale / qerr of every patch row (one warp per patch)
+cudaError_t launch_half_rows(const float* X, int64_t N, int ld, uint16_t* x16, float* inv_scale, float* qerr,
+                             cudaStream_t st);
+// per-node fp16 piece tables of level l (nullptr on allocation failure)
+uint8_t* build_half_table(const TreeHandle* t, int l, cudaStream_t st);
+extern int g_half_scores;   // 1: Gram-path level passes read fp16 rows (default), 0: fp32 rows / 3xTF32
 cudaError_t launch_score_ts(const ScoreArgs& s, int sms, cudaStream_t st);
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method);
 size_t staged_workspace_bytes(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int method);
