@@ -451,7 +451,7 @@ WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int 
     w.e_ws = add((size_t)N * 8);
     w.s0 = add((size_t)N * t->root_children * 4);
     w.bsel = add((size_t)N * 4);
-    w.corr = add((size_t)N * t->max_children * 4);
+    w.corr = add((size_t)N * ((t->max_children + 3) & ~3) * 4);   // rows of whole float4
     // reserved whenever the shapes allow it (the option is read at encode time)
     w.half = true;
     for (int l = 1; l < L; ++l) w.half = w.half && score_sh_fits(d->ld, t->staged_levels[l].npad);
@@ -597,7 +597,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
         if (corr_pre != nullptr &&
             (e = launch_gram_corr(N, active, path_ws, L, l, t->child_begin, t->child_count,
                                   (int)t->level_offsets[l + 1], t->pair_tables[l], t->pair_width[l], S_ws, c_ws, K,
-                                  it, corr_pre, t->max_children, st)) != cudaSuccess)
+                                  it, corr_pre, (t->max_children + 3) & ~3, st)) != cudaSuccess)
           return e;
         ScoreArgs s{};
         s.R = R0; s.ld = d->ld; s.nrows = N; s.perm = l == 0 ? nullptr : perm; s.items = items;
@@ -618,7 +618,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
         s.corr = t->pair_tables[l]; s.corr_w = t->pair_width[l]; s.corr_off = (int)t->level_offsets[l + 1];
         s.sup = S_ws; s.supc = c_ws; s.sup_t = it; s.sup_ld = K;
         s.cent = t->cent; s.xn2 = xn2; s.recheck_rel = 1e-5f;
-        s.corr_pre = corr_pre; s.corr_pre_ld = t->max_children;
+        s.corr_pre = corr_pre; s.corr_pre_ld = (t->max_children + 3) & ~3;
         if (l == 0) { s.raw_out = s0; s.raw_w = t->root_children; }   // iteration 0: cache c_v . x of the root
         if (half && l > 0) {
           s.R16 = x16; s.table_h = t->half_tables[l]; s.inv_scale = inv_scale; s.qerr = qerr;

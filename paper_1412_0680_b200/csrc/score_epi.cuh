@@ -45,6 +45,15 @@ __device__ __forceinline__ void acc_ld32h(uint32_t taddr, uint32_t off2, float s
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = scale * fmaf(kPieceStep, v[j], w[j]);
 }
+// the same for 16 columns (two pieces): the epilogue of score_sh works in 16-column
+// steps to stay inside its register budget
+__device__ __forceinline__ void acc_ld16h(uint32_t taddr, uint32_t off2, float scale, float (&v)[16]) {
+  float w[16];
+  tmem_ld16(taddr + off2, v);
+  tmem_ld16(taddr, w);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = scale * fmaf(kPieceStep, v[j], w[j]);
+}
 // rows of either kind: `scale` > 0 selects the three-piece half-precision read-back
 __device__ __forceinline__ void acc_ld32x(uint32_t taddr, uint32_t off2, float scale, float (&v)[32]) {
   if (scale > 0.f)
@@ -136,12 +145,29 @@ __device__ __forceinline__ float warp_dot(const float* __restrict__ x, const flo
   float s = 0.f;
   const float4* x4 = reinterpret_cast<const float4*>(x);
   const float4* c4 = reinterpret_cast<const float4*>(c);
-  for (int i = (int)(threadIdx.x & 31); i < ld / 4; i += 32) {
-    const float4 u = __ldg(x4 + i), v = __ldg(c4 + i);
-    s = fmaf(u.x, v.x, s);
-    s = fmaf(u.y, v.y, s);
-    s = fmaf(u.z, v.z, s);
-    s = fmaf(u.w, v.w, s);
+  // four float4 of each row in flight per lane (a serial loop pays one memory
+  // round trip per 128 columns: ~13 us for a 1600-float row, which made the
+  // re-checks the bottleneck of the whole pass); per-lane summation order is the
+  // plain loop's, so the result is bit-identical
+  const int nq = ld / 4;
+  int i = (int)(threadIdx.x & 31);
+  for (; i < nq; i += 4 * 32) {
+    float4 u[4], v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool on = i + 32 * q < nq;
+      u[q] = on ? __ldg(x4 + i + 32 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[q] = on ? __ldg(c4 + i + 32 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (i + 32 * q < nq) {
+        s = fmaf(u[q].x, v[q].x, s);
+        s = fmaf(u[q].y, v[q].y, s);
+        s = fmaf(u[q].z, v[q].z, s);
+        s = fmaf(u[q].w, v[q].w, s);
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);

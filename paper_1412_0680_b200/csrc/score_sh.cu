@@ -26,6 +26,7 @@
 // Semantics: pkg/src/stmp/pursuit.py:134-162 (greedy level choice, first max of
 // |score| in child order; leaf metadata for the last level).
 #include <cuda_fp16.h>
+#include <stdio.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -85,6 +86,13 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_
       : "memory");
 }
 
+#ifndef STMP_SH_FENCE
+#define STMP_SH_FENCE 1
+#endif
+#ifndef STMP_SH_SKIP   // timing experiments only: 1 = no MMAs, 2 = no row gather, 4 = no table copies
+#define STMP_SH_SKIP 0
+#endif
+
 template <int NA, int NB, int CPS>
 __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, int nacc) {
   pdl_enter();
@@ -107,6 +115,10 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
   uint64_t* accfull = aempty + NA;     // [2] accumulator complete (commit)
   uint64_t* accempty = accfull + 2;    // [2] accumulator read back by the 128 epilogue threads
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + Ly.slot);
+  // this CTA's work items, read once: every role looks its tiles up here instead
+  // of paying a global round trip at each tile boundary
+  constexpr int kItemCache = 48;
+  __shared__ int4 s_items[kItemCache];
 
   if (warp == 0) tmem_alloc(tmem_slot, a.tmem_cols);
   if (tid == 0) {
@@ -129,12 +141,26 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#ifdef STMP_SH_TRACE   // timing experiments only: event times of CTA 0's first 64 chunks
+  __shared__ long long tr[5][64];
+  __shared__ long long trt[8][32];
+  __shared__ int trn[32];
+  const long long tr_t0 = clock64();
+#define SH_TR(k, g) if (blockIdx.x == 0 && (g) < 64) tr[k][g] = clock64()
+#define SH_TRT(k, seq) if ((seq) < 32) trt[k][seq] = clock64() - tr_t0
+#else
+#define SH_TR(k, g)
+#define SH_TRT(k, seq)
+#endif
 
   const int num_items = item_count(a);
   const int per = (num_items + gridDim.x - 1) / gridDim.x;
   const int i0 = blockIdx.x * per;
   const int i1 = min(num_items, i0 + per);
   const int total = i1 > i0 ? (i1 - i0) * kch : 0;   // chunks of this CTA
+  for (int i = tid; i < min(i1 - i0, kItemCache); i += kThreads) s_items[i] = item_at(a, i0 + i);
+  __syncthreads();
+  auto item_of = [&](int seq) { return seq < kItemCache ? s_items[seq] : item_at(a, i0 + seq); };
   const uint32_t tb = table_h_bytes(kch, npad);
   const uint32_t chunk_bytes = (uint32_t)npad * 128u * kPieces;
   const uint32_t accw = (uint32_t)(npad + 31) / 32 * 32;   // columns per piece group (npad % 32 == 0)
@@ -147,9 +173,13 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
       int bin = 0;
       for (int g = 0; g < total; ++g) {
         const int seq = g / kch, c = g - seq * kch;
-        if (c == 0) bin = item_at(a, i0 + seq).x;
+        if (c == 0) bin = item_of(seq).x;
         const int s = g % NB;
         if (g >= NB) mbar_wait(&done[s], (uint32_t)(g / NB - 1) & 1u);
+        if (STMP_SH_SKIP & 4) {
+          mbar_arrive(&full[s]);
+          continue;
+        }
         mbar_arrive_expect_tx(&full[s], chunk_bytes);
         bulk_g2s_hint(base + Ly.btab + s * bslot, a.table_h + (size_t)bin * tb + (size_t)c * chunk_bytes, chunk_bytes,
                       &full[s], tab_policy);
@@ -158,75 +188,112 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
   } else if (warp == 4) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
+      // one thread issues everything, so its instruction count per chunk is the
+      // pipeline's clock: running counters instead of divisions, operand
+      // descriptors advanced by adds (the address field counts 16-byte units)
       const uint32_t idesc = idesc_f16(kT, kPieces * npad);
-      const uint32_t a_s = smem_u32(base + Ly.land);
-      const uint32_t b_s = smem_u32(base + Ly.btab);
+      const uint64_t adesc0 = sw128_kmajor_desc(smem_u32(base + Ly.land));
+      const uint64_t bdesc0 = sw128_kmajor_desc(smem_u32(base + Ly.btab));
+      const int ks_last = a.ks_last;
+      int seq = 0, c = 0, sa = 0, s = 0;
+      uint32_t pa = 0, pb = 0;   // phase parities of the row / table rings
       for (int g = 0; g < total; ++g) {
-        const int seq = g / kch, c = g - seq * kch;
-        const int sa = g % NA, s = g % NB;
         const int acc = nacc == 2 ? (seq & 1) : 0;
         const uint32_t dcol = tmem + (uint32_t)acc * accs;
+        if (c == 0) { SH_TRT(0, seq); }
         if (c == 0 && seq >= nacc) mbar_wait(&accempty[acc], (uint32_t)(seq / nacc - 1) & 1u);
-        mbar_wait(&astaged[sa], (uint32_t)(g / NA) & 1u);
-        mbar_wait(&full[s], (uint32_t)(g / NB) & 1u);
+        if (c == 0) { SH_TRT(1, seq); }
+        mbar_wait(&astaged[sa], pa);
+        SH_TR(2, g);
+        mbar_wait(&full[s], pb);
+        SH_TR(3, g);
+        if (STMP_SH_FENCE == 2) fence_proxy_async_smem();
         tc_fence_after();
-        const uint32_t ah = a_s + (uint32_t)sa * kSlot;
-        const uint32_t bh = b_s + (uint32_t)s * bslot;
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          if (c == kch - 1 && ks >= a.ks_last) break;   // zero padding on both operands
-          mma_f16(dcol, sw128_kmajor_desc(ah + ks * 32u), sw128_kmajor_desc(bh + ks * 32u), idesc,
-                  (c | ks) ? 1u : 0u);
+        const uint64_t ad = adesc0 + (uint64_t)((uint32_t)sa * (kSlot >> 4));
+        const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)s * (bslot >> 4));
+        const int nks = c == kch - 1 ? ks_last : 4;   // the rest is zero padding on both operands
+        if (!(STMP_SH_SKIP & 1)) {
+          mma_f16(dcol, ad, bd, idesc, c ? 1u : 0u);
+          if (nks > 1) mma_f16(dcol, ad + 2, bd + 2, idesc, 1u);
+          if (nks > 2) mma_f16(dcol, ad + 4, bd + 4, idesc, 1u);
+          if (nks > 3) mma_f16(dcol, ad + 6, bd + 6, idesc, 1u);
         }
         mma_commit(&done[s]);
         mma_commit(&aempty[sa]);
         if (c == kch - 1) mma_commit(&accfull[acc]);
+        SH_TR(4, g);
+        if (++c == kch) { c = 0; ++seq; }
+        if (++sa == NA) { sa = 0; pa ^= 1u; }
+        if (++s == NB) { s = 0; pb ^= 1u; }
       }
     }
   } else if (warp < 4) {
     // ------------------------------------------------ row gather (warps 0-3)
     const uint32_t land_s = smem_u32(base + Ly.land);
     const uint64_t row_policy = l2_policy_evict_first();
-    int r_item = -1, r_row = -1;
-    auto row_of = [&](int item) {
-      if (item != r_item) {
-        r_item = item;
-        const int4 it = item_at(a, item);
-        r_row = tid < it.z ? patch_of(a, row_at(a, it, tid)) : -1;
-      }
-      return r_row;
+    // row id of this thread in tile `seq`; the next tile's is fetched one tile ahead
+    auto row_fetch = [&](int seq) {
+      if (i0 + seq >= i1) return -1;
+      const int4 it = item_of(seq);
+      return tid < it.z ? patch_of(a, row_at(a, it, tid)) : -1;
     };
+    int r_next = row_fetch(0);
     // chunk g of this warp's 32 rows -> landing slot g % NA: lanes 8q..8q+7 copy the
-    // 128-byte chunk (64 halfs) of row 4i+q, four whole lines per instruction
-    auto issue_a = [&](int g) {
-      if (g < total) {
-        const int seq = g / kch, c = g - seq * kch;
-        const int rmine = row_of(i0 + seq);
-        const uint32_t dst = land_s + (uint32_t)(g % NA) * kSlot;
-        const int q = lane >> 3, j = lane & 7;
+    // 128-byte chunk (64 halfs) of row 4i+q, four whole lines per instruction; the
+    // eight source pointers of a lane are set up once per tile
+    const int q = lane >> 3, j = lane & 7;
+    const uint16_t* rp[8];
+    int rp_seq = -1;
+    // chunks are issued in order: running (tile, chunk, slot) counters
+    int ig = 0, iseq = 0, ic = 0, islot = 0;
+    auto issue_next = [&]() {
+      if (ig < total) {
+        if (iseq != rp_seq) {
+          rp_seq = iseq;
+          const int rmine = r_next;
+          r_next = row_fetch(iseq + 1);   // in flight during this tile's chunks
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int rl = 4 * i + q;   // row within the warp
-          const int r = __shfl_sync(kFull, rmine, rl);
-          const uint16_t* src = a.R16 + (r >= 0 ? (int64_t)r * a.ld + 64 * c + 8 * j : 0);
-          cp_async16_hint(dst + sw128_offset((uint32_t)(warp * 32 + rl), (uint32_t)j), src, r >= 0 ? 16u : 0u,
-                          row_policy);
+          for (int i = 0; i < 8; ++i) {
+            const int r = __shfl_sync(kFull, rmine, 4 * i + q);
+            rp[i] = r >= 0 ? a.R16 + (int64_t)r * a.ld + 8 * j : nullptr;
+          }
         }
+        const uint32_t dst = land_s + (uint32_t)islot * kSlot;
+#pragma unroll
+        for (int i = 0; i < ((STMP_SH_SKIP & 2) ? 0 : 8); ++i)
+          cp_async16_hint(dst + sw128_offset((uint32_t)(warp * 32 + 4 * i + q), (uint32_t)j),
+                          rp[i] ? rp[i] + 64 * ic : a.R16, rp[i] ? 16u : 0u, row_policy);
+        ++ig;
+        if (++ic == kch) { ic = 0; ++iseq; }
+        if (++islot == NA) islot = 0;
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    for (int g = 0; g < NA; ++g) issue_a(g);
+    // Iteration g hands chunk g to the MMA warp first and only then refills the
+    // slot of chunk g - 1 (whose MMAs were issued a whole iteration ago), so the
+    // copy instructions of one chunk overlap the MMA issue of the next instead of
+    // alternating with it (measured: the two took ~800 + ~700 cycles in turn).
+    // Groups: chunks 0 .. NA-1 up front, then one per iteration from g = 1 on, so
+    // NA - 2 groups follow chunk g's.
+    for (int g = 0; g < NA; ++g) issue_next();
+    int sa = 0, sp = NA - 1;   // slot of chunk g, slot of chunk g - 1
+    uint32_t pp = 0;           // parity of chunk g - 1's use of its slot
     for (int g = 0; g < total; ++g) {
-      const int sa = g % NA;
-      asm volatile("cp.async.wait_group %0;" ::"n"(NA - 1) : "memory");
-      fence_proxy_async_smem();   // the tensor core reads the slot through the async proxy
+      asm volatile("cp.async.wait_group %0;" ::"n"(NA - 2) : "memory");
+      if (tid == 0) { SH_TR(0, g); }
+      if (STMP_SH_FENCE == 1) fence_proxy_async_smem();   // the tensor core reads the slot through the async proxy
       mbar_arrive(&astaged[sa]);
-      // the slot is refilled with chunk g + NA once the MMAs of chunk g retire
-      if (g + NA < total) {
-        mbar_wait(&aempty[sa], (uint32_t)(g / NA) & 1u);
-        __syncwarp();
+      if (g >= 1) {
+        if (ig < total) {
+          mbar_wait(&aempty[sp], pp);
+          if (tid == 0) { SH_TR(1, g); }
+          __syncwarp();
+        }
+        issue_next();
       }
-      issue_a(g + NA);
+      sp = sa;
+      if (g >= 1 && sp == 0) pp ^= 1u;   // chunk g - 1 wrapped to slot 0: next pass over the ring
+      if (++sa == NA) sa = 0;
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else {
@@ -234,24 +301,142 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
     const int et = (warp & 3) * 32 + lane;          // tile row = TMEM lane
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     for (int seq = 0; seq < i1 - i0; ++seq) {
-      const int4 it = item_at(a, i0 + seq);
+      const int4 it = item_of(seq);
       const int cur_bin = it.x, cur_rows = it.z;
       const int p = et < it.z ? patch_of(a, row_at(a, it, et)) : -1;
       const int acc = nacc == 2 ? (seq & 1) : 0;
-      mbar_wait(&accfull[acc], (uint32_t)(seq / nacc) & 1u);
-      tc_fence_after();
       const int gnode = a.level_base + cur_bin;
       const int cb = __ldg(a.child_begin + gnode);
       const int cc = __ldg(a.child_count + gnode);
+      const bool valid = et < cur_rows && p >= 0;
+      // Everything the row needs from global memory is requested before the wait
+      // for the tile's MMAs (under the row stream a round trip costs thousands of
+      // cycles, and the epilogue of a tile must fit into the next tile's MMAs):
+      // 1 / s_p, the near-tie window, and the first 32 columns of the correction row.
+      const bool has_corr = a.corr_pre != nullptr && a.sup_t > 0;
+      const float4* crow = reinterpret_cast<const float4*>(a.corr_pre + (int64_t)(valid ? p : 0) * a.corr_pre_ld);
+      float4 cr[4];   // corrections of the 16 columns at hand
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4)
+        cr[q4] = has_corr && valid && 4 * q4 < cc ? ld_now(crow + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float scale = valid ? ld_now(a.inv_scale + p) : 1.f;   // > 0 on every lane: the read-back is warp-collective
+      const float delta =
+          valid ? a.recheck_rel * (float)sqrt(ld_now(a.xn2 + p)) + a.recheck_q * ld_now(a.qerr + p) : 0.f;
+      mbar_wait_backoff(&accfull[acc], (uint32_t)(seq / nacc) & 1u);   // a tile's MMAs take tens of microseconds
+      if (et == 0) { SH_TRT(3, seq); }
+      tc_fence_after();
+      const uint32_t taddr = tmem + lane_base + (uint32_t)acc * accs;
       int best = 0;
       float bestv = -1.f, rawbest = 0.f, second = -1.f;
-      const bool valid = et < cur_rows && p >= 0;
-      const float scale = valid ? __ldg(a.inv_scale + p) : 1.f;   // > 0 on every lane: the read-back is warp-collective
-      const uint32_t taddr = tmem + lane_base + (uint32_t)acc * accs;
-      corr_abs_argmax(taddr, accw, cc, a, valid ? p : -1, cb - a.corr_off, bestv, best, rawbest, second, scale);
-      recheck_near_ties(taddr, accw, cc, cb, a, valid ? p : -1, second, bestv, best, rawbest, scale);
+      if (et == 0) { SH_TRT(4, seq); }
+      // corrected scores c . x - sum_k c_k P[S_k][child], first max of |score| in child
+      // order (pursuit.py:151), 16 columns at a time
+      for (int c0 = 0; c0 < cc; c0 += 16) {
+        float4 cn[4];   // the next 16 columns' corrections, in flight during this step
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          cn[q4] = has_corr && valid && c0 + 16 + 4 * q4 < cc ? ld_now(crow + (c0 + 16) / 4 + q4)
+                                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+        float v[16];
+        acc_ld16h(taddr + (uint32_t)c0, accw, scale, v);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          v[4 * q4] -= cr[q4].x;
+          v[4 * q4 + 1] -= cr[q4].y;
+          v[4 * q4 + 2] -= cr[q4].z;
+          v[4 * q4 + 3] -= cr[q4].w;
+        }
+        const int nc = min(16, cc - c0);
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj)
+          if (jj < nc) {
+            const float m = fabsf(v[jj]);
+            if (m > bestv) {
+              second = bestv;
+              bestv = m;
+              best = c0 + jj;
+            } else {
+              second = fmaxf(second, m);
+            }
+          }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) cr[q4] = cn[q4];
+      }
+      if (et == 0) { SH_TRT(5, seq); }
+      // Near ties (score_epi.cuh: recheck_near_ties, same rule): rows whose two best
+      // scores are closer than delta note the children within 2 delta of the best
+      // -- a second read of the accumulator --, the accumulator is released, and
+      // only then are the candidates re-scored with exact dots.
+      const bool flagged = valid && bestv - second < delta;
+      const unsigned todo0 = __ballot_sync(kFull, flagged);
+      unsigned cmask[2] = {0u, 0u};
+      if (todo0) {
+        const float lo = bestv - 2.f * delta;
+        for (int c0 = 0; c0 < cc && c0 < 64; c0 += 16) {
+          float v[16];
+          acc_ld16h(taddr + (uint32_t)c0, accw, scale, v);
+          if (flagged) {
+            const int nc = min(16, cc - c0);
+            unsigned mk = 0u;
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const float corr = has_corr && jj < nc ? __ldg(a.corr_pre + (int64_t)p * a.corr_pre_ld + c0 + jj) : 0.f;
+              if (jj < nc && fabsf(v[jj] - corr) >= lo) mk |= 1u << jj;
+            }
+            cmask[c0 >> 5] |= mk << (c0 & 16);
+          }
+        }
+      }
       tc_fence_before();
       mbar_arrive(&accempty[acc]);
+      {
+        unsigned todo = todo0;
+        while (todo) {
+          const int src = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const int q = __shfl_sync(kFull, p, src);
+          const float* xrow = a.R + (int64_t)q * a.ld;
+          // all lines of the row and of every candidate centroid are requested at
+          // once (L2 prefetches), so the dots below pay one DRAM round trip together
+          // instead of one per 128 columns each
+          const unsigned cm0 = __shfl_sync(kFull, cmask[0], src), cm1 = __shfl_sync(kFull, cmask[1], src);
+          const int nlines = a.ld / 32;
+          for (int i = lane; i < nlines; i += 32) prefetch_l2(xrow + 32 * i);
+          for (int h = 0; h < 2; ++h) {
+            unsigned cand = h ? cm1 : cm0;
+            while (cand) {
+              const int jj = __ffs(cand) - 1;
+              cand &= cand - 1;
+              const float* crow_x = a.cent + (int64_t)(cb + 32 * h + jj) * a.ld;
+              for (int i = lane; i < nlines; i += 32) prefetch_l2(crow_x + 32 * i);
+            }
+          }
+          float nbv = -1.f, nraw = 0.f;
+          int nbest = 0;
+          for (int h = 0; h < 2; ++h) {
+            unsigned cand = h ? cm1 : cm0;
+            while (cand) {
+              const int jj = __ffs(cand) - 1;
+              cand &= cand - 1;
+              const int col = 32 * h + jj;
+              const float raw = warp_dot(xrow, a.cent + (int64_t)(cb + col) * a.ld, a.ld);
+              const float corr = has_corr ? __ldg(a.corr_pre + (int64_t)q * a.corr_pre_ld + col) : 0.f;
+              const float sj = fabsf(raw - corr);
+              if (sj > nbv) {   // columns visited in increasing order: strict > keeps the first max
+                nbv = sj;
+                nbest = col;
+                nraw = raw;
+              }
+            }
+          }
+          if (lane == src) {
+            bestv = nbv;
+            best = nbest;
+            rawbest = nraw;
+          }
+        }
+      }
+      if (et == 0) { SH_TRT(2, seq); }
       int leaf_info = 0, leaf_cnt = 0;
       if (last && valid) {   // the winner's leaf record, from the fp32 table block (L2-resident)
         const int* info = reinterpret_cast<const int*>(reinterpret_cast<const uint8_t*>(a.table) +
@@ -285,6 +470,18 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
   __syncthreads();
   tc_fence_after();
   if (warp == 0) tmem_dealloc(tmem, a.tmem_cols);
+#ifdef STMP_SH_TRACE
+  if ((blockIdx.x == 0 || blockIdx.x == 101 || blockIdx.x == 290) && tid == 0 && a.sup_t == 5) {
+    const long long tend = clock64() - tr_t0;
+    for (int q = 0; q < i1 - i0 && q < 32; ++q)
+      printf("TT L%d cta %d tile %d rows %d mma_start %lld acc_free %lld accfull %lld meta %lld argmax %lld epi_done %lld nrecheck(w0) %d end %lld\n", a.level, blockIdx.x, q,
+             item_of(q).z, trt[0][q], trt[1][q], trt[3][q], trt[4][q], trt[5][q], trt[2][q], trn[q], tend);
+  }
+  if (blockIdx.x == 0 && tid == 0 && a.sup_t == 5 && a.level == 99)
+    for (int g = 0; g < 64; ++g)
+      printf("TR L%d g %d landed %lld aempty %lld astaged %lld full %lld issued %lld\n", a.level, g, tr[0][g] - tr[0][0],
+             tr[1][g] - tr[0][0], tr[2][g] - tr[0][0], tr[3][g] - tr[0][0], tr[4][g] - tr[0][0]);
+#endif
 }
 
 template <int NA, int NB, int CPS>
@@ -385,8 +582,16 @@ bool score_sh_fits(int ld, int npad) {
 
 cudaError_t launch_score_sh(const ScoreArgs& s, int sms, cudaStream_t st) {
   if (!score_sh_fits(s.ld, s.npad)) return cudaErrorNotSupported;
-  if (s.npad > 32) return launch_sh<3, 3, 2>(s, sms, st);   // 48 KB of rows + 3 x 16 KB of table per CTA
-  return launch_sh<4, 4, 2>(s, sms, st);                    // 64 KB + 4 x 8 KB
+  // ring depths as a decimal code NA NB CPS (row slots, table slots, CTAs per SM);
+  // developer hook for sweeps: -DSTMP_SH_WIDE=822
+#ifndef STMP_SH_WIDE
+#define STMP_SH_WIDE 422   // npad 64: 64 KB of rows + 2 x 16 KB of table per CTA
+#endif
+#ifndef STMP_SH_NARROW
+#define STMP_SH_NARROW 532   // npad 32: 80 KB + 3 x 8 KB
+#endif
+  if (s.npad > 32) return launch_sh<STMP_SH_WIDE / 100, STMP_SH_WIDE / 10 % 10, STMP_SH_WIDE % 10>(s, sms, st);
+  return launch_sh<STMP_SH_NARROW / 100, STMP_SH_NARROW / 10 % 10, STMP_SH_NARROW % 10>(s, sms, st);
 }
 
 cudaError_t launch_half_rows(const float* X, int64_t N, int ld, uint16_t* x16, float* inv_scale, float* qerr,

@@ -42,6 +42,12 @@ def main():
         name = e.name.replace("(anonymous namespace)::", "").split("(")[0][-48:]
         agg[name][0] += 1
         agg[name][1] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+    if os.environ.get("KPROF_LIST"):   # every launch of the last encode, in launch order
+        evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+        evs.sort(key=lambda e: e.time_range.start)
+        for e in evs[-(len(evs) // reps):]:
+            t = e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+            print(f"    {t:9.1f} us  {e.name.replace('(anonymous namespace)::', '').split('(')[0][-48:]}")
     tot = sum(v[1] for v in agg.values())
     opts = " ".join(sys.argv[3:]) or "defaults"
     print(f"config {cid}, {N} patches, {opts}: {tot / reps / 1e3:.3f} ms of kernels per encode")
