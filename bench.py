@@ -411,17 +411,18 @@ def main():
     timed_ms = sum(f["ms"] for f in fams.values()) or 1.0
     dom = max(fams, key=lambda f: fams[f]["ms"]) if fams else "other"
     gram = any("update_gram_kernel" in k for k in ktimes)
+    half = any("score_sh_kernel" in k for k in ktimes)   # Gram-path level passes on fp16 rows
     staged_beam = any("beam_resolve_kernel" in k for k in ktimes)
     if dom == "fused":
         work = RL.fused_work(cfg, N, alpha, args.method)
     elif staged_beam:
         work = RL.family_work(cfg, dom, N, args.method, exhaustive, alpha=alpha)
     elif gram:
-        work = RL.gram_family_work(cfg, dom, N)
+        work = RL.gram_family_work(cfg, dom, N, half)
     else:
         work = RL.family_work(cfg, dom, N, args.method, exhaustive)
     if gram:   # the step model of the path that ran (Gram path: no residual traffic)
-        rm = RL.gram_model(cfg, N, hbm_gbs=hbm)
+        rm = RL.gram_model(cfg, N, hbm_gbs=hbm, half=half)
     dom_ms = fams[dom]["ms"] if fams else launch_ms
     dom_launches = fams[dom]["launches"] if fams else 1
     avg_s = dom_ms / dom_launches / 1e3
@@ -453,7 +454,8 @@ def main():
         "families": {f: {"launches": v["launches"], "ms": round(v["ms"], 4), "share": round(v["ms"] / timed_ms, 4)}
                      for f, v in sorted(fams.items(), key=lambda kv: -kv[1]["ms"])},
         # the whole staged step against the §8d per-patch model (the pipeline as one unit)
-        "step": {"path": "gram (no residual; pair tables)" if gram else "residual (SURVEY §8d staged design)",
+        "step": {"path": ("gram (no residual; pair tables" + ("; fp16 rows in the level passes)" if half else ")")) if gram
+                 else "residual (SURVEY §8d staged design)",
                  "bound": rm["bound"], "bytes_per_patch": rm["bytes_per_patch"],
                  "flops_per_patch": rm["flops_per_patch"], "launch_ms": launch_ms,
                  "launches": per_step, "model_patches_per_s": rm["patches_per_s_roof"],

@@ -182,6 +182,12 @@ int stmp_apply_operator(int32_t kind, const float* X, int64_t N, int32_t n_in, c
  *                needs single-atom depth-L nodes and m x nodes x 4 B of free device
  *                memory): 0 off, 1 auto = rows >= 256 and >= 8x the widest node
  *                (default), 2 whenever supported;
+ *   "half_scores": 1 (default) the Gram path's level passes multiply fp16 copies of the
+ *                patch rows (x16 = fp16(s x), one power-of-two scale per patch) by two fp16
+ *                pieces of every centroid; the exact near-tie re-check widens its window by
+ *                the rows' quantisation noise, so decisions stay the fp32 ones; 0 = fp32 rows
+ *                (3xTF32).  Applies where every level >= 1 has nodes of <= 64 children and
+ *                the padded row length is a multiple of 64;
  *   "pdl": 1 (default) launch the staged kernels with programmatic dependent launch, 0 plain;
  *   "graphs": 1 (default) replay repeated staged encodes (same buffers, sizes, stream) as CUDA graphs. */
 int stmp_set_option(const char* key, int64_t value);

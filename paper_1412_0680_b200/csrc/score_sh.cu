@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
   auto item_of = [&](int seq) { return seq < kItemCache ? s_items[seq] : item_at(a, i0 + seq); };
   const uint32_t tb = table_h_bytes(kch, npad);
   const uint32_t chunk_bytes = (uint32_t)npad * 128u * kPieces;
-  const uint32_t accw = (uint32_t)(npad + 31) / 32 * 32;   // columns per piece group (npad % 32 == 0)
+  const uint32_t accw = (uint32_t)npad;   // columns per piece group: piece q's scores start at column q npad
   const uint32_t accs = (uint32_t)kPieces * accw;                        // stride of the accumulator buffers
 
   if (warp == 5) {
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
 template <int NA, int NB, int CPS>
 cudaError_t launch_sh(ScoreArgs s, int sms, cudaStream_t st) {
   const uint32_t smem = sh_layout(s.npad, NA, NB).total;
-  const int accw = (s.npad + 31) / 32 * 32;
+  const int accw = s.npad;
   constexpr int kCols = 512 / CPS;   // TMEM columns per CTA
   const int nacc = 2 * kPieces * accw <= kCols ? 2 : 1;
   int cols = 32;
@@ -576,8 +576,8 @@ __global__ void __launch_bounds__(256) table_h_kernel(const float* __restrict__ 
 }  // namespace
 
 bool score_sh_fits(int ld, int npad) {
-  // N = kPieces npad <= 256 per MMA, whole 32-column accumulator groups, 64-column chunks
-  return ld % 64 == 0 && npad % 32 == 0 && npad >= 32 && npad <= 64;
+  // 64-column chunks; N = kPieces npad per MMA, the epilogue reads 16 columns at a time
+  return ld % 64 == 0 && npad % 16 == 0 && npad >= 16 && npad <= 64;
 }
 
 cudaError_t launch_score_sh(const ScoreArgs& s, int sms, cudaStream_t st) {

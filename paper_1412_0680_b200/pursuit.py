@@ -413,10 +413,12 @@ def encode_host(selector, X: np.ndarray, K: int, method: str = "omp", tol: float
     ``pin_memory()`` tensors' numpy views) for full copy bandwidth.
 
     ``chunk`` (rows per encode) defaults to 2^17 for narrow rows (config 1: 178 M
-    patches/s against a 55 GB/s pinned-copy floor of 217 M/s) and to half the
-    batch for rows of >= 256 floats: there every encode also streams the deepest
-    level's node tables once per iteration whatever its size (config 4: 94 ms
-    for 2^19 patches in two chunks, 129 ms in four, 459 ms in 32)."""
+    patches/s against a 55 GB/s pinned-copy floor of 217 M/s) and to a quarter of
+    the batch for rows of >= 256 floats: there every encode also streams the
+    deepest level's node tables once per iteration whatever its size, so chunks
+    should stay large, but the copy of the first chunk and the encode of the last
+    are not overlapped (config 4, 2^19 patches, 55.6 GB/s pinned copies = a
+    60.4 ms floor: 71.4 ms in four chunks, 80.8 ms in two, 99.1 ms in one)."""
     if method not in ("mp", "omp"):
         raise ValueError(f"unknown method {method!r}")
     X = np.asarray(X)
@@ -427,7 +429,7 @@ def encode_host(selector, X: np.ndarray, K: int, method: str = "omp", tol: float
         raise ValueError(f"patches have dimension {X.shape[1]}, dictionary atoms have {g.n}")
     N = X.shape[0]
     if chunk is None:
-        chunk = 1 << 17 if g.n < 256 else max(4096, -(-N // 2))
+        chunk = 1 << 17 if g.n < 256 else max(4096, -(-N // 4))
     if out is None:
         out = dict(idx=np.empty((N, K), np.int32), coef=np.empty((N, K), np.float32),
                    count=np.empty(N, np.int32), resnorm=np.empty(N, np.float32),

@@ -104,13 +104,14 @@ def test_options_and_launch_counter(lib):
     before = _lib.kernel_launches()
     assert before >= 0
     for key, bad in (("path", 3), ("score_kernel", 4), ("score_kernel", 1), ("update_kernel", 2),
-                     ("gram", 1), ("score_tma", 1)):
+                     ("gram", 1), ("score_tma", 1), ("half_scores", 2), ("half_scores", -1)):
         with pytest.raises(ValueError):
             _lib.set_option(key, bad)
     with pytest.raises(ValueError):
         _lib.set_option("no_such_option", 0)
     _lib.set_option("update_kernel", 1)
     _lib.set_option("score_kernel", 2)
+    _lib.set_option("half_scores", 1)
     _lib.set_option("path", _lib.PATH_AUTO)
     assert _lib.kernel_launches() == before   # option changes launch nothing
 

@@ -43,6 +43,7 @@ def restore_defaults(_lib):
     _lib.set_option("score_kernel", 2)
     _lib.set_option("update_kernel", 1)
     _lib.set_option("gram_path", 1)
+    _lib.set_option("half_scores", 1)
 
 
 @pytest.fixture(params=PATHS)
@@ -533,6 +534,31 @@ def test_gram_path_exact_sparse_and_tolerance(tol_tag, tol):
     rep = compare({k: v[rows] for k, v in out.items()}, ref, X[rows], check_path=True)
     print(f"gram exact-sparse {tol_tag}: {rep.summary()}")
     assert rep.ok, rep.summary()
+
+
+@pytest.mark.parametrize("cid,rows", [(4, 512), (1, 4096), (0, 4096)])
+@pytest.mark.parametrize("half", [0, 1])
+def test_gram_level_passes_fp16_rows_and_fp32_rows(cid, rows, half):
+    """Gram path with the level passes on fp16 patch rows (score_sh.cu, the default)
+    and on fp32 rows (score_st.cu, half_scores = 0): both must meet the oracle, and
+    the option must select the kernel."""
+    from paper_1412_0680_b200 import _lib
+    cfg, wl, flat = config(cid)
+    X, ref = oracle_config(cid, rows, "omp")
+    sel = P().TreeSelector(flat, wl.atoms, cfg.alpha)
+    _lib.set_option("path", _lib.PATH_STAGED)
+    _lib.set_option("gram_path", 2)
+    _lib.set_option("half_scores", half)
+    try:
+        out, names = launched(lambda: run(sel, X, cfg.K, "omp"))
+    finally:
+        restore_defaults(_lib)
+    assert any("update_gram_kernel" in k for k in names), sorted(names)
+    assert any("score_sh_kernel" in k for k in names) == bool(half), sorted(names)
+    rep = compare(out, ref, X)
+    print(f"c{cid} gram half_scores={half}: {rep.summary()}")
+    assert rep.ok, rep.summary()
+    assert rep.excused <= max(2, rows // 500)
 
 
 # ----------------------------------------------------------------- beam (non-greedy alpha) descent
