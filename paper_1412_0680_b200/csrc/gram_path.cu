@@ -306,7 +306,10 @@ __global__ void __launch_bounds__(256) update_gram_kernel(GramArgs a) {
     if (hist[i]) atomicAdd(&a.root_counts[i], hist[i]);
 }
 
-__global__ void __launch_bounds__(256) gram_corr_kernel(int64_t N, const int* active, const int* path_ws, int L,
+#ifndef STMP_CORR_MINB
+#define STMP_CORR_MINB 8
+#endif
+__global__ void __launch_bounds__(256, STMP_CORR_MINB) gram_corr_kernel(int64_t N, const int* active, const int* path_ws, int L,
                                                         int level, const int* child_begin, const int* child_count,
                                                         int col_off, const float* __restrict__ tab, int64_t tab_w,
                                                         const int* S_ws, const float* c_ws, int K, int T,
@@ -314,22 +317,40 @@ __global__ void __launch_bounds__(256) gram_corr_kernel(int64_t N, const int* ac
   pdl_enter();
   const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (p >= N || !active[p]) return;
-  const int node = path_ws[p * L + level - 1];
+  if (p >= N) return;
+  // one round trip for the patch's state (ld_now: issued here, before anything
+  // waits), one for its node's child range, then the table rows
+  const int act = ld_now(active + p);
+  const int node = ld_now(path_ws + p * L + level - 1);
+  const int Sk = lane < T ? ld_now(S_ws + p * K + lane) : 0;
+  const float ck = lane < T ? ld_now(c_ws + p * K + lane) : 0.f;
+  if (!act) return;
   const int cb = __ldg(child_begin + node), cc = __ldg(child_count + node);
-  const int Sk = lane < T ? S_ws[p * K + lane] : 0;
-  const float ck = lane < T ? c_ws[p * K + lane] : 0.f;
   const float* base = tab + (cb - col_off);
-  // (measured: batching the k loop for more loads in flight per lane is slower --
-  // 313 -> 437 us per launch at half the occupancy; the random 128/256-byte table
-  // rows, not the load latency, bound this kernel)
+  // support rows loaded before the first FMA.  Measured on config 4 (22 launches
+  // per encode): 1 row 301 us per launch, 4 rows 274, 6 rows 270, 8 rows 345 (spills
+  // at the 32-register bound), 8 / 12 rows at 40 / 48 registers 314 / 397: beyond a
+  // few rows in flight the random table rows (TLB reach, DRAM pages), not the load
+  // latency, set the pace, and occupancy matters more.
+#ifndef STMP_CORR_BATCH
+#define STMP_CORR_BATCH 6
+#endif
+  constexpr int kB = STMP_CORR_BATCH;
   for (int j0 = 0; j0 < cc; j0 += 32) {
     const int j = j0 + lane;
     float acc = 0.f;
-    for (int k = 0; k < T; ++k) {
-      const int s_k = __shfl_sync(kFull, Sk, k);
-      const float c_k = __shfl_sync(kFull, ck, k);
-      if (j < cc) acc = fmaf(c_k, __ldg(base + (int64_t)s_k * tab_w + j), acc);
+    for (int k0 = 0; k0 < T; k0 += kB) {
+      float v[kB], c_k[kB];
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+        const int k = min(k0 + q, T - 1);
+        const int s_k = __shfl_sync(kFull, Sk, k);
+        c_k[q] = __shfl_sync(kFull, ck, k);
+        v[q] = j < cc ? __ldg(base + (int64_t)s_k * tab_w + j) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < kB; ++q)
+        if (k0 + q < T) acc = fmaf(c_k[q], v[q], acc);
     }
     if (j < cc) out[p * ld + j] = acc;
   }

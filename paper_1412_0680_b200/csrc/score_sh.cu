@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
       printf("TT L%d cta %d tile %d rows %d mma_start %lld acc_free %lld accfull %lld meta %lld argmax %lld epi_done %lld nrecheck(w0) %d end %lld\n", a.level, blockIdx.x, q,
              item_of(q).z, trt[0][q], trt[1][q], trt[3][q], trt[4][q], trt[5][q], trt[2][q], trn[q], tend);
   }
-  if (blockIdx.x == 0 && tid == 0 && a.sup_t == 5 && a.level == 99)
+  if (blockIdx.x == 0 && tid == 0 && a.sup_t == 5)
     for (int g = 0; g < 64; ++g)
       printf("TR L%d g %d landed %lld aempty %lld astaged %lld full %lld issued %lld\n", a.level, g, tr[0][g] - tr[0][0],
              tr[1][g] - tr[0][0], tr[2][g] - tr[0][0], tr[3][g] - tr[0][0], tr[4][g] - tr[0][0]);
