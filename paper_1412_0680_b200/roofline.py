@@ -73,7 +73,8 @@ def model(cfg, N: int | None = None, method: str = "omp", exhaustive: bool = Fal
 
 # ---------------------------------------------------------------- per kernel family
 # Kernel families of one staged encode, by (mangled) kernel name.
-FAMILIES = (("score", ("score_ts_kernel", "score_st_kernel", "score_sh_kernel", "gram_corr_kernel")),
+FAMILIES = (("corr", ("gram_corr_kernel",)),
+            ("score", ("score_ts_kernel", "score_st_kernel", "score_sh_kernel")),
             ("exact_scan", ("exact_scan_kernel",)),
             ("update", ("update_omp8_kernel", "update_wide_kernel", "update_gram_kernel", "update_kernel")),
             ("scatter", ("scatter_scan_kernel", "scatter_kernel", "scatter_root_kernel", "scan_kernel",
@@ -131,10 +132,12 @@ def gram_family_work(cfg, family: str, N: int, half: bool = False) -> dict:
 
     * score: x rows per pass -- the root once (iteration 0, 4n B, plus its raw
       scores 4 k_1 B cached), levels 1..L-1 every iteration (4n B, or 2n B with
-      ``half``: fp16 rows, score_sh.cu) -- the support's correction reads
-      T x k_{l+1} pair-table floats per pass, node tables only where a level's
-      centroids exceed L2 (each visited node once per iteration; 4 B per value
-      either way: tf32 hi | lo or two fp16 pieces); FLOPs 2n per scored child.
+      ``half``: fp16 rows, score_sh.cu) plus the precomputed correction row
+      (4 k_{l+1} B), node tables only where a level's centroids exceed L2 (each
+      visited node once per iteration; 4 B per value either way: tf32 hi | lo or
+      two fp16 pieces); FLOPs 2n per scored child.
+    * corr (gram_corr_kernel, one launch per level >= 1 and iteration >= 1): the
+      support's T x k_{l+1} pair-table floats in, one k_{l+1}-float row out.
     * init (``half``): the fp16 row copy reads x and writes 2n B per patch once.
     * update: x and the chosen atom (2 x 4n B) for the exact right-hand side, T Gram
       entries, the cached root scores (4 k_1 B) and the solver state (M row, c, y).
@@ -148,9 +151,12 @@ def gram_family_work(cfg, family: str, N: int, half: bool = False) -> dict:
     tables = sum(4 * n * k for k in kids[1:] if 4 * n * k > L2_BYTES)
     if family == "score":
         row = 2 * n if half else 4 * n
-        b = 4 * n + 4 * br[0] + K * (L - 1) * (row + 8) + T_sum * 4 * sum(br[1:])
+        b = 4 * n + 4 * br[0] + K * (L - 1) * (row + 8) + (K - 1) * 4 * sum(br[1:])
         return binding({"bytes": float(N * b + K * tables),
                         "flops": float(N * 2 * n * (br[0] + K * sum(br[1:])))})
+    if family == "corr":
+        b = (T_sum + K - 1) * 4 * sum(br[1:])
+        return {"bytes": float(N * b), "flops": float(N * 2 * T_sum * sum(br[1:])), "bound": "hbm"}
     if family == "update":
         b = sum(8 * n + 4 * T + 4 * br[0] + 4 * 3 * (T + 1) for T in range(K))
         return {"bytes": float(N * b), "flops": float(N * K * 2 * n), "bound": "hbm"}
@@ -161,7 +167,7 @@ def gram_family_work(cfg, family: str, N: int, half: bool = False) -> dict:
 
 def gram_model(cfg, N: int, hbm_gbs: float = 6548.2, half: bool = False) -> dict:
     """The Gram path's whole-step algorithmic bytes per patch (sum of its families)."""
-    fams = ("score", "update", "scatter", "init")
+    fams = ("score", "corr", "update", "scatter", "init")
     B = sum(gram_family_work(cfg, f, N, half)["bytes"] for f in fams) / N
     F = sum(gram_family_work(cfg, f, N, half)["flops"] for f in fams) / N
     return dict(flops_per_patch=F, bytes_per_patch=B, bound="hbm", t_roof_per_patch=B / (hbm_gbs * 1e9),
