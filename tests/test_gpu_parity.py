@@ -561,6 +561,32 @@ def test_gram_level_passes_fp16_rows_and_fp32_rows(cid, rows, half):
     assert rep.excused <= max(2, rows // 500)
 
 
+def test_fp16_rows_follow_the_patch_scale():
+    """The fp16 row copies carry one power-of-two scale per patch: patches scaled
+    by 2^-60 .. 2^60 (exact in fp32, so the f64 oracle's results scale exactly too)
+    must give the same selections and exactly scaled coefficients and norms."""
+    from paper_1412_0680_b200 import _lib
+    cfg, wl, flat = config(4)
+    X, ref = oracle_config(4, 512, "omp")
+    scale = np.ldexp(1.0, np.resize(np.array([-60, -7, 0, 9, 60]), len(X))).astype(np.float64)
+    Xs = (X.astype(np.float64) * scale[:, None]).astype(np.float32)
+    assert np.array_equal(Xs.astype(np.float64), X.astype(np.float64) * scale[:, None])
+    sref = dict(ref)
+    sref["coef"] = ref["coef"] * scale[:, None]
+    sref["resnorm"] = ref["resnorm"] * scale
+    sel = P().TreeSelector(flat, wl.atoms, cfg.alpha)
+    _lib.set_option("path", _lib.PATH_STAGED)
+    try:
+        out, names = launched(lambda: run(sel, Xs, cfg.K, "omp"))
+    finally:
+        restore_defaults(_lib)
+    assert any("score_sh_kernel" in k for k in names), sorted(names)
+    rep = compare(out, sref, Xs)
+    print(f"c4 fp16 rows, scaled patches: {rep.summary()}")
+    assert rep.ok, rep.summary()
+    assert rep.excused <= 2
+
+
 # ----------------------------------------------------------------- beam (non-greedy alpha) descent
 
 @pytest.mark.parametrize("tag,alpha", [("beam", 0.3), ("full", 1.0)])
