@@ -543,6 +543,12 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       ui.xn2 = (double*)(b + w.xn2);
       ui.e_ws = (double*)(b + w.e_ws);
       ui.X2 = nullptr;
+      // level passes on fp16 rows (score_sh.cu): init writes the fp16 copy in the same pass over x
+      if (w.half && g_half_scores != 0 && (int)t->half_tables.size() == L) {
+        ui.x16 = (uint16_t*)(b + w.x16);
+        ui.inv_scale = (float*)(b + w.inv_scale);
+        ui.qerr = (float*)(b + w.qerr);
+      }
     }
     if ((e = launch_init(uc, ui, ublocks, st)) != cudaSuccess) return e;
   }
@@ -574,12 +580,11 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
     ga.Lf = Lf; ga.e_ws = e_ws; ga.xn2 = xn2; ga.tol = tol; ga.active = active; ga.idx = idx; ga.coef = coef;
     ga.count = count; ga.resnorm = resnorm; ga.ip = ip;
     ga.xr = R0; ga.atoms = d->atoms; ga.cent = t->cent; ga.ld = d->ld; ga.rho = 1e-2f; ga.recheck_rel = 1e-5f;
-    // level passes on fp16 rows (score_sh.cu) when the tree carries the fp16 piece tables
+    // level passes on fp16 rows (score_sh.cu) when the tree carries the fp16 piece tables (init wrote x16)
     const bool half = w.half && g_half_scores != 0 && (int)t->half_tables.size() == L;
     uint16_t* x16 = half ? (uint16_t*)(b + w.x16) : nullptr;
     float* inv_scale = half ? (float*)(b + w.inv_scale) : nullptr;
     float* qerr = half ? (float*)(b + w.qerr) : nullptr;
-    if (half && (e = launch_half_rows(R0, N, d->ld, x16, inv_scale, qerr, st)) != cudaSuccess) return e;
     for (int it = 0; it < K; ++it) {
       for (int l = it == 0 ? 0 : 1; l < L; ++l) {
         const StagedLevel& lv = t->staged_levels[l];
@@ -620,7 +625,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
         s.cent = t->cent; s.xn2 = xn2; s.recheck_rel = 1e-5f;
         s.corr_pre = corr_pre; s.corr_pre_ld = (t->max_children + 3) & ~3;
         if (l == 0) { s.raw_out = s0; s.raw_w = t->root_children; }   // iteration 0: cache c_v . x of the root
-        if (half && l > 0) {
+        if (half && l > 0) {   // (the root pass stays on fp32 rows: its raw scores are cached for every later root choice)
           s.R16 = x16; s.table_h = t->half_tables[l]; s.inv_scale = inv_scale; s.qerr = qerr;
           // window += 16 sigma of the rows' quantisation noise on a unit centroid's score (||e|| / sqrt(n))
           s.recheck_q = 16.f / sqrtf((float)d->n);

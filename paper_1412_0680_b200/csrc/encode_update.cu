@@ -9,6 +9,8 @@
 // column sweeps in which lane j owns rows j, j+G, ... of the Cholesky factor.
 // Semantics: pkg/src/stmp/pursuit.py:207-221 (MP) and the SURVEY §8c OMP
 // restatement over omp_refit (pursuit.py:235-250).
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "sm100.cuh"
@@ -115,6 +117,43 @@ __global__ void __launch_bounds__(128) init_kernel(UpdateArgs a) {
     }
     if (a.R) x.store(a.R + p * a.ld, gl, F);
     if (a.X2) x.store(const_cast<float*>(a.X2) + p * a.ld2, gl, F);
+    if (a.x16) {
+      // fp16 row copy for the Gram path's level passes (score_sh.cu): s = 2^(15 - e)
+      // with max |x| = f 2^e, f in [0.5, 1), so the largest element lands in
+      // [2^14, 2^15) and elements down to 2^-28 of it stay normal halfs
+      float mx = 0.f;
+#pragma unroll
+      for (int i = 0; i < CPL * 4; ++i) mx = fmaxf(mx, fabsf(x.v[i]));
+#pragma unroll
+      for (int o = G >> 1; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(group_mask<G>(), mx, o));
+      int e = 0;
+      if (mx > 0.f && mx < 3.0e38f) frexpf(mx, &e);
+      const int sh = max(-100, min(100, 15 - e));
+      const float s = ldexpf(1.f, sh), is = ldexpf(1.f, -sh);
+      uint2* out = reinterpret_cast<uint2*>(a.x16 + p * a.ld);
+      float err2 = 0.f;
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) {
+        const int c = gl + G * i;
+        if (c < F) {
+          unsigned short h[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const __half hv = __float2half_rn(x.v[4 * i + k] * s);
+            const float d = x.v[4 * i + k] - __half2float(hv) * is;
+            err2 = fmaf(d, d, err2);
+            h[k] = __half_as_ushort(hv);
+          }
+          out[c] = make_uint2((unsigned)h[0] | ((unsigned)h[1] << 16), (unsigned)h[2] | ((unsigned)h[3] << 16));
+        }
+      }
+#pragma unroll
+      for (int o = G >> 1; o; o >>= 1) err2 += __shfl_xor_sync(group_mask<G>(), err2, o);
+      if (gl == 0) {
+        a.inv_scale[p] = is;
+        a.qerr[p] = sqrtf(err2);
+      }
+    }
   }
   ss = group_sum<G>(ss);
   const float xn = sqrtf(ss);

@@ -2,8 +2,8 @@
 //
 // On the Gram path (gram_path.cu) the rows the level passes multiply are the
 // patches x themselves, never a residual, so they can be prepared once per
-// encode: x16 = fp16(s_p x) with a power-of-two scale s_p per patch (half the
-// bytes of every pass), and the exact near-tie re-check of the epilogue
+// encode (by the init kernel, encode_update.cu, in its pass over x): x16 =
+// fp16(s_p x) with a power-of-two scale s_p per patch (half the bytes of every pass), and the exact near-tie re-check of the epilogue
 // (score_epi.cuh) widens its window by the rows' quantisation noise, so a
 // decision is either unaffected by it or re-taken with exact fp32 FFMA dots.
 // The child centroids keep 22 significant bits: c = p0 + 2^-11 p1 with fp16
@@ -499,50 +499,6 @@ cudaError_t launch_sh(ScoreArgs s, int sms, cudaStream_t st) {
   return launch_kernel(score_sh_kernel<NA, NB, CPS>, sms * CPS, kThreads, (size_t)smem, st, true, s, nacc);
 }
 
-// x16 = fp16(s x) with s = 2^(15 - e), max |x| = f 2^e, f in [0.5, 1): the largest
-// element lands in [2^14, 2^15), so elements down to 2^-28 of it stay normal
-// halfs.  One warp per patch row (ld floats, zero padding included).
-__global__ void __launch_bounds__(256) half_rows_kernel(const float* __restrict__ X, int64_t N, int ld,
-                                                        uint16_t* __restrict__ x16, float* __restrict__ inv_scale,
-                                                        float* __restrict__ qerr) {
-  const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (p >= N) return;
-  const float4* row = reinterpret_cast<const float4*>(X + p * ld);
-  const int nq = ld / 4;
-  float mx = 0.f;
-  for (int i = lane; i < nq; i += 32) {
-    const float4 v = __ldg(row + i);
-    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
-  int e = 0;
-  if (mx > 0.f && mx < 3.0e38f) frexpf(mx, &e);
-  const int sh = max(-100, min(100, 15 - e));
-  const float s = ldexpf(1.f, sh), is = ldexpf(1.f, -sh);
-  uint2* out = reinterpret_cast<uint2*>(x16 + p * ld);
-  float err2 = 0.f;
-  for (int i = lane; i < nq; i += 32) {
-    const float4 v = __ldg(row + i);   // second read: the row is L1 / L2 hot
-    const __half h0 = __float2half_rn(v.x * s), h1 = __float2half_rn(v.y * s), h2 = __float2half_rn(v.z * s),
-                 h3 = __float2half_rn(v.w * s);
-    const float d0 = v.x - __half2float(h0) * is, d1 = v.y - __half2float(h1) * is,
-                d2 = v.z - __half2float(h2) * is, d3 = v.w - __half2float(h3) * is;
-    err2 = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, err2))));
-    uint2 w;
-    w.x = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-    w.y = (uint32_t)__half_as_ushort(h2) | ((uint32_t)__half_as_ushort(h3) << 16);
-    out[i] = w;
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) err2 += __shfl_xor_sync(kFull, err2, o);
-  if (lane == 0) {
-    inv_scale[p] = is;
-    qerr[p] = sqrtf(err2);
-  }
-}
-
 // Per-node half-precision score tables of one level: each child centroid value
 // c = p0 + 2^-11 p1 (+ 2^-22 p2, exact, when kPieces == 3) in fp16 pieces, round
 // to nearest (p0 keeps 11 significant bits, p1 the next 11), laid out [chunk of
@@ -592,11 +548,6 @@ cudaError_t launch_score_sh(const ScoreArgs& s, int sms, cudaStream_t st) {
 #endif
   if (s.npad > 32) return launch_sh<STMP_SH_WIDE / 100, STMP_SH_WIDE / 10 % 10, STMP_SH_WIDE % 10>(s, sms, st);
   return launch_sh<STMP_SH_NARROW / 100, STMP_SH_NARROW / 10 % 10, STMP_SH_NARROW % 10>(s, sms, st);
-}
-
-cudaError_t launch_half_rows(const float* X, int64_t N, int ld, uint16_t* x16, float* inv_scale, float* qerr,
-                             cudaStream_t st) {
-  return launch_kernel(half_rows_kernel, (unsigned)((N + 7) / 8), 256, 0, st, true, X, N, ld, x16, inv_scale, qerr);
 }
 
 uint8_t* build_half_table(const TreeHandle* t, int l, cudaStream_t st) {

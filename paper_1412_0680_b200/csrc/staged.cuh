@@ -139,6 +139,11 @@ struct UpdateArgs {
   int iter;              // iteration index = support size of every active patch
   double* xn2;           // Gram path: ||x||^2 per patch (init), and the running ||r||^2
   double* e_ws;
+  // Gram path with fp16 level passes (score_sh.cu): init also writes the fp16 row
+  // copy x16 = fp16(s_p x), 1 / s_p and ||x - x16 / s_p|| (nullptr: not needed)
+  uint16_t* x16;
+  float* inv_scale;
+  float* qerr;
 };
 
 // Gram path (gram_path.cu, OMP on trees whose depth-L nodes are single atoms):
@@ -245,9 +250,6 @@ bool score_sh_fits(int ld, int npad);
 cudaError_t launch_score_sh(const ScoreArgs& s, int sms, cudaStream_t st);
 // bytes of one node's half-precision table block
 __host__ __device__ inline uint32_t table_h_bytes(int kch64, int npad) { return (uint32_t)kch64 * 2u * npad * 128u; }
-// x16 / inv_scale / qerr of every patch row (one warp per patch)
-cudaError_t launch_half_rows(const float* X, int64_t N, int ld, uint16_t* x16, float* inv_scale, float* qerr,
-                             cudaStream_t st);
 // per-node fp16 piece tables of level l (nullptr on allocation failure)
 uint8_t* build_half_table(const TreeHandle* t, int l, cudaStream_t st);
 extern int g_half_scores;   // 1: Gram-path level passes read fp16 rows (default), 0: fp32 rows / 3xTF32

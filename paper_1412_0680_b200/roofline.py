@@ -79,7 +79,7 @@ FAMILIES = (("corr", ("gram_corr_kernel",)),
             ("update", ("update_omp8_kernel", "update_wide_kernel", "update_gram_kernel", "update_kernel")),
             ("scatter", ("scatter_scan_kernel", "scatter_kernel", "scatter_root_kernel", "scan_kernel",
                          "scatter_entries_kernel", "beam_resolve_kernel")),
-            ("init", ("init_kernel", "half_rows_kernel")),
+            ("init", ("init_kernel",)),
             ("fused", ("encode_fused_kernel",)))
 
 
@@ -138,7 +138,7 @@ def gram_family_work(cfg, family: str, N: int, half: bool = False) -> dict:
       two fp16 pieces); FLOPs 2n per scored child.
     * corr (gram_corr_kernel, one launch per level >= 1 and iteration >= 1): the
       support's T x k_{l+1} pair-table floats in, one k_{l+1}-float row out.
-    * init (``half``): the fp16 row copy reads x and writes 2n B per patch once.
+    * init (``half``): the init pass also writes the fp16 row copy, 2n B per patch.
     * update: x and the chosen atom (2 x 4n B) for the exact right-hand side, T Gram
       entries, the cached root scores (4 k_1 B) and the solver state (M row, c, y).
     * scatter / init as in family_work.
@@ -161,7 +161,7 @@ def gram_family_work(cfg, family: str, N: int, half: bool = False) -> dict:
         b = sum(8 * n + 4 * T + 4 * br[0] + 4 * 3 * (T + 1) for T in range(K))
         return {"bytes": float(N * b), "flops": float(N * K * 2 * n), "bound": "hbm"}
     if family == "init" and half:
-        return {"bytes": float(N * (4 * n * 2 + 4 * n + 2 * n)), "flops": 0.0, "bound": "hbm"}
+        return {"bytes": float(N * (4 * n * 2 + 2 * n)), "flops": 0.0, "bound": "hbm"}
     return family_work(cfg, family, N, "omp", False)
 
 

@@ -27,14 +27,14 @@ def test_gram_model_is_the_sum_of_its_families_and_half_rows_cost_less():
     assert RL.gram_family_work(cfg, "update", cfg.N, True) == RL.gram_family_work(cfg, "update", cfg.N, False)
     # the fp16 copy is paid once, in the init family
     assert RL.gram_family_work(cfg, "init", cfg.N, True)["bytes"] - \
-        RL.gram_family_work(cfg, "init", cfg.N, False)["bytes"] == cfg.N * 6 * cfg.n
+        RL.gram_family_work(cfg, "init", cfg.N, False)["bytes"] == cfg.N * 2 * cfg.n
 
 
 def test_kernel_families():
     names = {"void stmp::(anonymous namespace)::score_sh_kernel<4, 2, 2>(stmp::ScoreArgs, int)": "score",
              "stmp::(anonymous namespace)::gram_corr_kernel(long, int const*)": "corr",
              "void stmp::(anonymous namespace)::update_gram_kernel<5, 2>(stmp::GramArgs)": "update",
-             "stmp::(anonymous namespace)::half_rows_kernel(float const*, long, int)": "init",
+             "void stmp::(anonymous namespace)::init_kernel<32, 13>(stmp::UpdateArgs)": "init",
              "void stmp::(anonymous namespace)::scatter_scan_kernel<2>(long)": "scatter",
              "void stmp::(anonymous namespace)::exact_scan_kernel<4, 2>(stmp::ScoreArgs)": "exact_scan"}
     for name, fam in names.items():
