@@ -117,8 +117,13 @@ __device__ __forceinline__ float warp_sum_f(float v) {
 //     root scores s0, with the near-tie re-check (exact dots; the re-scored s0
 //     entries are written back).
 // Solver state is laid out per patch: S, c, y [N][K], M [N][K(K+1)/2].
+// four CTAs per SM (64 registers, ~80 B of spills) for root nodes of <= 64 children: left to
+// itself ptxas takes 72-74 registers at T = 5, 9, 10, 11 and those launches run 7-13 % slower
+#ifndef STMP_GRAM_MINB
+#define STMP_GRAM_MINB 4
+#endif
 template <int T, int kMaxPer>   // kMaxPer: root children per lane (root_w <= 32 kMaxPer)
-__global__ void __launch_bounds__(256) update_gram_kernel(GramArgs a) {
+__global__ void __launch_bounds__(256, (STMP_GRAM_MINB > 1 && kMaxPer == 2) ? STMP_GRAM_MINB : 1) update_gram_kernel(GramArgs a) {
   pdl_enter();
   __shared__ int hist[256];
   for (int i = threadIdx.x; i < a.root_w; i += blockDim.x) hist[i] = 0;
