@@ -402,7 +402,7 @@ struct WsLayout {
       num_items, cursor2;
   // Gram path only
   bool gram = false;
-  size_t xn2 = 0, e_ws = 0, s0 = 0, bsel = 0, corr = 0;
+  size_t xn2 = 0, e_ws = 0, s0 = 0, corr = 0;
   // half-precision rows of the Gram path's level passes (score_sh.cu)
   bool half = false;
   size_t x16 = 0, inv_scale = 0, qerr = 0;
@@ -450,7 +450,6 @@ WsLayout layout(const DictHandle* d, const TreeHandle* t, int64_t N, int K, int 
     w.xn2 = add((size_t)N * 8);
     w.e_ws = add((size_t)N * 8);
     w.s0 = add((size_t)N * t->root_children * 4);
-    w.bsel = add((size_t)N * 4);
     w.corr = add((size_t)N * ((t->max_children + 3) & ~3) * 4);   // rows of whole float4
     // reserved whenever the shapes allow it (the option is read at encode time)
     w.half = true;
@@ -570,9 +569,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
     double* xn2 = (double*)(b + w.xn2);
     double* e_ws = (double*)(b + w.e_ws);
     float* s0 = (float*)(b + w.s0);
-    float* bsel = (float*)(b + w.bsel);
     GramArgs ga{};
-    ga.N = N; ga.K = K; ga.L = L; ga.leaf_sel = leaf_sel; ga.bsel = bsel;
+    ga.N = N; ga.K = K; ga.L = L; ga.leaf_sel = leaf_sel;
     ga.gram = t->pair_tables[L - 1]; ga.gram_w = t->pair_width[L - 1]; ga.leaf_pos = t->leaf_pos;
     ga.root_tab = t->pair_tables[0]; ga.s0 = s0; ga.root_w = t->root_children;
     ga.root_cb = (int)t->level_offsets[1];
@@ -617,7 +615,6 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
           s.next_base = (int)t->level_offsets[l + 1];
         } else {
           s.leaf_sel = leaf_sel;
-          s.bsel = bsel;
         }
         // the rows are x: scores corrected by the support's pair-table products
         s.corr = t->pair_tables[l]; s.corr_w = t->pair_width[l]; s.corr_off = (int)t->level_offsets[l + 1];

@@ -66,12 +66,12 @@ __device__ __forceinline__ void acc_ld32x(uint32_t taddr, uint32_t off2, float s
 // the node's cc children; subtract the support's contribution
 // sum_k c_k P[S_k][colbase + v] (the patch's current OMP support and
 // coefficients), then the first max of |score| in child order
-// (pursuit.py:151).  `rawbest` is the winner's uncorrected c . x (for the last
-// level: a . x, the OMP right-hand side); iteration 0's root pass also stores
-// every raw score (raw_out) for the later root choices.  p < 0: no patch row.
+// (pursuit.py:151); `second` is the runner-up's |score| (the near-tie test).
+// Iteration 0's root pass also stores every raw score (raw_out) for the later
+// root choices.  p < 0: no patch row.
 __device__ __forceinline__ void corr_abs_argmax(uint32_t taddr, uint32_t off2, int cc, const ScoreArgs& a, int p,
-                                                int colbase, float& bestv, int& best, float& rawbest,
-                                                float& second, float scale = 0.f) {
+                                                int colbase, float& bestv, int& best, float& second,
+                                                float scale = 0.f) {
   const int T = p >= 0 && a.corr ? a.sup_t : 0;
   const bool vec = ((colbase | (int)a.corr_w) & 3) == 0;
   for (int c0 = 0; c0 < cc; c0 += 32) {
@@ -79,9 +79,6 @@ __device__ __forceinline__ void corr_abs_argmax(uint32_t taddr, uint32_t off2, i
     acc_ld32x(taddr + (uint32_t)c0, off2, scale, v);   // every lane of the warp takes part
     if (p < 0) continue;
     const int nc = min(32, cc - c0);
-    float raw[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) raw[j] = v[j];
     if (a.raw_out) {
       float* dst = a.raw_out + (int64_t)p * a.raw_w + c0;
 #pragma unroll
@@ -132,7 +129,6 @@ __device__ __forceinline__ void corr_abs_argmax(uint32_t taddr, uint32_t off2, i
           second = bestv;
           bestv = m;
           best = c0 + j;
-          rawbest = raw[j];
         } else {
           second = fmaxf(second, m);
         }
@@ -181,8 +177,7 @@ __device__ __forceinline__ float warp_dot(const float* __restrict__ x, const flo
 // whose approximate score lies within 2 delta of the best -- the others cannot
 // win -- and the first maximum in child order is kept (pursuit.py:151).
 __device__ __forceinline__ void recheck_near_ties(uint32_t taddr, uint32_t off2, int cc, int cb, const ScoreArgs& a,
-                                                  int p, float second, float& bestv, int& best, float& rawbest,
-                                                  float scale = 0.f) {
+                                                  int p, float second, float& bestv, int& best, float scale = 0.f) {
   const int lane = (int)(threadIdx.x & 31);
   // half-precision rows add their quantisation noise to the window: recheck_q * ||x - x16 / s||
   const float delta = p >= 0 ? a.recheck_rel * (float)sqrt(a.xn2[p]) + (a.qerr ? a.recheck_q * a.qerr[p] : 0.f) : 0.f;
@@ -193,7 +188,7 @@ __device__ __forceinline__ void recheck_near_ties(uint32_t taddr, uint32_t off2,
     const int q = __shfl_sync(kFull, p, src);
     const float lo = __shfl_sync(kFull, bestv, src) - 2.f * __shfl_sync(kFull, delta, src);
     const float* xrow = a.R + (int64_t)q * a.ld;
-    float nbv = -1.f, nraw = 0.f;
+    float nbv = -1.f;
     int nbest = 0;
     for (int c0 = 0; c0 < cc; c0 += 32) {
       float v[32];
@@ -223,14 +218,12 @@ __device__ __forceinline__ void recheck_near_ties(uint32_t taddr, uint32_t off2,
         if (sj > nbv) {   // columns visited in increasing order: strict > keeps the first max
           nbv = sj;
           nbest = c0 + j;
-          nraw = raw;
         }
       }
     }
     if (lane == src) {
       bestv = nbv;
       best = nbest;
-      rawbest = nraw;
     }
   }
 }

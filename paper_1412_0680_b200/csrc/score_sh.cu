@@ -86,12 +86,6 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_
       : "memory");
 }
 
-#ifndef STMP_SH_FENCE
-#define STMP_SH_FENCE 1
-#endif
-#ifndef STMP_SH_SKIP   // timing experiments only: 1 = no MMAs, 2 = no row gather, 4 = no table copies
-#define STMP_SH_SKIP 0
-#endif
 
 template <int NA, int NB, int CPS>
 __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, int nacc) {
@@ -176,10 +170,6 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
         if (c == 0) bin = item_of(seq).x;
         const int s = g % NB;
         if (g >= NB) mbar_wait(&done[s], (uint32_t)(g / NB - 1) & 1u);
-        if (STMP_SH_SKIP & 4) {
-          mbar_arrive(&full[s]);
-          continue;
-        }
         mbar_arrive_expect_tx(&full[s], chunk_bytes);
         bulk_g2s_hint(base + Ly.btab + s * bslot, a.table_h + (size_t)bin * tb + (size_t)c * chunk_bytes, chunk_bytes,
                       &full[s], tab_policy);
@@ -207,17 +197,14 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
         SH_TR(2, g);
         mbar_wait(&full[s], pb);
         SH_TR(3, g);
-        if (STMP_SH_FENCE == 2) fence_proxy_async_smem();
         tc_fence_after();
         const uint64_t ad = adesc0 + (uint64_t)((uint32_t)sa * (kSlot >> 4));
         const uint64_t bd = bdesc0 + (uint64_t)((uint32_t)s * (bslot >> 4));
         const int nks = c == kch - 1 ? ks_last : 4;   // the rest is zero padding on both operands
-        if (!(STMP_SH_SKIP & 1)) {
-          mma_f16(dcol, ad, bd, idesc, c ? 1u : 0u);
-          if (nks > 1) mma_f16(dcol, ad + 2, bd + 2, idesc, 1u);
-          if (nks > 2) mma_f16(dcol, ad + 4, bd + 4, idesc, 1u);
-          if (nks > 3) mma_f16(dcol, ad + 6, bd + 6, idesc, 1u);
-        }
+        mma_f16(dcol, ad, bd, idesc, c ? 1u : 0u);
+        if (nks > 1) mma_f16(dcol, ad + 2, bd + 2, idesc, 1u);
+        if (nks > 2) mma_f16(dcol, ad + 4, bd + 4, idesc, 1u);
+        if (nks > 3) mma_f16(dcol, ad + 6, bd + 6, idesc, 1u);
         mma_commit(&done[s]);
         mma_commit(&aempty[sa]);
         if (c == kch - 1) mma_commit(&accfull[acc]);
@@ -260,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
         }
         const uint32_t dst = land_s + (uint32_t)islot * kSlot;
 #pragma unroll
-        for (int i = 0; i < ((STMP_SH_SKIP & 2) ? 0 : 8); ++i)
+        for (int i = 0; i < 8; ++i)
           cp_async16_hint(dst + sw128_offset((uint32_t)(warp * 32 + 4 * i + q), (uint32_t)j),
                           rp[i] ? rp[i] + 64 * ic : a.R16, rp[i] ? 16u : 0u, row_policy);
         ++ig;
@@ -281,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
     for (int g = 0; g < total; ++g) {
       asm volatile("cp.async.wait_group %0;" ::"n"(NA - 2) : "memory");
       if (tid == 0) { SH_TR(0, g); }
-      if (STMP_SH_FENCE == 1) fence_proxy_async_smem();   // the tensor core reads the slot through the async proxy
+      fence_proxy_async_smem();   // the tensor core reads the slot through the async proxy
       mbar_arrive(&astaged[sa]);
       if (g >= 1) {
         if (ig < total) {
@@ -327,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
       tc_fence_after();
       const uint32_t taddr = tmem + lane_base + (uint32_t)acc * accs;
       int best = 0;
-      float bestv = -1.f, rawbest = 0.f, second = -1.f;
+      float bestv = -1.f, second = -1.f;
       if (et == 0) { SH_TRT(4, seq); }
       // corrected scores c . x - sum_k c_k P[S_k][child], first max of |score| in child
       // order (pursuit.py:151), 16 columns at a time
@@ -411,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
               for (int i = lane; i < nlines; i += 32) prefetch_l2(crow_x + 32 * i);
             }
           }
-          float nbv = -1.f, nraw = 0.f;
+          float nbv = -1.f;
           int nbest = 0;
           for (int h = 0; h < 2; ++h) {
             unsigned cand = h ? cm1 : cm0;
@@ -425,14 +412,12 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
               if (sj > nbv) {   // columns visited in increasing order: strict > keeps the first max
                 nbv = sj;
                 nbest = col;
-                nraw = raw;
               }
             }
           }
           if (lane == src) {
             bestv = nbv;
             best = nbest;
-            rawbest = nraw;
           }
         }
       }
@@ -451,7 +436,6 @@ __global__ void __launch_bounds__(kThreads, CPS) score_sh_kernel(ScoreArgs a, in
         if (a.path_out) a.path_out[((int64_t)p * a.K + a.count[p]) * a.L + a.level] = child;
         if (a.next_counts) atomicAdd(&s_hist[best], 1);
         if (last) a.leaf_sel[p] = leaf_info;
-        if (last && a.bsel) a.bsel[p] = rawbest;
         if (a.ip) add_ip(a.ip, p, cc + leaf_cnt, cc);
       }
       if (a.next_counts) {

@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, CPS) score_st_kernel(ScoreArgs a, in
       const int cb = __ldg(a.child_begin + gnode);
       const int cc = __ldg(a.child_count + gnode);
       int best = 0;
-      float bestv = -1.f, rawbest = 0.f;
+      float bestv = -1.f;
       const bool valid = tid < cur_rows && cur_p >= 0;
       const int p = cur_p;
       if (a.beam_keep > 0) {
@@ -445,10 +445,10 @@ __global__ void __launch_bounds__(kThreads, CPS) score_st_kernel(ScoreArgs a, in
         // Gram path: rows are x; score = c . x - sum_k c_k P[S_k][child] (gram_path.cu)
         float second = -1.f;
         corr_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * accs, off2, cc, a, valid ? p : -1,
-                        cb - a.corr_off, bestv, best, rawbest, second);
+                        cb - a.corr_off, bestv, best, second);
         if (a.cent != nullptr)
           recheck_near_ties(tmem + lane_base + kColAcc + (uint32_t)acc * accs, off2, cc, cb, a, valid ? p : -1,
-                            second, bestv, best, rawbest);
+                            second, bestv, best);
       } else {
         acc_abs_argmax(tmem + lane_base + kColAcc + (uint32_t)acc * accs, off2, (int)accw, npad, bestv, best);
       }
@@ -467,7 +467,6 @@ __global__ void __launch_bounds__(kThreads, CPS) score_st_kernel(ScoreArgs a, in
         if (a.path_out) a.path_out[((int64_t)p * a.K + a.count[p]) * a.L + a.level] = child;
         if (a.next_counts) atomicAdd(&s_hist[best], 1);
         if (last) a.leaf_sel[p] = leaf_info;
-        if (last && a.bsel) a.bsel[p] = rawbest;
         if (a.ip) add_ip(a.ip, p, cc + leaf_cnt, cc);
       }
       if (a.next_counts) {

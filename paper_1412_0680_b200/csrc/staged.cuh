@@ -47,7 +47,6 @@ struct ScoreArgs {
   int64_t sup_ld;        // K
   float* raw_out;        // root pass of iteration 0: raw scores c . x of all children -> [N][raw_w]
   int raw_w;
-  float* bsel;           // last level: raw score a . x of the winning leaf atom -> [N]
   // exact re-check of near ties: the tensor cores' truncating fp32 accumulation
   // leaves ~1e-6 ||x|| of error on c . x, so decisions whose top-2 corrected
   // scores are closer than recheck_rel * ||x|| are re-scored with FFMA dots
@@ -153,7 +152,6 @@ struct GramArgs {
   int64_t N;
   int K, L, iter;
   const int* leaf_sel;     // atom chosen by the last score pass
-  const float* bsel;       // its raw score a . x
   const float* gram;       // pair table of the last level = the Gram matrix in leaf order [m][m]
   int64_t gram_w;
   const int* leaf_pos;     // [m] column of each atom in the last-level table
