@@ -488,6 +488,21 @@ def main():
         rep = compare(gpu, ref, X_host[:done], check_path=False)
         parity = rep.as_dict()
         parity["reference"] = "f64 oracle (the cpu_baseline run) on the same prefix; near ties = top-2 gap < 1e-5"
+        if half:
+            # size-independent check over the whole batch: the fp16 row copies only pre-rank the
+            # children, so the encode must equal the one on f32 rows (half_scores = 0) patch for patch
+            _lib.set_option("half_scores", 0)
+            try:
+                ref32 = step()
+                torch.cuda.synchronize()
+            finally:
+                _lib.set_option("half_scores", 1)
+            parity["f32_rows_full_batch"] = {
+                "patches": N,
+                "patches_with_different_support": int((res.idx != ref32.idx).any(1).sum()),
+                "coef_bitwise_equal": bool(torch.equal(res.coef, ref32.coef)),
+                "resnorm_bitwise_equal": bool(torch.equal(res.resnorm, ref32.resnorm))}
+            del ref32
 
     line = {
         "metric": METRIC, "value": value, "unit": "patches/s", "n_gpus": world,
@@ -497,7 +512,12 @@ def main():
         "config": {"workload": workload, "patches_per_gpu": N, "dictionary": [cfg.m, cfg.n],
                    "branching": list(cfg.branching), "K": cfg.K, "method": args.method,
                    "parallelism": f"patch shards x{world}",
-                   "l2": f"inputs {N * cfg.n * 4 / 1e6:.0f} MB vs 126 MB L2 (no explicit flush)"},
+                   "l2": f"inputs {N * cfg.n * 4 / 1e6:.0f} MB vs 126 MB L2 (no explicit flush)",
+                   # every selection, coefficient and norm is an f32 result (3xTF32 / FFMA); where the
+                   # level passes read fp16 row copies they only pre-rank the children: decisions within
+                   # the copies' noise window are re-taken with exact f32 dots (same outputs as half_scores=0)
+                   "arithmetic": ("f32 results; level passes pre-rank on fp16 row copies with exact f32 re-checks"
+                                  if half else "f32 (3xTF32 tensor-core scores, FFMA updates)")},
         "roofline": roof,
         "cpu_baseline": cpu,
         "parity": parity,

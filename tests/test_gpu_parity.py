@@ -561,6 +561,33 @@ def test_gram_level_passes_fp16_rows_and_fp32_rows(cid, rows, half):
     assert rep.excused <= max(2, rows // 500)
 
 
+def test_fp16_and_fp32_rows_give_identical_outputs():
+    """The fp16 row copies only pre-rank the children (near ties are re-taken with
+    exact f32 dots on either path), so 16,384 config-4 patches must come out the
+    same with half_scores = 1 and 0: supports equal, coefficients and norms bitwise."""
+    from paper_1412_0680_b200 import _lib
+    from paper_1412_0680_b200 import workloads as W
+    cfg, wl, flat = config(4)
+    X = torch.as_tensor(W.make_patches(wl, 16384)).cuda()
+    sel = P().TreeSelector(flat, wl.atoms, cfg.alpha)
+    _lib.set_option("path", _lib.PATH_STAGED)
+    outs = []
+    try:
+        for half in (1, 0):
+            _lib.set_option("half_scores", half)
+            r = P().encode(sel, X, cfg.K, method="omp", paths=True)
+            torch.cuda.synchronize()
+            outs.append(r)
+    finally:
+        restore_defaults(_lib)
+    a, b = outs
+    differing = int((a.idx != b.idx).any(1).sum())
+    print(f"fp16 vs fp32 rows: {differing} of {len(X)} patches differ")
+    assert differing == 0
+    assert bool(torch.equal(a.coef, b.coef)) and bool(torch.equal(a.resnorm, b.resnorm))
+    assert bool(torch.equal(a.path, b.path)) and bool(torch.equal(a.ip, b.ip))
+
+
 def test_fp16_rows_follow_the_patch_scale():
     """The fp16 row copies carry one power-of-two scale per patch: patches scaled
     by 2^-60 .. 2^60 (exact in fp32, so the f64 oracle's results scale exactly too)
