@@ -588,6 +588,36 @@ def test_fp16_and_fp32_rows_give_identical_outputs():
     assert bool(torch.equal(a.path, b.path)) and bool(torch.equal(a.ip, b.ip))
 
 
+def test_fp16_rows_many_tiles_per_cta_and_ragged_batch():
+    """score_sh with more work items per CTA than its shared-memory item cache holds
+    (4,000,003 config-1 patches on the forced Gram path: ~110 tiles per CTA at level
+    1) and a batch that is not a multiple of the tile: outputs equal the f32-row path."""
+    from paper_1412_0680_b200 import _lib
+    from paper_1412_0680_b200 import workloads as W
+    cfg, wl, flat = config(1)
+    base = W.make_patches(wl, 1 << 18)
+    N = 4_000_003
+    X = torch.as_tensor(base).cuda().repeat(16, 1)[:N].contiguous()
+    X += 1e-3 * torch.randn(X.shape, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5))
+    sel = P().TreeSelector(flat, wl.atoms, cfg.alpha)
+    _lib.set_option("path", _lib.PATH_STAGED)
+    _lib.set_option("gram_path", 2)
+    outs = []
+    try:
+        for half in (1, 0):
+            _lib.set_option("half_scores", half)
+            (r, names) = launched(lambda: P().encode(sel, X, cfg.K, method="omp"))
+            assert any("score_sh_kernel" in k for k in names) == bool(half), sorted(names)
+            outs.append(r)
+    finally:
+        restore_defaults(_lib)
+    a, b = outs
+    differing = int((a.idx != b.idx).any(1).sum())
+    print(f"c1 gram, {N} patches, fp16 vs fp32 rows: {differing} patches differ")
+    assert differing == 0
+    assert bool(torch.equal(a.coef, b.coef)) and bool(torch.equal(a.count, b.count))
+
+
 def test_fp16_rows_follow_the_patch_scale():
     """The fp16 row copies carry one power-of-two scale per patch: patches scaled
     by 2^-60 .. 2^60 (exact in fp32, so the f64 oracle's results scale exactly too)
