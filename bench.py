@@ -412,6 +412,7 @@ def main():
     dom = max(fams, key=lambda f: fams[f]["ms"]) if fams else "other"
     gram = any("update_gram_kernel" in k for k in ktimes)
     half = any("score_sh_kernel" in k for k in ktimes)   # Gram-path level passes on fp16 rows
+    s16 = any("score_s16_kernel" in k for k in ktimes)   # residual-path passes with the 3xFP16 split
     staged_beam = any("beam_resolve_kernel" in k for k in ktimes)
     if dom == "fused":
         work = RL.fused_work(cfg, N, alpha, args.method)
@@ -441,6 +442,9 @@ def main():
                 # the scores are fp32-accurate 3xTF32 (three tf32 products per k-step): against the
                 # dense TF32 rate measured live in this run, divided by 3
                 "peak_3xtf32": tf32 / 3, "frac_3xtf32": achieved / (tf32 / 3) if tf32 else None,
+                # passes that ran the 3xFP16 split (score_s16.cu) spend three fp16 products per k-step:
+                # their ceiling is the dense 16-bit rate / 3
+                "peak_3xfp16": bf16 / 3 if s16 else None, "frac_3xfp16": achieved / (bf16 / 3) if s16 else None,
                 "hbm_frac": work["bytes"] / dom_launches / avg_s / 1e9 / hbm}
     roof.update({
         "kernel": f"{dom}: {', '.join(sorted(set(fams[dom]['kernels'])))}" if fams else "?",

@@ -174,8 +174,10 @@ int stmp_apply_operator(int32_t kind, const float* X, int64_t N, int32_t n_in, c
 /* Process-wide tuning knobs (no reference counterpart):
  *   "path": 0 auto (default), 1 fused warp-per-patch kernel, 2 staged tensor-core pipeline;
  *   "staged_min_batch": batch size from which `auto` picks the staged pipeline;
- *   "score_kernel": staged score pass 2 node table in shared memory where it fits (default),
- *                   3 streamed table at every level (always used where the table does not fit);
+ *   "score_kernel": staged score pass 2 node table in shared memory where it fits (default; where it
+ *                   does not, the streamed pass -- on nodes of > 128 children with the 3xFP16 split),
+ *                   3 streamed table, 3xTF32, at every level, 4 streamed table, 3xFP16 split, at every
+ *                   level of the residual pipeline;
  *   "update_kernel": staged OMP update 0 generic, 1 lockstep / wide-row (default);
  *   "gram_path": tree OMP without a residual in HBM, on per-tree pair tables of
  *                child-centroid . atom products (the Gram matrix at the last level;

@@ -436,8 +436,9 @@ int stmp_set_option(const char* key, int64_t value) {
     return STMP_OK;
   }
   if (strcmp(key, "score_kernel") == 0) {
-    if (value < 2 || value > 3)
-      return fail(STMP_EINVAL, "score_kernel must be 2 (node table in shared memory) or 3 (streamed table)");
+    if (value < 2 || value > 4)
+      return fail(STMP_EINVAL, "score_kernel must be 2 (node table in shared memory), 3 (streamed table) or "
+                               "4 (streamed table, 3xFP16 split)");
     stmp::g_score_ws = (int)value;
     return STMP_OK;
   }

@@ -137,6 +137,8 @@ struct TreeHandle {
   std::vector<int64_t> pair_width;
   int* leaf_pos = nullptr;
   bool pair_tried = false;
+  std::vector<uint8_t*> s16_tables;    // per level: [c_a | c_b] fp16 tables of the 3xFP16 pass (score_s16.cu), built on first use
+  bool s16_tried = false;
   std::vector<uint8_t*> half_tables;   // per level >= 1: fp16 piece tables (score_sh.cu), built with the pair tables
 };
 

@@ -18,6 +18,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "sm100.cuh"
@@ -388,7 +390,27 @@ bool build_staged_tables(TreeHandle* t, const int32_t* child_begin, const int32_
   return true;
 }
 
+bool ensure_s16_tables(TreeHandle* t, cudaStream_t st) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (t->s16_tried) return !t->s16_tables.empty();
+  t->s16_tried = true;
+  std::vector<uint8_t*> tabs(t->levels, nullptr);
+  bool good = true;
+  for (int l = 0; l < t->levels && good; ++l)
+    good = score_s16_fits(t->ld, t->staged_levels[l].npad) && (tabs[l] = build_s16_table(t, l, st)) != nullptr;
+  if (!good) {
+    for (uint8_t* p : tabs) cudaFree(p);
+    cudaGetLastError();
+    return false;
+  }
+  t->s16_tables = tabs;
+  return true;
+}
+
 void free_staged_tables(TreeHandle* t) {
+  for (uint8_t* p : t->s16_tables) cudaFree(p);
+  t->s16_tables.clear();
   for (float* p : t->staged_tables) cudaFree(p);
   t->staged_tables.clear();
   t->staged_levels.clear();
@@ -696,7 +718,15 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       }
       s.tmem_cols = lv.tmem_cols;
       const bool whole = score_smem_bytes(s.kchunks, lv.npad) <= 227 * 1024;
-      if (g_score_ws == 3 || !whole || !score_ts_fits(s.kchunks, lv.npad, l + 1 == L))
+      // streamed passes over wide nodes (> 128 children: config 2) are tensor-bound: 3xFP16 split by
+      // default (score_kernel = 3 keeps them on 3xTF32, 4 takes the 3xFP16 pass at every level)
+      const bool streamed = !whole || !score_ts_fits(s.kchunks, lv.npad, l + 1 == L);
+      const bool want16 = g_score_ws == 4 || (g_score_ws == 2 && streamed && lv.npad > 128);
+      if (want16 && score_s16_fits(d->ld, lv.npad) && ensure_s16_tables(const_cast<TreeHandle*>(t), st)) {
+        s.table_h = t->s16_tables[l];   // 3xFP16 split, rows scaled by the residual norm the update wrote
+        s.rnorm = resnorm;
+        e = launch_score_s16(s, sms, st);
+      } else if (g_score_ws == 3 || !whole || !score_ts_fits(s.kchunks, lv.npad, l + 1 == L))
         e = launch_score_st(s, sms, st);
       else
         e = launch_score_ts(s, sms, st);

@@ -62,6 +62,45 @@ __device__ __forceinline__ void acc_ld32x(uint32_t taddr, uint32_t off2, float s
     acc_ld32(taddr, off2, v);
 }
 
+// first max of |score| over the node's children (ties to the lowest child
+// position, pursuit.py:151), two passes as tmem_abs_argmax (sm100.cuh)
+__device__ __forceinline__ void acc_abs_argmax(uint32_t taddr, uint32_t off2, int ncols, int nvalid, float& bestv,
+                                               int& best) {
+  float m = -1.f;
+  int bc = 0;
+  for (int c0 = 0; c0 < ncols; c0 += 32) {
+    float v[32];
+    acc_ld32(taddr + (uint32_t)c0, off2, v);
+    if (c0 + 32 > nvalid) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = c0 + j < nvalid ? v[j] : 0.f;
+    }
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+      for (int j = 0; j < w; ++j) v[j] = fmaxf(fabsf(v[j]), fabsf(v[j + w]));
+    const float t = fabsf(v[0]);
+    if (t > m) {
+      m = t;
+      bc = c0;
+    }
+  }
+  // the TMEM address of tcgen05.ld must be warp-uniform: every lane walks every
+  // chunk and resolves the column inside its own winning chunk
+  int idx = 0;
+  for (int c0 = 0; c0 < ncols; c0 += 32) {
+    float v[32];
+    acc_ld32(taddr + (uint32_t)c0, off2, v);
+    if (c0 == bc) {
+      idx = 31;
+#pragma unroll
+      for (int j = 31; j >= 0; --j) idx = (c0 + j < nvalid && fabsf(v[j]) == m) ? j : idx;
+    }
+  }
+  bestv = m;
+  best = bc + idx;
+}
+
 // Epilogue of the Gram path (gram_path.cu): the accumulator holds c_v . x for
 // the node's cc children; subtract the support's contribution
 // sum_k c_k P[S_k][colbase + v] (the patch's current OMP support and

@@ -64,6 +64,8 @@ struct ScoreArgs {
   const float* inv_scale;   // 1 / s_p
   const float* qerr;        // ||x - x16 / s_p|| per patch
   float recheck_q;          // near-tie window += recheck_q * qerr
+  // 3xFP16 pass of the residual pipeline (score_s16.cu): table_h = [c_a | c_b] pieces of 2^8 c
+  const float* rnorm;       // ||r|| per patch (the resnorm output every update writes): the row scale
 
   // ---- staged beam descent (run_staged_beam): the pass scores (patch, node)
   // entries instead of patches; perm holds entry ids
@@ -250,6 +252,11 @@ cudaError_t launch_score_sh(const ScoreArgs& s, int sms, cudaStream_t st);
 __host__ __device__ inline uint32_t table_h_bytes(int kch64, int npad) { return (uint32_t)kch64 * 2u * npad * 128u; }
 // per-node fp16 piece tables of level l (nullptr on allocation failure)
 uint8_t* build_half_table(const TreeHandle* t, int l, cudaStream_t st);
+// 3xFP16 streamed pass of the residual pipeline (score_s16.cu, score_kernel = 4)
+bool score_s16_fits(int ld, int npad);
+cudaError_t launch_score_s16(const ScoreArgs& s, int sms, cudaStream_t st);
+uint8_t* build_s16_table(const TreeHandle* t, int l, cudaStream_t st);
+bool ensure_s16_tables(TreeHandle* t, cudaStream_t st);
 extern int g_half_scores;   // 1: Gram-path level passes read fp16 rows (default), 0: fp32 rows / 3xTF32
 cudaError_t launch_score_ts(const ScoreArgs& s, int sms, cudaStream_t st);
 bool staged_supported(const DictHandle* d, const TreeHandle* t, int K, int method);

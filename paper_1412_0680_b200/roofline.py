@@ -74,7 +74,7 @@ def model(cfg, N: int | None = None, method: str = "omp", exhaustive: bool = Fal
 # ---------------------------------------------------------------- per kernel family
 # Kernel families of one staged encode, by (mangled) kernel name.
 FAMILIES = (("corr", ("gram_corr_kernel",)),
-            ("score", ("score_ts_kernel", "score_st_kernel", "score_sh_kernel")),
+            ("score", ("score_ts_kernel", "score_st_kernel", "score_sh_kernel", "score_s16_kernel")),
             ("exact_scan", ("exact_scan_kernel",)),
             ("update", ("update_omp8_kernel", "update_wide_kernel", "update_gram_kernel", "update_kernel")),
             ("scatter", ("scatter_scan_kernel", "scatter_kernel", "scatter_root_kernel", "scan_kernel",

@@ -103,7 +103,7 @@ def test_argument_validation_maps_to_value_error(lib):
 def test_options_and_launch_counter(lib):
     before = _lib.kernel_launches()
     assert before >= 0
-    for key, bad in (("path", 3), ("score_kernel", 4), ("score_kernel", 1), ("update_kernel", 2),
+    for key, bad in (("path", 3), ("score_kernel", 5), ("score_kernel", 1), ("update_kernel", 2),
                      ("gram", 1), ("score_tma", 1), ("half_scores", 2), ("half_scores", -1)):
         with pytest.raises(ValueError):
             _lib.set_option(key, bad)

@@ -32,9 +32,10 @@ def P():
 # are (2, 1, 1).  Every id runs a distinct kernel set: the whole-table score pass
 # (score_ts) or the streamed one (score_st) at every level; the lockstep /
 # wide-row OMP update or the generic one; the Gram path (no residual, pair
-# tables; auto = config 4) forced on, or off.
+# tables; auto = config 4) forced on, or off; the streamed pass with the 3xFP16
+# split (score_s16) at every level of the residual pipeline.
 STAGED_KERNELS = {"staged-ts": (2, 1, 1), "staged-st": (3, 1, 1), "staged-generic": (2, 0, 0),
-                  "staged-resid": (2, 1, 0), "staged-gram": (2, 1, 2)}
+                  "staged-resid": (2, 1, 0), "staged-gram": (2, 1, 2), "staged-s16": (4, 1, 0)}
 PATHS = ["fused", *STAGED_KERNELS]
 
 
@@ -305,11 +306,12 @@ def _tree_cases():
     cases = [(0, 10_000, "omp"), (0, 10_000, "mp"), (1, 16_384, "omp"), (1, 4096, "mp"),
              (2, 16_384, "omp"), (3, 16_384, "omp"), (4, 512, "omp"), (4, 256, "mp")]
     # ids that would rerun the default kernels of a config are left out:
-    # configs 2 and 4 already stream every node table ("staged-st"); only config 4
+    # config 4 already streams every node table ("staged-st"; config 2 streams the 3xFP16
+    # pass by default, so "staged-st" is its 3xTF32 variant); only config 4
     # takes the Gram path by default ("staged-resid" elsewhere = "staged-ts"); config
     # 3's ragged last level has a centroid that is not its atom and config 4 is on
     # the Gram path already ("staged-gram"); the Gram path is OMP only.
-    skip = {("staged-st", 2), ("staged-st", 4), ("staged-resid", 0), ("staged-resid", 1), ("staged-resid", 2),
+    skip = {("staged-st", 4), ("staged-resid", 0), ("staged-resid", 1), ("staged-resid", 2),
             ("staged-resid", 3), ("staged-gram", 3), ("staged-gram", 4)}
     return [(c, r, m, p) for c, r, m in cases for p in PATHS
             if (p, c) not in skip and not (m == "mp" and p in ("staged-gram", "staged-resid"))]
@@ -341,6 +343,9 @@ def test_config_tree_parity(cid, rows, method, path):
     out, names = launched(lambda: run(sel, X, cfg.K, method))
     gram = any("update_gram_kernel" in k for k in names)
     assert gram == expects_gram(cid, method, path), sorted(names)
+    # the 3xFP16 pass: forced, or by default on config 2's streamed 256-child nodes
+    s16 = path == "staged-s16" or (cid == 2 and path in ("staged-ts", "staged-generic"))
+    assert any("score_s16_kernel" in k for k in names) == s16, sorted(names)
     rep = compare(out, ref, X)
     print(f"c{cid} {method} {path}: {rep.summary()}")
     assert rep.ok, rep.summary()

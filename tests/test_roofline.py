@@ -35,6 +35,7 @@ def test_kernel_families():
              "stmp::(anonymous namespace)::gram_corr_kernel(long, int const*)": "corr",
              "void stmp::(anonymous namespace)::update_gram_kernel<5, 2>(stmp::GramArgs)": "update",
              "void stmp::(anonymous namespace)::init_kernel<32, 13>(stmp::UpdateArgs)": "init",
+             "stmp::(anonymous namespace)::score_s16_kernel(stmp::ScoreArgs, int)": "score",
              "void stmp::(anonymous namespace)::scatter_scan_kernel<2>(long)": "scatter",
              "void stmp::(anonymous namespace)::exact_scan_kernel<4, 2>(stmp::ScoreArgs)": "exact_scan"}
     for name, fam in names.items():
