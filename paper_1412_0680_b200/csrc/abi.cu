@@ -261,6 +261,7 @@ void stmp_dict_free(stmp_dict* d) {
   purge_graphs(d->generation);
   cudaFree(d->atoms);
   cudaFree(d->xtable);
+  cudaFree(d->xtable16);
   delete d;
 }
 

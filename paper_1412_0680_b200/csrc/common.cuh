@@ -102,6 +102,8 @@ struct DictHandle {
   uint64_t generation = 0; // process-unique id (the graph cache keys on it, never on the address)
   float* xtable = nullptr; // tf32 hi/lo atom blocks for the exhaustive scan (built lazily)
   bool xtable_tried = false;
+  uint8_t* xtable16 = nullptr;  // fp16 piece atom blocks for the 3xFP16 exhaustive scan (built lazily)
+  bool xtable16_tried = false;
 };
 
 

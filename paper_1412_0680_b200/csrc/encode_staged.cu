@@ -663,6 +663,8 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
   }
   const float* xtable = t ? nullptr : ensure_xtable(const_cast<DictHandle*>(d), st);
   if (!t && xtable == nullptr) return cudaErrorMemoryAllocation;
+  // exhaustive scan with the 3xFP16 split (exact_scan.cu) unless score_kernel = 3 asks for 3xTF32
+  const uint8_t* xtable16 = (!t && g_score_ws != 3) ? ensure_xtable16(const_cast<DictHandle*>(d), st) : nullptr;
 
   for (int it = 0; it < K; ++it) {
     if (!t) {
@@ -679,6 +681,7 @@ cudaError_t run_staged(const DictHandle* d, const TreeHandle* t, const float* X,
       s.R = it == 0 ? R0 : R; s.ld = d->ld; s.nrows = N; s.perm = root_direct ? nullptr : perm; s.items = items;
       s.num_items = num_items; s.active = active;
       s.table = xtable; s.npad = xtable_block_width(d->ld); s.kchunks = d->ld / 32;
+      if (xtable16 != nullptr) { s.table_h = xtable16; s.rnorm = resnorm; }
       s.nblocks = (int)((d->m + s.npad - 1) / s.npad); s.m_atoms = (int)d->m;
       s.leaf_sel = leaf_sel; s.ip = ip; s.K = K; s.L = 0;
       s.ks_last = (d->n - 32 * (s.kchunks - 1) + 7) / 8;

@@ -15,8 +15,16 @@
 // 128 two accumulators alternate, so the fold of block j overlaps the MMAs of
 // block j + 1; BW = 256 (long rows, where a block's MMAs take tens of
 // microseconds) uses one.
+// F16 = true is the same scan with the 3xFP16 split of score_s16.cu (rows scaled
+// by a power of two from the residual norm and split into two fp16 pieces in
+// TMEM, atoms as two fp16 pieces of 2^8 a, 64-column chunks, three kind::f16
+// MMAs per 16-column k-step): the accuracy class of 3xTF32 at twice the tensor
+// rate and half the dictionary-table bytes; the running argmax is invariant
+// under the positive row scale.
 // Semantics: exact_select, pkg/src/stmp/pursuit.py:102-109 (np.argmax of |A r|:
 // the first maximum, i.e. the lowest atom index; counter += m).
+#include <cuda_fp16.h>
+
 #include <mutex>
 
 #include "common.cuh"
@@ -41,10 +49,10 @@ struct XsLayout {
   uint32_t land, btab, bars, slot, total;
 };
 
-__host__ __device__ inline XsLayout xs_layout(int bw, int na, int nb) {
+__host__ __device__ inline XsLayout xs_layout(int bw, int na, int nb, bool f16) {
   XsLayout L{};
   uint32_t o = 0;
-  L.land = o; o += (uint32_t)na * kSlot;
+  L.land = o; o += (uint32_t)na * kSlot * (f16 ? 2u : 1u);   // F16: 64-column chunks (two swizzled halves)
   L.btab = o; o += (uint32_t)nb * (uint32_t)bw * 256u;
   L.bars = o; o = L.bars + (uint32_t)(2 * nb + 2 * kNAB + 4) * 8;
   L.slot = o; o += 16;
@@ -52,7 +60,7 @@ __host__ __device__ inline XsLayout xs_layout(int bw, int na, int nb) {
   return L;
 }
 
-template <int NA, int NB>
+template <int NA, int NB, bool F16>
 __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, int nacc) {
   pdl_enter();
   extern __shared__ uint8_t smem_raw[];
@@ -65,7 +73,8 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
   const int kch = a.kchunks;
   const int nblk = a.nblocks;
   const int m = a.m_atoms;
-  const XsLayout Ly = xs_layout(bw, NA, NB);
+  const XsLayout Ly = xs_layout(bw, NA, NB, F16);
+  constexpr uint32_t kLand = kSlot * (F16 ? 2u : 1u);
   const uint32_t bslot = (uint32_t)bw * 256u;
   uint64_t* full = reinterpret_cast<uint64_t*>(base + Ly.bars);
   uint64_t* done = full + NB;
@@ -111,14 +120,14 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
         const int s = g % NB;
         if (g >= NB) mbar_wait(&done[s], (uint32_t)(g / NB - 1) & 1u);
         mbar_arrive_expect_tx(&full[s], bslot);
-        bulk_g2s(base + Ly.btab + s * bslot, reinterpret_cast<const uint8_t*>(a.table) + (size_t)bc * bslot, bslot,
-                 &full[s]);
+        bulk_g2s(base + Ly.btab + s * bslot,
+                 (F16 ? a.table_h : reinterpret_cast<const uint8_t*>(a.table)) + (size_t)bc * bslot, bslot, &full[s]);
       }
     }
   } else if (warp == 4) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = idesc_tf32(kT, bw);
+      const uint32_t idesc = F16 ? idesc_f16(kT, bw) : idesc_tf32(kT, bw);
       const uint32_t b_s = smem_u32(base + Ly.btab);
       for (int g = 0; g < total; ++g) {
         const int bs = g / kch, c = g - bs * kch;   // bs: block sequence number of this CTA
@@ -137,6 +146,12 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
           const uint32_t al = ah + 32;
           const uint32_t o = ks * 32u;
           if (c == kch - 1 && ks >= a.ks_last) break;   // zero padding on both operands
+          if (F16) {   // r_a.a_a + r_a.a_b + r_b.a_a: cells [0, 32) = r_a, [32, 64) = r_b; 16 columns per k-step
+            mma_f16_ts(dcol, ah, sw128_kmajor_desc(bh + o), idesc, (c | ks) ? 1u : 0u);
+            mma_f16_ts(dcol, ah, sw128_kmajor_desc(bl + o), idesc, 1u);
+            mma_f16_ts(dcol, al, sw128_kmajor_desc(bh + o), idesc, 1u);
+            continue;
+          }
           mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bh + o), idesc, (c | ks) ? 1u : 0u);
           mma_tf32_ts(dcol, ah, sw128_kmajor_desc(bl + o), idesc, 1u);
           mma_tf32_ts(dcol, al, sw128_kmajor_desc(bh + o), idesc, 1u);
@@ -165,14 +180,20 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
       if (g < total) {
         const int c = g % kch;
         const int rmine = row_of(i0 + g / per_item);
-        const uint32_t dst = land_s + (uint32_t)(g % NA) * kSlot;
         const int q = lane >> 3, j = lane & 7;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int rl = 4 * i + q;
-          const int r = __shfl_sync(kFull, rmine, rl);
-          const float* src = a.R + (r >= 0 ? (int64_t)r * a.ld + 32 * c + 4 * j : 0);
-          cp_async16(dst + sw128_offset((uint32_t)(warp * 32 + rl), (uint32_t)j), src, r >= 0 ? 16u : 0u);
+        for (int h = 0; h < (F16 ? 2 : 1); ++h) {
+          const uint32_t dst = land_s + (uint32_t)(g % NA) * kLand + (uint32_t)h * kSlot;
+          const int col0 = F16 ? 64 * c + 32 * h : 32 * c;
+          const bool cols = col0 < a.ld;   // F16: the padded row may end inside the 64-column chunk
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rl = 4 * i + q;
+            const int r = __shfl_sync(kFull, rmine, rl);
+            const bool on = r >= 0 && cols;
+            const float* src = a.R + (on ? (int64_t)r * a.ld + col0 + 4 * j : 0);
+            cp_async16(dst + sw128_offset((uint32_t)(warp * 32 + rl), (uint32_t)j), src, on ? 16u : 0u);
+          }
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
@@ -182,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
     bool valid = false;
     int best = 0;
     float bestv = -1.f;
+    float rscale = 1.f;   // F16: the row's power-of-two scale
     for (int g = 0; g < total; ++g) {
       const int item = i0 + g / per_item, rem = g % per_item;
       const int blk = rem / kch, c = rem - blk * kch;
@@ -195,6 +217,43 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
       }
       asm volatile("cp.async.wait_group %0;" ::"n"(NA - 1) : "memory");
       __syncwarp();
+      if (F16) {
+        if (rem == 0) {   // s = 2^(14 - e) for ||r|| = f 2^e: every |r_i| s stays below 2^14
+          int e = 0;
+          const float nrm = cur_p >= 0 ? __ldg(a.rnorm + cur_p) : 0.f;
+          if (nrm > 0.f && nrm < 3.0e38f) frexpf(nrm, &e);
+          rscale = ldexpf(1.f, max(-100, min(100, 14 - e)));
+        }
+        if (g >= kNAB) {
+          mbar_wait(&aempty[ab], (uint32_t)(g / kNAB - 1) & 1u);
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint8_t* slot = base + Ly.land + (uint32_t)(g % NA) * kLand + (uint32_t)h * kSlot;
+          uint32_t ca[16], cb[16];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 v = *reinterpret_cast<const float4*>(slot + sw128_offset(tid, j));
+            const __half2 a01 = __floats2half2_rn(v.x * rscale, v.y * rscale);
+            const __half2 a23 = __floats2half2_rn(v.z * rscale, v.w * rscale);
+            const float2 f01 = __half22float2(a01), f23 = __half22float2(a23);
+            const __half2 b01 = __floats2half2_rn(fmaf(v.x, rscale, -f01.x), fmaf(v.y, rscale, -f01.y));
+            const __half2 b23 = __floats2half2_rn(fmaf(v.z, rscale, -f23.x), fmaf(v.w, rscale, -f23.y));
+            ca[2 * j] = *reinterpret_cast<const uint32_t*>(&a01);
+            ca[2 * j + 1] = *reinterpret_cast<const uint32_t*>(&a23);
+            cb[2 * j] = *reinterpret_cast<const uint32_t*>(&b01);
+            cb[2 * j + 1] = *reinterpret_cast<const uint32_t*>(&b23);
+          }
+          tmem_st16(tmem + lane_base + (uint32_t)ab * 64u + 16u * h, ca);
+          tmem_st16(tmem + lane_base + (uint32_t)ab * 64u + 32u + 16u * h, cb);
+        }
+        __syncwarp();
+        issue_a(g + NA);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&astaged[ab]);
+      } else {
       float hi[32], lo[32];
       const uint8_t* slot = base + Ly.land + (uint32_t)(g % NA) * kSlot;
 #pragma unroll
@@ -218,6 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) exact_scan_kernel(ScoreArgs a, in
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&astaged[ab]);
+      }
       if (c != kch - 1) continue;
 
       // ---- fold this block's scores into the running argmax
@@ -268,19 +328,43 @@ __global__ void __launch_bounds__(256) xtable_kernel(const float* __restrict__ a
   }
 }
 
+// Dictionary -> [block][chunk of 64 columns][a_a | a_b][bw rows x 128 B] SW128 with 2^8 a = a_a + a_b
+// in fp16 pieces (rows past m and columns past ld zero).
+__global__ void __launch_bounds__(256) xtable16_kernel(const float* __restrict__ atoms, int64_t m, int ld, int bw,
+                                                       uint8_t* __restrict__ out) {
+  const int kch = (ld + 63) / 64;
+  const int blk = blockIdx.x / kch, kc = blockIdx.x - blk * kch;
+  uint8_t* plane = out + ((size_t)blockIdx.x) * bw * 256;
+  for (int e = threadIdx.x; e < bw * 64; e += blockDim.x) {
+    const int j = e >> 6, q = e & 63;
+    const int64_t atom = (int64_t)blk * bw + j;
+    const int col = kc * 64 + q;
+    const float val = atom < m && col < ld ? atoms[atom * ld + col] * 256.f : 0.f;
+    const __half p0 = __float2half_rn(val);
+    const __half p1 = __float2half_rn(val - __half2float(p0));
+    const uint32_t off = sw128_offset((uint32_t)j, (uint32_t)(q >> 3)) + (uint32_t)(q & 7) * 2u;
+    *reinterpret_cast<__half*>(plane + off) = p0;
+    *reinterpret_cast<__half*>(plane + (size_t)bw * 128 + off) = p1;
+  }
+}
+
 std::mutex g_xtable_mu;
 
-template <int NA, int NB>
+template <int NA, int NB, bool F16>
 cudaError_t launch_xs(ScoreArgs s, int sms, cudaStream_t st) {
-  const uint32_t smem = xs_layout(s.npad, NA, NB).total;
+  const uint32_t smem = xs_layout(s.npad, NA, NB, F16).total;
+  if (F16) {   // 64-column chunks, 16-column k-steps
+    s.kchunks = (s.ld + 63) / 64;
+    s.ks_last = (s.ld - 64 * (s.kchunks - 1) + 15) / 16;
+  }
   const int nacc = s.npad <= 128 ? 2 : 1;
   int cols = 32;
   while (cols < (int)kColAcc + nacc * s.npad) cols <<= 1;
   s.tmem_cols = cols;
-  cudaError_t e = cudaFuncSetAttribute(exact_scan_kernel<NA, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(exact_scan_kernel<NA, NB, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_kernel(exact_scan_kernel<NA, NB>, sms, kThreads, (size_t)smem, st, true, s, nacc);
+  return launch_kernel(exact_scan_kernel<NA, NB, F16>, sms, kThreads, (size_t)smem, st, true, s, nacc);
 }
 
 }  // namespace
@@ -308,10 +392,37 @@ const float* ensure_xtable(DictHandle* d, cudaStream_t st) {
   return tab;
 }
 
+const uint8_t* ensure_xtable16(DictHandle* d, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g_xtable_mu);
+  if (d->xtable16 != nullptr || d->xtable16_tried) return d->xtable16;
+  d->xtable16_tried = true;
+  const int bw = xtable_block_width(d->ld);
+  const int64_t nblk = (d->m + bw - 1) / bw;
+  const int kch = (d->ld + 63) / 64;
+  uint8_t* tab = nullptr;
+  if (cudaMalloc(&tab, (size_t)nblk * kch * bw * 256) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  xtable16_kernel<<<(unsigned)(nblk * kch), 256, 0, st>>>(d->atoms, d->m, d->ld, bw, tab);
+  note_launch();
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+    cudaFree(tab);
+    return nullptr;
+  }
+  d->xtable16 = tab;
+  return tab;
+}
+
 cudaError_t launch_exact_scan(const ScoreArgs& s, int sms, cudaStream_t st) {
   // 128-atom blocks: 16 KB + 16 KB per chunk slot pair; 256-atom blocks: 64 KB slots
-  if (s.npad == 128) return launch_xs<4, 3>(s, sms, st);
-  if (s.npad == 256) return launch_xs<4, 2>(s, sms, st);
+  if (s.table_h != nullptr && s.rnorm != nullptr) {   // 3xFP16 split (64-column chunks: 32 KB landing slots)
+    if (s.npad == 128) return launch_xs<2, 3, true>(s, sms, st);
+    if (s.npad == 256) return launch_xs<2, 2, true>(s, sms, st);
+    return cudaErrorNotSupported;
+  }
+  if (s.npad == 128) return launch_xs<4, 3, false>(s, sms, st);
+  if (s.npad == 256) return launch_xs<4, 2, false>(s, sms, st);
   return cudaErrorNotSupported;
 }
 

@@ -68,11 +68,6 @@ __host__ __device__ inline ShLayout sh_layout(int npad, int na, int nb) {
   return L;
 }
 
-// Instruction descriptor: kind::f16, fp16 A and B, f32 accumulate, both K-major.
-__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
-  return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
 // D[tmem] (+)= A[smem] * B[smem]^T, kind::f16, one CTA.
 __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                         uint32_t accumulate) {

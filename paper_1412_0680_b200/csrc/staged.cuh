@@ -240,6 +240,7 @@ bool score_ts_fits(int kchunks, int npad, bool last);
 // atoms; a.table = ensure_xtable(d), a.npad = block width, a.leaf_sel = best atom
 int xtable_block_width(int ld);
 const float* ensure_xtable(DictHandle* d, cudaStream_t st);
+const uint8_t* ensure_xtable16(DictHandle* d, cudaStream_t st);   // fp16 pieces, nullptr if it cannot be built
 cudaError_t launch_exact_scan(const ScoreArgs& s, int sms, cudaStream_t st);
 // streamed-table score pass (score_st.cu): any K, npad <= 256
 bool score_st_fits(int kchunks, int npad, bool last);

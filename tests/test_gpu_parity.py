@@ -371,13 +371,18 @@ def test_config0_golden_prefix():
         assert rep.ok, f"{tag}: {rep.summary()}"
 
 
-@pytest.mark.parametrize("path", ["fused", "staged-ts"], indirect=True)
+# "staged-ts": the scan with the 3xFP16 split (default); "staged-st" (score_kernel = 3): 3xTF32
+@pytest.mark.parametrize("path", ["fused", "staged-ts", "staged-st"], indirect=True)
 @pytest.mark.parametrize("cid,rows", [(1, 256), (1, 4096), (4, 8), (4, 300)])
 def test_config_exhaustive_parity(cid, rows, path):
     cfg, wl = dictionary(cid)
     X, ref = oracle_config(cid, rows, "omp", exhaustive=True)
     sel = P().ExactSelector(wl.atoms)
-    out = run(sel, X, cfg.K, "omp")
+    out, names = launched(lambda: run(sel, X, cfg.K, "omp"))
+    f16 = [k for k in names if "exact_scan_kernel" in k and ("Lb1E" in k or "true" in k)]   # <NA, NB, F16 = true>
+    if path != "fused":
+        assert any("exact_scan_kernel" in k for k in names), sorted(names)
+        assert bool(f16) == (path == "staged-ts"), sorted(names)
     rep = compare(out, ref, X, check_path=False)
     print(f"c{cid} exhaustive {path}: {rep.summary()}")
     assert rep.ok, rep.summary()
