@@ -412,7 +412,12 @@ def main():
     dom = max(fams, key=lambda f: fams[f]["ms"]) if fams else "other"
     gram = any("update_gram_kernel" in k for k in ktimes)
     half = any("score_sh_kernel" in k for k in ktimes)   # Gram-path level passes on fp16 rows
-    s16 = any("score_s16_kernel" in k for k in ktimes)   # residual-path passes with the 3xFP16 split
+    # tensor-core scores with the 3xFP16 split (score_s16.cu, exact_scan F16 mode): three fp16 products
+    # per k-step, so the tensor ceiling of the step model is the dense 16-bit rate / 3, not TF32 / 3
+    s16 = any("score_s16_kernel" in k or ("exact_scan_kernel" in k and ("Lb1E" in k or "true" in k))
+              for k in ktimes)
+    if s16 and not gram:
+        rm = RL.model(cfg, N=N, method=args.method, exhaustive=exhaustive, hbm_gbs=hbm, tensor_tflops=bf16 / 3)
     staged_beam = any("beam_resolve_kernel" in k for k in ktimes)
     if dom == "fused":
         work = RL.fused_work(cfg, N, alpha, args.method)
